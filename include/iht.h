@@ -1,0 +1,246 @@
+/*
+ * iht.h -- C ABI of libiht.so, the B200 (sm_100a) hot path of low-precision
+ * Iterative Hard Thresholding (arXiv 1802.04907, "Compressive Sensing with Low
+ * Precision Data Representation").
+ *
+ * Citations: P:L = PAPER.md line L (paper LaTeX source), S:L = SPEC.md line L.
+ * Readings of ambiguous passages (c1..c20) are listed in DESIGN.md.
+ *
+ * The method (Eq. modified_update_rule; Algorithm 1):
+ *     r     = y-hat - Phi-hat_F x                 forward residual
+ *     g     = Re( Phi-hat_A^H r )                 adjoint gradient
+ *     x    <- H_s( x + mu g )                     update + top-s
+ * with Phi-hat_A, Phi-hat_F two independent stochastic quantisations of Phi
+ * and y-hat = Q(y) quantised once.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ * - Every pointer named *_dev / device is CUDA device memory owned by the
+ *   caller (the Python binding allocates it through torch).  The library never
+ *   allocates in the per-iteration path; workspace sizes come from the
+ *   *_ws_bytes queries.  Host pointers are named *_host.
+ * - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   Every call only ENQUEUES work on that stream; nothing synchronises except
+ *   where stated (iht_quantize reads nothing back; iht_solver_run with
+ *   IHT_HOST_IO synchronises the stream before returning).
+ * - Return value: IHT_OK (0) or a negative IHT_E* code; iht_strerror() names it.
+ *   No exception crosses the ABI.  Argument errors are detected on the host
+ *   before anything is enqueued.
+ * - Stacked real rows: a complex matrix (planes = 2) is treated as the real
+ *   matrix [Re Phi; Im Phi] (re plane then im plane), so that
+ *   Re(Phi^H r) = Re(Phi)^T Re(r) + Im(Phi)^T Im(r)  (reading c13).
+ *   A length-R "stacked vector" (y-hat, r) holds plane p, row m at index
+ *   p * rows_pad + m, with rows_pad = iht_rows_pad(rows) (rows rounded up to a
+ *   multiple of 256); pad entries are 0.
+ * - Column strips: quantised codes of column n occupy strip_bytes bytes at
+ *   codes + n * strip_bytes; inside a strip, plane p starts at byte
+ *   p * rows_pad * bits / 8 and row m's b-bit code sits at bit m*bits of that
+ *   plane segment, little-endian, LSB first.  strip_bytes is a multiple of 32.
+ *   Codes of pad rows are 0.
+ */
+#ifndef IHT_H_
+#define IHT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IHT_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define IHT_API __attribute__((visibility("default")))
+#else
+#define IHT_API
+#endif
+
+enum {
+  IHT_OK = 0,
+  IHT_EINVAL = -1,       /* bad argument: dimension mismatch, bits not in {2,4,8},
+                            s > rows, misaligned pointer, workspace too small          */
+  IHT_EDOMAIN = -2,      /* non-finite input or non-finite x + mu g in H_s          */
+  IHT_ECUDA = -3,        /* a CUDA runtime call failed                                             */
+  IHT_ENCCL = -4,        /* NCCL could not be loaded or a collective failed                        */
+  IHT_ENOMEM = -5,       /* solver could not allocate its (one-time) workspace                     */
+  IHT_EUNSUPPORTED = -6  /* valid but not implemented configuration                                */
+};
+
+/* Name of a status code. Static storage; never NULL. */
+IHT_API const char* iht_strerror(int status);
+IHT_API int iht_abi_version(void);
+/* Text of the last CUDA error seen by this thread (after an IHT_ECUDA). */
+IHT_API const char* iht_last_cuda_error(void);
+
+/* ------------------------------------------------------------------ sizes */
+/* rows rounded up to a multiple of 256 (whole 32-byte sectors and adjoint k-steps). */
+IHT_API int64_t iht_rows_pad(int64_t rows);
+/* Bytes of one column strip: planes * iht_rows_pad(rows) * bits / 8.        */
+IHT_API int64_t iht_strip_bytes(int64_t rows, int planes, int bits);
+/* Bytes of one quantised copy: cols * iht_strip_bytes(rows, planes, bits).  */
+IHT_API int64_t iht_qmat_bytes(int64_t rows, int64_t cols, int planes, int bits);
+/* Length of a stacked vector (y-hat, r): planes * iht_rows_pad(rows).        */
+IHT_API int64_t iht_vec_len(int64_t rows, int planes);
+
+/* One quantised copy Phi-hat_k of (this shard of) Phi: 2^b-level (or odd,
+ * P:689) stochastic codes of Sec. 3 "Quantization" plus the global
+ * scale c (reading c3).  Dequantised entry: sigma * (2 code - (L-1)),
+ * sigma = scale_c / (L-1).  The struct is plain data; codes is caller-owned. */
+typedef struct {
+  int64_t rows;        /* logical rows of this shard (measurements / visibilities)   */
+  int64_t cols;        /* N, columns (unknowns / pixels)                             */
+  int64_t row_offset;  /* global index of this shard's first row (row sharding)      */
+  int32_t planes;      /* 1 = real, 2 = complex (re plane, im plane)                 */
+  int32_t bits;        /* b in {2, 4, 8}                                             */
+  int32_t level_mode;  /* 0: L = 2^b levels; 1: L = 2^{b-1}+1        */
+  int32_t copy_id;     /* Philox counter word 2: which independent copy      */
+  uint64_t seed;       /* Philox key                                                 */
+  float scale_c;       /* c = max |component| over the WHOLE Phi, all shards */
+  int32_t reserved;
+  int64_t strip_bytes; /* must equal iht_strip_bytes(rows, planes, bits)             */
+  void* codes;         /* device, cols * strip_bytes bytes                           */
+} iht_qmat;
+
+/* --------------------------------------------------------------- (a1) scale */
+/* c = max over `count` fp32 values of |src[i]| (complex data: pass 2x the
+ * element count; re and im are pooled, reading c3).  P:686 "c_v is the maximum
+ * value of the components of v in magnitude".  Writes one float to c_dev
+ * (device).  A NaN anywhere makes the result NaN (caller maps it to
+ * IHT_EDOMAIN).  Deterministic. */
+IHT_API int iht_absmax(const float* src_dev, int64_t count, float* c_dev, void* stream);
+
+/* ------------------------------------------------------- (a2) quantise Phi */
+/* Stochastically quantise the rows x cols block src (row-major, row stride ld
+ * ELEMENTS; complex = interleaved (re, im) pairs, ld in complex elements) into
+ * ncopies independent copies in one pass over src (one fp32 read emits every
+ * copy).  Sec. 3 "Quantization", fp32 Q-contract of DESIGN.md:
+ *   sf = fl32((L-1) / fl32(2c)); t = clamp(fl32(fl32(v + c) * sf), 0, L-1);
+ *   i = floor t; code = L-1 if i = L-1 else i + (u < t - i),
+ *   u = (w >> 8) 2^-24, w = Philox4x32-10 word (n & 3) of counter
+ *   (n >> 2, row_offset + m, copy_id, (plane << 8) | 0), key (lo32 seed, hi32 seed).
+ * dst[k] describes copy k (same rows/cols/planes/bits/level_mode/scale_c/
+ * row_offset for all k; own copy_id, seed, codes).  Errors: IHT_EINVAL on
+ * inconsistent descriptors. */
+IHT_API int iht_quantize(const float* src_dev, int64_t ld, const iht_qmat* dst, int ncopies,
+                 void* stream);
+/* Block-wise form (config 4's 64 GiB fp32 Phi is never resident): quantise only
+ * the local rows [row_begin, row_begin + nrows) of the copies dst[k]; src_dev
+ * points at local row row_begin.  row_begin must be a multiple of 256 and nrows
+ * too unless the block ends at dst->rows.  Codes are identical to a whole-matrix
+ * call because the Philox counters use global indices. */
+IHT_API int iht_quantize_rows(const float* src_dev, int64_t ld, const iht_qmat* dst, int ncopies,
+                              int64_t row_begin, int64_t nrows, void* stream);
+
+/* -------------------------------------------------------- (a3) quantise y */
+/* y-hat = Q_{b_y}(y) once (Alg. 1 input): element m of plane p draws
+ * word 0 of counter (0, row_offset + m, 0, (p << 8) | 1).  Writes the
+ * dequantised stacked vector yhat_dev (length iht_vec_len(rows, planes),
+ * pads 0) and, if codes_dev != NULL, the codes (uint8, planes * rows, plane
+ * major).  The scale c is read from the device (c_dev) so that the call can sit
+ * after iht_absmax / an all-reduce without a host round trip. */
+IHT_API int iht_quantize_vec(const float* y_dev, int64_t rows, int64_t row_offset, int planes, int bits,
+                     int level_mode, uint64_t seed, const float* c_dev, float* yhat_dev,
+                     uint8_t* codes_dev, void* stream);
+
+/* ------------------------------------------------------------ (a4) forward */
+/* r = y-hat - Phi-hat_F x for s-sparse real x ("matrix times a sparse
+ * vector ... scale-and-add"): only the x_nnz support columns of F
+ * are read.  x_idx_dev / x_val_dev: device arrays of length >= max_nnz;
+ * x_nnz_dev: device int32 (values < 0 are treated as 0).  yhat_dev and r_dev are
+ * stacked vectors of length iht_vec_len(F rows, planes). */
+IHT_API int64_t iht_forward_ws_bytes(const iht_qmat* F, int32_t max_nnz);
+IHT_API int iht_forward(const iht_qmat* F, const int32_t* x_idx_dev, const float* x_val_dev,
+                const int32_t* x_nnz_dev, int32_t max_nnz, const float* yhat_dev, float* r_dev,
+                void* ws_dev, int64_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------ (a5) adjoint */
+/* g = Re(Phi-hat_A^H r) for all N columns: g_n = sigma_A sum_m
+ * q_{m,n} r_m over the stacked rows; the whole copy is streamed once.  r_dev:
+ * stacked vector (pad entries must be 0); g_dev: N floats.  Deterministic (no
+ * float atomics).  `variant`: 0 = default (int8 tensor-core MMA path), 1 =
+ * CUDA-core FFMA path (kept as the measured baseline). */
+IHT_API int64_t iht_adjoint_ws_bytes(const iht_qmat* A);
+IHT_API int iht_adjoint(const iht_qmat* A, const float* r_dev, float* g_dev, int variant, void* ws_dev,
+                int64_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------- (a6) update + H_s */
+/* a = x + mu g, then H_s: keep the s entries of largest |a|,
+ * ties to the LOWEST index, zeros never kept (reading c15).  Output
+ * support strictly increasing in out_idx_dev[0..*out_nnz_dev) with
+ * values a_n.  Non-finite a sets *out_nnz_dev = -1 (IHT_EDOMAIN is reported by
+ * iht_solver_run).  Inputs x_* as in iht_forward; g_dev: N floats.  Output
+ * buffers must not alias the inputs. */
+IHT_API int64_t iht_threshold_ws_bytes(int64_t N, int32_t s);
+IHT_API int iht_threshold(const int32_t* x_idx_dev, const float* x_val_dev, const int32_t* x_nnz_dev,
+                  const float* g_dev, float mu, int32_t s, int64_t N, int32_t* out_idx_dev,
+                  float* out_val_dev, int32_t* out_nnz_dev, void* ws_dev, int64_t ws_bytes,
+                  void* stream);
+
+/* --------------------------------------------------------- multi-GPU comm */
+/* One NCCL communicator per rank (row-sharded Phi, north star).
+ * NCCL is loaded with dlopen at first use (libnccl.so.2; the copy torch has
+ * already loaded is reused).  Rank 0 calls iht_comm_unique_id, the 128 bytes
+ * are broadcast by the caller (torch.distributed), then every rank calls
+ * iht_comm_create.  Returns IHT_ENCCL when NCCL is unavailable. */
+typedef struct iht_comm iht_comm;
+IHT_API int iht_comm_unique_id(void* id_host_128);
+IHT_API int iht_comm_create(int rank, int world, const void* id_host_128, int device, iht_comm** out);
+IHT_API int iht_comm_destroy(iht_comm* comm);
+/* In-place sum / max all-reduce of `count` floats on the stream (test hook). */
+IHT_API int iht_comm_allreduce(iht_comm* comm, float* buf_dev, int64_t count, int op_max, void* stream);
+
+/* ------------------------------------------------------------ (b) solver */
+typedef struct {
+  int32_t s;            /* sparsity                                              */
+  int32_t n_iter;       /* n*                                                     */
+  float mu;             /* fixed step (reading c9)                                       */
+  int32_t b_y;          /* bits of y-hat                                                 */
+  int32_t level_mode;   /* as iht_qmat.level_mode, for y-hat                             */
+  int32_t adjoint_variant; /* iht_adjoint variant                                        */
+  uint64_t seed;        /* quantiser key for y-hat                                       */
+  int32_t trace;        /* 1: keep every iterate x^[n] (see iht_solver_trace)            */
+  int32_t use_graph;    /* 1: capture the n_iter loop into one CUDA graph (default)      */
+  iht_comm* comm;       /* NULL: single GPU; else g is all-reduced (sum) every iteration */
+} iht_config;
+
+/* Stateful solver over a pool of K quantised copies pool[0..K) (all with the
+ * same shape; K = 2 n* is Algorithm 1 exactly, smaller K reuses copies,
+ * reading c6): iteration n (1-based) uses pool[(2n-2) % K] for the adjoint
+ * (Phi-hat_{2n-1}) and pool[(2n-1) % K] for the forward (Phi-hat_{2n}).
+ * x^[1] = 0 (reading c8).  create allocates the one-time workspace (and,
+ * lazily, the CUDA graph); the pool's codes must outlive the solver. */
+typedef struct iht_solver iht_solver;
+IHT_API int iht_solver_create(const iht_qmat* pool, int K, const iht_config* cfg, iht_solver** out);
+IHT_API int iht_solver_destroy(iht_solver* solver);
+
+#define IHT_HOST_IO 1   /* y and the outputs are host pointers (pinned for async copies) */
+
+/* Run Algorithm 1 on this shard's observations y (fp32 rows values, complex
+ * interleaved; device or, with IHT_HOST_IO, host).  Steps: c_y = absmax(y)
+ * (all-reduced max across ranks), y-hat = Q(y), then n_iter iterations of
+ * forward -> adjoint -> [all-reduce g] -> update + H_s.  Writes the final
+ * support (<= s indices, increasing) and values, and *out_nnz (device or host
+ * per flags).  Returns IHT_EDOMAIN if a non-finite value reached H_s. */
+IHT_API int iht_solver_run(iht_solver* solver, const float* y, int flags, int32_t* out_idx,
+                   float* out_val, int32_t* out_nnz, void* stream);
+/* Copy the recorded iterates (cfg.trace = 1) of the last run to host arrays:
+ * idx_host/val_host of n_iter * s entries (row n-1 = x^[n+1] after iteration
+ * n), nnz_host of n_iter entries.  Synchronises the stream. */
+IHT_API int iht_solver_trace(iht_solver* solver, int32_t* idx_host, float* val_host, int32_t* nnz_host,
+                     void* stream);
+/* Device pointers of the internal stacked vectors of the LAST iteration
+ * (r, y-hat) and of g, for parity tests; lengths iht_vec_len(rows, planes) / N. */
+IHT_API int iht_solver_buffers(iht_solver* solver, const float** yhat_dev, const float** r_dev,
+                       const float** g_dev);
+/* Number of kernel launches one iht_solver_run enqueues (for gpu_launches). */
+IHT_API int64_t iht_solver_launches_per_run(const iht_solver* solver);
+
+/* One-shot convenience: create, run, destroy. */
+IHT_API int iht_solve(const iht_qmat* pool, int K, const iht_config* cfg, const float* y, int flags,
+              int32_t* out_idx, float* out_val, int32_t* out_nnz, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IHT_H_ */

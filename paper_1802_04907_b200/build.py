@@ -1,0 +1,98 @@
+"""Build libiht.so (and the workload generator libihtgen.so) in-tree with nvcc for sm_100a.
+
+    python -m paper_1802_04907_b200.build [--force]
+
+Every .cu is compiled with
+    -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
+and linked into a shared library next to this file (the .so travels to the GPU
+box with the gpurun snapshot; it is git-ignored).
+"""
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+INCLUDE = os.path.join(ROOT, "include")
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libiht.so")
+GEN_SRC = os.path.join(ROOT, "workloads", "csrc", "gen.cu")
+GEN_LIB = os.path.join(ROOT, "workloads", "libihtgen.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+         "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+
+
+def nvcc():
+    exe = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(exe):
+        raise RuntimeError("nvcc not found")
+    return exe
+
+
+def _sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+
+
+def _headers():
+    hs = [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
+    hs += [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    return hs
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(src, obj, verbose):
+    cmd = [nvcc(), *ARCH, *FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")
+    log = obj + ".ptxas.txt"
+    with open(log, "w") as f:
+        f.write(res.stderr)
+    if verbose:
+        print(f"[build] {os.path.basename(src)}", file=sys.stderr)
+    return obj
+
+
+def build(force=False, verbose=True):
+    """Compile libiht.so and libihtgen.so if any source is newer than the library."""
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = _sources()
+    hdrs = _headers()
+    objs = []
+    jobs = []
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        for s in srcs:
+            o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
+            objs.append(o)
+            if force or _stale(o, [s, *hdrs]):
+                jobs.append(ex.submit(_compile, s, o, verbose))
+        for j in jobs:
+            j.result()
+    if force or _stale(LIB, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
+        subprocess.run(cmd, check=True, capture_output=True, text=True)
+        if verbose:
+            print(f"[build] linked {LIB}", file=sys.stderr)
+    if force or _stale(GEN_LIB, [GEN_SRC]):
+        cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", GEN_SRC, "-o", GEN_LIB]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {GEN_SRC}:\n{res.stderr}")
+        if verbose:
+            print(f"[build] linked {GEN_LIB}", file=sys.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

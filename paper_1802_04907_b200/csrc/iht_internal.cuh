@@ -1,0 +1,77 @@
+// Internal helpers shared by the libiht kernels (sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "iht.h"
+
+#define IHT_CUDA_CHECK(expr)                                   \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) {                                   \
+      iht_set_last_cuda_error(_e, #expr, __FILE__, __LINE__);  \
+      return IHT_ECUDA;                                        \
+    }                                                          \
+  } while (0)
+
+#define IHT_LAUNCH_CHECK() IHT_CUDA_CHECK(cudaGetLastError())
+
+void iht_set_last_cuda_error(cudaError_t e, const char* expr, const char* file, int line);
+
+namespace iht {
+
+constexpr int kNumSMs = 148;  // B200; launch code queries the device, this is a default
+
+__host__ __device__ inline int num_levels(int bits, int level_mode) {
+  return level_mode == 0 ? (1 << bits) : ((1 << (bits - 1)) + 1);
+}
+
+// Universal row padding: a multiple of 256 rows, so that every plane segment is a whole
+// number of 32-byte sectors (256/b rows) and of adjoint k-steps (512/b rows) for b >= 2.
+__host__ __device__ inline int64_t rows_pad(int64_t rows) { return (rows + 255) / 256 * 256; }
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Counter-based RNG of the Q-contract (reading c4); own implementation.
+struct u32x4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = u32x4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Q-contract rounding of one fp32 component (no FMA contraction: _rn intrinsics).
+__device__ __forceinline__ uint32_t q_contract(float v, float c, float sf, int L, uint32_t w) {
+  float t = __fmul_rn(__fadd_rn(v, c), sf);
+  t = fminf(fmaxf(t, 0.0f), (float)(L - 1));
+  const int i = __float2int_rd(t);
+  if (i >= L - 1) return (uint32_t)(L - 1);
+  const float p = __fsub_rn(t, (float)i);
+  const float u = __fmul_rn(__uint2float_rn(w >> 8), 5.9604644775390625e-08f);  // 2^-24
+  return (uint32_t)i + (u < p ? 1u : 0u);
+}
+
+// sf = fl32(fl32(L-1) / fl32(2c)), 0 when c == 0.
+__device__ __forceinline__ float q_scale_factor(float c, int L) {
+  return c == 0.0f ? 0.0f : __fdiv_rn((float)(L - 1), __fmul_rn(2.0f, c));
+}
+
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+template <typename T>
+__host__ __device__ inline T ceil_div(T a, T b) {
+  return (a + b - 1) / b;
+}
+
+}  // namespace iht

@@ -1,0 +1,361 @@
+// (b) the solver: Algorithm 1 with fixed step mu over a pool of K
+// quantised copies, the n* iterations captured once into a CUDA graph; plus the
+// size queries, error strings and the NCCL communicator (row-sharded multi-GPU,
+// north star: "each GPU computes its partial g, and an NCCL all-reduce over NVLink
+// sums the length-N g, after which thresholding is replicated").
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>   // types and enum values only: NCCL itself is loaded with dlopen
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "iht_internal.cuh"
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_last_cuda_error[512];
+
+void iht_set_last_cuda_error(cudaError_t e, const char* expr, const char* file, int line) {
+  snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "%s (%s) at %s:%d: %s", cudaGetErrorName(e),
+           expr, file, line, cudaGetErrorString(e));
+}
+
+extern "C" const char* iht_last_cuda_error(void) { return g_last_cuda_error; }
+
+extern "C" const char* iht_strerror(int status) {
+  switch (status) {
+    case IHT_OK: return "IHT_OK";
+    case IHT_EINVAL: return "IHT_EINVAL: invalid argument";
+    case IHT_EDOMAIN: return "IHT_EDOMAIN: non-finite value";
+    case IHT_ECUDA: return "IHT_ECUDA: CUDA runtime error";
+    case IHT_ENCCL: return "IHT_ENCCL: NCCL unavailable or failed";
+    case IHT_ENOMEM: return "IHT_ENOMEM: out of device memory";
+    case IHT_EUNSUPPORTED: return "IHT_EUNSUPPORTED: configuration not implemented";
+    default: return "IHT_E?: unknown status";
+  }
+}
+
+extern "C" int iht_abi_version(void) { return IHT_ABI_VERSION; }
+
+// ------------------------------------------------------------------ sizes
+extern "C" int64_t iht_rows_pad(int64_t rows) { return rows <= 0 ? 0 : iht::rows_pad(rows); }
+extern "C" int64_t iht_strip_bytes(int64_t rows, int planes, int bits) {
+  if (rows <= 0 || (planes != 1 && planes != 2) || (bits != 2 && bits != 4 && bits != 8)) return -1;
+  return (int64_t)planes * iht::rows_pad(rows) * bits / 8;
+}
+extern "C" int64_t iht_qmat_bytes(int64_t rows, int64_t cols, int planes, int bits) {
+  const int64_t sb = iht_strip_bytes(rows, planes, bits);
+  return (sb < 0 || cols <= 0) ? -1 : sb * cols;
+}
+extern "C" int64_t iht_vec_len(int64_t rows, int planes) {
+  if (rows <= 0 || (planes != 1 && planes != 2)) return -1;
+  return (int64_t)planes * iht::rows_pad(rows);
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+bool load_nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);  // torch's copy if loaded
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce;
+  return g_nccl.ok;
+}
+}  // namespace
+
+struct iht_comm {
+  ncclComm_t comm;
+  int rank, world;
+};
+
+extern "C" int iht_comm_unique_id(void* id128) {
+  if (id128 == nullptr) return IHT_EINVAL;
+  if (!load_nccl()) return IHT_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return IHT_ENCCL;
+  memcpy(id128, &id, sizeof(id));
+  return IHT_OK;
+}
+
+extern "C" int iht_comm_create(int rank, int world, const void* id128, int device, iht_comm** out) {
+  if (out == nullptr || id128 == nullptr || world < 1 || rank < 0 || rank >= world) return IHT_EINVAL;
+  if (!load_nccl()) return IHT_ENCCL;
+  IHT_CUDA_CHECK(cudaSetDevice(device));
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclComm_t c;
+  if (g_nccl.CommInitRank(&c, world, id, rank) != ncclSuccess) return IHT_ENCCL;
+  *out = new iht_comm{c, rank, world};
+  return IHT_OK;
+}
+
+extern "C" int iht_comm_destroy(iht_comm* comm) {
+  if (comm == nullptr) return IHT_OK;
+  if (g_nccl.ok) g_nccl.CommDestroy(comm->comm);
+  delete comm;
+  return IHT_OK;
+}
+
+extern "C" int iht_comm_allreduce(iht_comm* comm, float* buf, int64_t count, int op_max, void* stream) {
+  if (comm == nullptr || buf == nullptr || count < 0) return IHT_EINVAL;
+  if (g_nccl.AllReduce(buf, buf, (size_t)count, ncclFloat32, op_max ? ncclMax : ncclSum, comm->comm,
+                       (cudaStream_t)stream) != ncclSuccess)
+    return IHT_ENCCL;
+  return IHT_OK;
+}
+
+// ------------------------------------------------------------------ solver
+struct iht_solver {
+  std::vector<iht_qmat> pool;
+  iht_config cfg;
+  int64_t rows, N, vlen;
+  int planes;
+  // device buffers (one allocation)
+  void* block = nullptr;
+  float *y = nullptr, *c_y = nullptr, *yhat = nullptr, *r = nullptr, *g = nullptr;
+  void *ws_adj = nullptr, *ws_thr = nullptr;
+  int64_t ws_adj_bytes = 0, ws_thr_bytes = 0;
+  int32_t* xs_idx = nullptr;   // [nslots][s]
+  float* xs_val = nullptr;     // [nslots][s]
+  int32_t* xs_nnz = nullptr;   // [nslots]
+  int nslots = 0;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+  int final_slot = 0;
+};
+
+static int slot_of(const iht_solver* S, int n) {   // slot holding x^[n+1] after iteration n
+  return S->cfg.trace ? n : (n & 1);
+}
+
+// Enqueue one complete run (absmax .. last threshold) on stream st; counts launches.
+static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
+  int64_t L = 0;
+  int rc;
+  const int64_t ycount = S->rows * S->planes;
+  if ((rc = iht_absmax(S->y, ycount, S->c_y, st)) != IHT_OK) return rc;
+  L += 1;
+  if (S->cfg.comm && S->cfg.comm->world > 1) {
+    if ((rc = iht_comm_allreduce(S->cfg.comm, S->c_y, 1, 1, st)) != IHT_OK) return rc;
+  }
+  const iht_qmat& q0 = S->pool[0];
+  if ((rc = iht_quantize_vec(S->y, S->rows, q0.row_offset, S->planes, S->cfg.b_y, S->cfg.level_mode,
+                             S->cfg.seed, S->c_y, S->yhat, nullptr, st)) != IHT_OK)
+    return rc;
+  L += 1;
+  // x^[1] = 0 (reading c8): the "slot -1" is represented by slot_of(n=0)
+  const int s0 = S->cfg.trace ? 0 : 0;
+  IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz + s0, 0, sizeof(int32_t), st));
+  const int K = (int)S->pool.size();
+  const int s = S->cfg.s;
+  for (int n = 1; n <= S->cfg.n_iter; ++n) {
+    const int in_slot = S->cfg.trace ? (n - 1) : ((n - 1) & 1);
+    const int out_slot = S->cfg.trace ? n : (n & 1);
+    const iht_qmat& A = S->pool[(2 * n - 2) % K];   // Phi-hat_{2n-1} (1-based), adjoint
+    const iht_qmat& F = S->pool[(2 * n - 1) % K];   // Phi-hat_{2n}, forward
+    if ((rc = iht_forward(&F, S->xs_idx + (int64_t)in_slot * s, S->xs_val + (int64_t)in_slot * s,
+                          S->xs_nnz + in_slot, s, S->yhat, S->r, nullptr, 0, st)) != IHT_OK)
+      return rc;
+    L += 1;
+    if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
+      return rc;
+    L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
+    if (S->cfg.comm && S->cfg.comm->world > 1) {
+      if ((rc = iht_comm_allreduce(S->cfg.comm, S->g, S->N, 0, st)) != IHT_OK) return rc;
+    }
+    if ((rc = iht_threshold(S->xs_idx + (int64_t)in_slot * s, S->xs_val + (int64_t)in_slot * s,
+                            S->xs_nnz + in_slot, S->g, S->cfg.mu, s, S->N,
+                            S->xs_idx + (int64_t)out_slot * s, S->xs_val + (int64_t)out_slot * s,
+                            S->xs_nnz + out_slot, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+      return rc;
+    L += 1;
+    S->final_slot = out_slot;
+  }
+  if (S->cfg.n_iter == 0) S->final_slot = 0;
+  if (launches) *launches = L;
+  return IHT_OK;
+}
+
+extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* cfg, iht_solver** out) {
+  if (pool == nullptr || K < 1 || cfg == nullptr || out == nullptr) return IHT_EINVAL;
+  if (cfg->s < 0 || cfg->n_iter < 0 || !isfinite(cfg->mu)) return IHT_EINVAL;
+  if (cfg->b_y < 2 || cfg->b_y > 8 || (cfg->level_mode != 0 && cfg->level_mode != 1)) return IHT_EINVAL;
+  if (cfg->adjoint_variant != 0 && cfg->adjoint_variant != 1) return IHT_EINVAL;
+  const iht_qmat& q0 = pool[0];
+  for (int k = 0; k < K; ++k) {
+    const iht_qmat& q = pool[k];
+    if (q.codes == nullptr || q.rows != q0.rows || q.cols != q0.cols || q.planes != q0.planes ||
+        q.bits != q0.bits || q.row_offset != q0.row_offset ||
+        q.strip_bytes != iht_strip_bytes(q.rows, q.planes, q.bits))
+      return IHT_EINVAL;
+  }
+  if (cfg->s > q0.rows * (cfg->comm ? cfg->comm->world : 1) * q0.planes || cfg->s > q0.cols)
+    return IHT_EINVAL;  // s <= M
+  iht_solver* S = new iht_solver();
+  S->pool.assign(pool, pool + K);
+  S->cfg = *cfg;
+  S->rows = q0.rows;
+  S->N = q0.cols;
+  S->planes = q0.planes;
+  S->vlen = iht_vec_len(q0.rows, q0.planes);
+  S->ws_adj_bytes = iht_adjoint_ws_bytes(&q0);
+  S->ws_thr_bytes = iht_threshold_ws_bytes(S->N, cfg->s);
+  S->nslots = cfg->trace ? cfg->n_iter + 1 : 2;
+  const int s = cfg->s > 0 ? cfg->s : 1;
+  auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+  const int64_t ycount = q0.rows * q0.planes;
+  const int64_t sz_y = al(ycount * 4), sz_c = al(4), sz_v = al(S->vlen * 4), sz_g = al(S->N * 4),
+                sz_wa = al(S->ws_adj_bytes), sz_wt = al(S->ws_thr_bytes),
+                sz_xi = al((int64_t)S->nslots * s * 4), sz_xv = al((int64_t)S->nslots * s * 4),
+                sz_xn = al((int64_t)S->nslots * 4);
+  const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_xi + sz_xv + sz_xn;
+  if (cudaMalloc(&S->block, total) != cudaSuccess) {
+    delete S;
+    return IHT_ENOMEM;
+  }
+  char* p = static_cast<char*>(S->block);
+  S->y = reinterpret_cast<float*>(p); p += sz_y;
+  S->c_y = reinterpret_cast<float*>(p); p += sz_c;
+  S->yhat = reinterpret_cast<float*>(p); p += sz_v;
+  S->r = reinterpret_cast<float*>(p); p += sz_v;
+  S->g = reinterpret_cast<float*>(p); p += sz_g;
+  S->ws_adj = S->ws_adj_bytes ? p : nullptr; p += sz_wa;
+  S->ws_thr = p; p += sz_wt;
+  S->xs_idx = reinterpret_cast<int32_t*>(p); p += sz_xi;
+  S->xs_val = reinterpret_cast<float*>(p); p += sz_xv;
+  S->xs_nnz = reinterpret_cast<int32_t*>(p); p += sz_xn;
+  if (cudaMemset(S->block, 0, total) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&S->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaFree(S->block);
+    delete S;
+    return IHT_ECUDA;
+  }
+  *out = S;
+  return IHT_OK;
+}
+
+extern "C" int iht_solver_destroy(iht_solver* S) {
+  if (S == nullptr) return IHT_OK;
+  if (S->exec) cudaGraphExecDestroy(S->exec);
+  if (S->cap_stream) cudaStreamDestroy(S->cap_stream);
+  if (S->block) cudaFree(S->block);
+  delete S;
+  return IHT_OK;
+}
+
+static int ensure_graph(iht_solver* S) {
+  if (S->exec) return IHT_OK;
+  cudaGraph_t graph;
+  IHT_CUDA_CHECK(cudaStreamBeginCapture(S->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int64_t L = 0;
+  const int rc = enqueue_run(S, S->cap_stream, &L);
+  cudaGraph_t g2;
+  const cudaError_t e = cudaStreamEndCapture(S->cap_stream, &g2);
+  if (rc != IHT_OK) {
+    if (e == cudaSuccess) cudaGraphDestroy(g2);
+    return rc;
+  }
+  IHT_CUDA_CHECK(e);
+  graph = g2;
+  const cudaError_t ei = cudaGraphInstantiate(&S->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  IHT_CUDA_CHECK(ei);
+  S->launches = L;
+  return IHT_OK;
+}
+
+extern "C" int iht_solver_run(iht_solver* S, const float* y, int flags, int32_t* out_idx, float* out_val,
+                              int32_t* out_nnz, void* stream) {
+  if (S == nullptr || y == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr)
+    return IHT_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool host = (flags & IHT_HOST_IO) != 0;
+  const int64_t ycount = S->rows * S->planes;
+  IHT_CUDA_CHECK(cudaMemcpyAsync(S->y, y, ycount * sizeof(float),
+                                 host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+  int rc;
+  if (S->cfg.use_graph) {
+    if ((rc = ensure_graph(S)) != IHT_OK) return rc;
+    IHT_CUDA_CHECK(cudaGraphLaunch(S->exec, st));
+  } else {
+    int64_t L = 0;
+    if ((rc = enqueue_run(S, st, &L)) != IHT_OK) return rc;
+    S->launches = L;
+  }
+  const int s = S->cfg.s;
+  const int fs = S->final_slot;
+  const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (s > 0) {
+    IHT_CUDA_CHECK(cudaMemcpyAsync(out_idx, S->xs_idx + (int64_t)fs * s, s * sizeof(int32_t), kind, st));
+    IHT_CUDA_CHECK(cudaMemcpyAsync(out_val, S->xs_val + (int64_t)fs * s, s * sizeof(float), kind, st));
+  }
+  IHT_CUDA_CHECK(cudaMemcpyAsync(out_nnz, S->xs_nnz + fs, sizeof(int32_t), kind, st));
+  if (host) {
+    IHT_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (*out_nnz < 0) return IHT_EDOMAIN;
+  }
+  return IHT_OK;
+}
+
+extern "C" int iht_solver_trace(iht_solver* S, int32_t* idx_host, float* val_host, int32_t* nnz_host,
+                                void* stream) {
+  if (S == nullptr || !S->cfg.trace) return IHT_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int s = S->cfg.s, n = S->cfg.n_iter;
+  if (n == 0) return IHT_OK;
+  if (s > 0) {
+    IHT_CUDA_CHECK(cudaMemcpyAsync(idx_host, S->xs_idx + s, (size_t)n * s * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, st));
+    IHT_CUDA_CHECK(cudaMemcpyAsync(val_host, S->xs_val + s, (size_t)n * s * sizeof(float),
+                                   cudaMemcpyDeviceToHost, st));
+  }
+  IHT_CUDA_CHECK(cudaMemcpyAsync(nnz_host, S->xs_nnz + 1, (size_t)n * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, st));
+  IHT_CUDA_CHECK(cudaStreamSynchronize(st));
+  return IHT_OK;
+}
+
+extern "C" int iht_solver_buffers(iht_solver* S, const float** yhat, const float** r, const float** g) {
+  if (S == nullptr) return IHT_EINVAL;
+  if (yhat) *yhat = S->yhat;
+  if (r) *r = S->r;
+  if (g) *g = S->g;
+  return IHT_OK;
+}
+
+extern "C" int64_t iht_solver_launches_per_run(const iht_solver* S) { return S ? S->launches : -1; }
+
+extern "C" int iht_solve(const iht_qmat* pool, int K, const iht_config* cfg, const float* y, int flags,
+                         int32_t* out_idx, float* out_val, int32_t* out_nnz, void* stream) {
+  iht_solver* S = nullptr;
+  int rc = iht_solver_create(pool, K, cfg, &S);
+  if (rc != IHT_OK) return rc;
+  rc = iht_solver_run(S, y, flags, out_idx, out_val, out_nnz, stream);
+  if (rc == IHT_OK) {
+    const cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) rc = IHT_ECUDA;
+  }
+  iht_solver_destroy(S);
+  return rc;
+}

@@ -1,0 +1,286 @@
+"""Python binding of libiht.so with the C ABI's names (argument marshalling only).
+
+Every step of the hot path runs in the library's CUDA kernels; torch supplies
+device memory (tensors), the current CUDA stream and process groups.  Functions
+mirror include/iht.h:
+
+    absmax, quantize, quantize_vec, forward, adjoint, threshold,   (a1)-(a6)
+    Solver / solve (iht_solver_*), Comm (iht_comm_*).
+"""
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import IhtConfig, IhtQmat, check, load
+
+__all__ = ["absmax", "quantize", "quantize_rows", "quantize_vec", "forward", "adjoint", "threshold", "Solver", "solve",
+           "Comm", "QCopy", "strip_bytes", "vec_len", "rows_pad"]
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libiht compute calls take CUDA tensors (no CPU path)")
+
+
+def rows_pad(rows):
+    return load().iht_rows_pad(rows)
+
+
+def strip_bytes(rows, planes, bits):
+    v = load().iht_strip_bytes(rows, planes, bits)
+    if v < 0:
+        raise ValueError("invalid (rows, planes, bits)")
+    return v
+
+
+def vec_len(rows, planes):
+    return load().iht_vec_len(rows, planes)
+
+
+@dataclass
+class QCopy:
+    """One quantised copy Phi-hat_k: descriptor + the torch uint8 tensor owning the codes."""
+    desc: IhtQmat
+    codes: torch.Tensor
+
+    @property
+    def rows(self):
+        return self.desc.rows
+
+    @property
+    def cols(self):
+        return self.desc.cols
+
+    @property
+    def planes(self):
+        return self.desc.planes
+
+    @property
+    def bits(self):
+        return self.desc.bits
+
+    @property
+    def scale_c(self):
+        return self.desc.scale_c
+
+
+def new_copy(rows, cols, planes, bits, level_mode, seed, copy_id, scale_c, row_offset=0, device=None,
+             codes=None):
+    sb = strip_bytes(rows, planes, bits)
+    if codes is None:
+        codes = torch.empty(cols * sb, dtype=torch.uint8, device=device or "cuda")
+    d = IhtQmat(rows=rows, cols=cols, row_offset=row_offset, planes=planes, bits=bits, level_mode=level_mode,
+                copy_id=copy_id, seed=seed, scale_c=float(scale_c), reserved=0, strip_bytes=sb,
+                codes=codes.data_ptr())
+    return QCopy(d, codes)
+
+
+def absmax(src, stream=None):
+    """(a1) c = max |src| (float32 / complex64 viewed as pairs); returns a 1-element CUDA tensor."""
+    _require_cuda(src)
+    flat = torch.view_as_real(src) if src.is_complex() else src
+    if not flat.is_contiguous():
+        raise ValueError("absmax needs a contiguous tensor")
+    out = torch.empty(1, dtype=torch.float32, device=src.device)
+    check(load().iht_absmax(_ptr(flat), flat.numel(), _ptr(out), _stream(stream)), "iht_absmax")
+    return out
+
+
+def quantize(phi, bits, level_mode, seed, copy_ids, scale_c, row_offset=0, stream=None):
+    """(a2) quantise a (rows x cols) float32 or complex64 CUDA matrix into len(copy_ids)
+    independent copies in one pass; returns a list of QCopy."""
+    _require_cuda(phi)
+    planes = 2 if phi.is_complex() else 1
+    rows, cols = phi.shape
+    if phi.stride(1) != 1:
+        raise ValueError("phi must be row-major (unit column stride)")
+    copies = [new_copy(rows, cols, planes, bits, level_mode, seed, cid, scale_c, row_offset, phi.device)
+              for cid in copy_ids]
+    arr = (IhtQmat * len(copies))(*[c.desc for c in copies])
+    base = torch.view_as_real(phi) if planes == 2 else phi
+    check(load().iht_quantize(_ptr(base), phi.stride(0), arr, len(copies), _stream(stream)), "iht_quantize")
+    return copies
+
+
+def quantize_rows(block, copies, row_begin, stream=None):
+    """(a2) block-wise: quantise local rows [row_begin, row_begin + block.shape[0]) of existing
+    copies (QCopy list sharing shape) from the CUDA block `block` (float32 / complex64)."""
+    _require_cuda(block)
+    arr = (IhtQmat * len(copies))(*[c.desc for c in copies])
+    base = torch.view_as_real(block) if block.is_complex() else block
+    check(load().iht_quantize_rows(_ptr(base), block.stride(0), arr, len(copies), row_begin, block.shape[0],
+                                   _stream(stream)), "iht_quantize_rows")
+    return copies
+
+
+def quantize_vec(y, bits, level_mode, seed, c_dev, row_offset=0, with_codes=False, stream=None):
+    """(a3) y-hat = Q(y) once; returns (yhat stacked float32, codes uint8 or None)."""
+    _require_cuda(y, c_dev)
+    planes = 2 if y.is_complex() else 1
+    rows = y.shape[0]
+    base = torch.view_as_real(y).contiguous() if planes == 2 else y.contiguous()
+    yhat = torch.empty(vec_len(rows, planes), dtype=torch.float32, device=y.device)
+    codes = torch.empty(planes * rows, dtype=torch.uint8, device=y.device) if with_codes else None
+    check(load().iht_quantize_vec(_ptr(base), rows, row_offset, planes, bits, level_mode, seed, _ptr(c_dev),
+                                  _ptr(yhat), _ptr(codes), _stream(stream)), "iht_quantize_vec")
+    return yhat, codes
+
+
+def forward(F, x_idx, x_val, x_nnz, yhat, max_nnz=None, stream=None):
+    """(a4) r = y-hat - Phi-hat_F x (support columns only); x_nnz is a 1-element int32 CUDA tensor."""
+    _require_cuda(x_idx, x_val, x_nnz, yhat)
+    max_nnz = x_idx.numel() if max_nnz is None else max_nnz
+    r = torch.empty_like(yhat)
+    check(load().iht_forward(ctypes.byref(F.desc), _ptr(x_idx), _ptr(x_val), _ptr(x_nnz), max_nnz, _ptr(yhat),
+                             _ptr(r), None, 0, _stream(stream)), "iht_forward")
+    return r
+
+
+def adjoint(A, r, variant=0, stream=None, out=None):
+    """(a5) g = Re(Phi-hat_A^H r) for all N columns (variant 0 = int8 MMA, 1 = FFMA)."""
+    _require_cuda(r)
+    lib = load()
+    ws_bytes = lib.iht_adjoint_ws_bytes(ctypes.byref(A.desc))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=r.device)
+    g = torch.empty(A.cols, dtype=torch.float32, device=r.device) if out is None else out
+    check(lib.iht_adjoint(ctypes.byref(A.desc), _ptr(r), _ptr(g), variant, _ptr(ws), ws_bytes, _stream(stream)),
+          "iht_adjoint")
+    return g
+
+
+def threshold(x_idx, x_val, x_nnz, g, mu, s, stream=None):
+    """(a6) x <- H_s(x + mu g): returns (idx int32[s], val float32[s], nnz int32[1]) on the device."""
+    _require_cuda(x_idx, x_val, x_nnz, g)
+    lib = load()
+    N = g.numel()
+    ws_bytes = lib.iht_threshold_ws_bytes(N, s)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=g.device)
+    oi = torch.empty(max(s, 1), dtype=torch.int32, device=g.device)
+    ov = torch.empty(max(s, 1), dtype=torch.float32, device=g.device)
+    on = torch.empty(1, dtype=torch.int32, device=g.device)
+    check(lib.iht_threshold(_ptr(x_idx), _ptr(x_val), _ptr(x_nnz), _ptr(g), float(mu), s, N, _ptr(oi), _ptr(ov),
+                            _ptr(on), _ptr(ws), ws_bytes, _stream(stream)), "iht_threshold")
+    return oi, ov, on
+
+
+class Comm:
+    """NCCL communicator of libiht (iht_comm_*); unique id broadcast via torch.distributed."""
+
+    def __init__(self, rank, world, device, group=None):
+        import torch.distributed as dist
+        lib = load()
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            check(lib.iht_comm_unique_id(ctypes.cast(uid, ctypes.c_void_p)), "iht_comm_unique_id")
+        if world > 1:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            ctypes.memmove(uid, obj[0], 128)
+        h = ctypes.c_void_p()
+        check(lib.iht_comm_create(rank, world, ctypes.cast(uid, ctypes.c_void_p), device, ctypes.byref(h)),
+              "iht_comm_create")
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def allreduce_(self, t, op_max=False, stream=None):
+        check(load().iht_comm_allreduce(self.handle, _ptr(t), t.numel(), int(op_max), _stream(stream)),
+              "iht_comm_allreduce")
+        return t
+
+    def close(self):
+        if self.handle:
+            load().iht_comm_destroy(self.handle)
+            self.handle = None
+
+
+class Solver:
+    """iht_solver_*: Algorithm 1 with fixed mu over a pool of quantised copies (CUDA graph)."""
+
+    def __init__(self, pool, s, n_iter, mu, b_y, seed, level_mode=0, adjoint_variant=0, trace=False,
+                 use_graph=True, comm=None):
+        lib = load()
+        self.pool = pool                     # keep the code tensors alive
+        self.s, self.n_iter = s, n_iter
+        self.trace = trace
+        arr = (IhtQmat * len(pool))(*[c.desc for c in pool])
+        cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
+                        adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
+                        comm=comm.handle if comm is not None else None)
+        h = ctypes.c_void_p()
+        check(lib.iht_solver_create(arr, len(pool), ctypes.byref(cfg), ctypes.byref(h)), "iht_solver_create")
+        self.handle = h
+        self.device = pool[0].codes.device
+        self.out_idx = torch.empty(max(s, 1), dtype=torch.int32, device=self.device)
+        self.out_val = torch.empty(max(s, 1), dtype=torch.float32, device=self.device)
+        self.out_nnz = torch.empty(1, dtype=torch.int32, device=self.device)
+
+    def run(self, y, stream=None):
+        """Device y (float32 or complex64 CUDA tensor of this shard's rows): enqueue a solve;
+        returns device (idx, val, nnz) tensors (valid after the stream reaches them)."""
+        _require_cuda(y)
+        base = torch.view_as_real(y) if y.is_complex() else y
+        check(load().iht_solver_run(self.handle, _ptr(base), 0, _ptr(self.out_idx), _ptr(self.out_val),
+                                    _ptr(self.out_nnz), _stream(stream)), "iht_solver_run")
+        return self.out_idx, self.out_val, self.out_nnz
+
+    def run_host(self, y_host, out_idx, out_val, out_nnz, stream=None):
+        """Host-buffer end-to-end call (IHT_HOST_IO): y_host and outputs are (pinned) CPU tensors;
+        the call copies in, solves, copies out and synchronises the stream."""
+        base = torch.view_as_real(y_host) if y_host.is_complex() else y_host
+        check(load().iht_solver_run(self.handle, _ptr(base), _lib.IHT_HOST_IO, _ptr(out_idx), _ptr(out_val),
+                                    _ptr(out_nnz), _stream(stream)), "iht_solver_run")
+        return out_idx, out_val, out_nnz
+
+    def trace_arrays(self, stream=None):
+        """Recorded iterates x^[2..n*+1]: (idx[n_iter, s], val[n_iter, s], nnz[n_iter]) numpy-like CPU tensors."""
+        idx = torch.empty((self.n_iter, max(self.s, 1)), dtype=torch.int32)
+        val = torch.empty((self.n_iter, max(self.s, 1)), dtype=torch.float32)
+        nnz = torch.empty(self.n_iter, dtype=torch.int32)
+        check(load().iht_solver_trace(self.handle, _ptr(idx), _ptr(val), _ptr(nnz), _stream(stream)),
+              "iht_solver_trace")
+        return idx, val, nnz
+
+    def buffers(self):
+        a, b, c = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        check(load().iht_solver_buffers(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
+              "iht_solver_buffers")
+        return a.value, b.value, c.value
+
+    def launches_per_run(self):
+        return int(load().iht_solver_launches_per_run(self.handle))
+
+    def close(self):
+        if self.handle:
+            load().iht_solver_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(pool, y, s, n_iter, mu, b_y, seed, **kw):
+    """One-shot iht_solve equivalent through the Solver object; returns CPU (idx, val)."""
+    sol = Solver(pool, s, n_iter, mu, b_y, seed, **kw)
+    idx, val, nnz = sol.run(y)
+    torch.cuda.current_stream().synchronize()
+    n = int(nnz.item())
+    sol.close()
+    if n < 0:
+        raise _lib.IhtError(_lib.IHT_EDOMAIN, "iht_solver_run")
+    return idx[:n].cpu(), val[:n].cpu()

@@ -1,0 +1,77 @@
+"""Test-side helpers: layout unpacking and comparison metrics (no method arithmetic)."""
+import numpy as np
+
+
+def rows_pad(rows):
+    return (rows + 255) // 256 * 256
+
+
+def unpack_strips(codes_u8, rows, cols, planes, bits):
+    """Column-strip bytes (cols * strip_bytes) -> codes array (planes, rows, cols) (iht.h layout)."""
+    rp = rows_pad(rows)
+    sb = planes * rp * bits // 8
+    strips = np.asarray(codes_u8, dtype=np.uint8).reshape(cols, sb)
+    out = np.empty((planes, rows, cols), dtype=np.uint8)
+    per_byte = 8 // bits
+    mask = (1 << bits) - 1
+    for p in range(planes):
+        seg = strips[:, p * rp * bits // 8:(p + 1) * rp * bits // 8]        # (cols, rp*bits/8)
+        vals = np.empty((cols, rp), dtype=np.uint8)
+        for k in range(per_byte):
+            vals[:, k::per_byte] = (seg >> (k * bits)) & mask
+        out[p] = vals[:, :rows].T
+    return out
+
+
+def pad_rows_of_strips(codes_u8, rows, cols, planes, bits):
+    """The pad rows' codes (must be 0)."""
+    rp = rows_pad(rows)
+    sb = planes * rp * bits // 8
+    strips = np.asarray(codes_u8, dtype=np.uint8).reshape(cols, sb)
+    per_byte = 8 // bits
+    mask = (1 << bits) - 1
+    pads = []
+    for p in range(planes):
+        seg = strips[:, p * rp * bits // 8:(p + 1) * rp * bits // 8]
+        vals = np.empty((cols, rp), dtype=np.uint8)
+        for k in range(per_byte):
+            vals[:, k::per_byte] = (seg >> (k * bits)) & mask
+        pads.append(vals[:, rows:])
+    return np.concatenate(pads, axis=1) if pads else np.zeros((cols, 0))
+
+
+def stack(vec, rows):
+    """Complex or real length-rows vector -> stacked real vector (planes * rows_pad), pads 0."""
+    vec = np.asarray(vec)
+    rp = rows_pad(rows)
+    if np.iscomplexobj(vec):
+        out = np.zeros(2 * rp)
+        out[:rows] = vec.real
+        out[rp:rp + rows] = vec.imag
+    else:
+        out = np.zeros(rp)
+        out[:rows] = vec
+    return out
+
+
+def unstack(stacked, rows, planes):
+    rp = rows_pad(rows)
+    stacked = np.asarray(stacked, dtype=np.float64)
+    if planes == 2:
+        return stacked[:rows] + 1j * stacked[rp:rp + rows]
+    return stacked[:rows]
+
+
+def rel_l2(got, ref, floor=0.0):
+    got = np.asarray(got, dtype=np.complex128 if np.iscomplexobj(got) or np.iscomplexobj(ref) else np.float64)
+    ref = np.asarray(ref, dtype=got.dtype)
+    den = max(np.linalg.norm(ref), floor)
+    if den == 0.0:
+        return float(np.linalg.norm(got))
+    return float(np.linalg.norm(got - ref) / den)
+
+
+def dense(idx, val, N):
+    x = np.zeros(N)
+    x[np.asarray(idx, dtype=np.int64)] = val
+    return x

@@ -1,0 +1,66 @@
+"""The C-ABI library loads on CPU and exports every symbol include/iht.h declares
+(no compute calls without a GPU); host-side argument checks answer without CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1802_04907_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "iht.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^IHT_API\s+[\w\s\*]*?\b(iht_\w+)\s*\(", txt, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_1802_04907_b200 import build
+        build.build(verbose=False)
+    return _lib.load()
+
+
+def test_header_declares_the_boundary():
+    names = declared()
+    for core in ["iht_quantize", "iht_forward", "iht_adjoint", "iht_threshold", "iht_solve", "iht_absmax",
+                 "iht_quantize_vec", "iht_solver_create", "iht_solver_run"]:
+        assert core in names
+    assert len(names) >= 25
+
+
+def test_every_declared_symbol_is_exported_and_bound(lib):
+    for name in declared():
+        assert hasattr(lib, name), name                 # dlsym succeeds
+        assert name in _lib.SIGNATURES, name            # the binding declares it
+
+
+def test_no_undeclared_signature():
+    assert set(_lib.SIGNATURES) == set(declared())
+
+
+def test_sizes_and_strings(lib):
+    assert lib.iht_abi_version() == 1
+    assert lib.iht_rows_pad(1) == 256 and lib.iht_rows_pad(256) == 256 and lib.iht_rows_pad(257) == 512
+    assert lib.iht_strip_bytes(65536, 1, 4) == 32768            # config 4: 32 KiB strips
+    assert lib.iht_strip_bytes(4096, 1, 2) == 1024              # config 2
+    assert lib.iht_strip_bytes(2304, 2, 2) == 1152              # config 3 (complex, 2 planes)
+    assert lib.iht_qmat_bytes(65536, 262144, 1, 4) == 8 * 2 ** 30
+    assert lib.iht_vec_len(2304, 2) == 4608
+    assert lib.iht_strip_bytes(10, 1, 3) == -1
+    assert b"EINVAL" in lib.iht_strerror(-1)
+    assert b"EDOMAIN" in lib.iht_strerror(-2)
+
+
+def test_host_side_validation_without_gpu(lib):
+    c = ctypes.c_void_p
+    assert lib.iht_absmax(c(0), -1, c(0), c(0)) == _lib.IHT_EINVAL
+    assert lib.iht_quantize(c(0), 0, None, 0, c(0)) == _lib.IHT_EINVAL
+    q = _lib.IhtQmat(rows=10, cols=10, planes=1, bits=3, strip_bytes=0, codes=None)
+    assert lib.iht_adjoint(ctypes.byref(q), c(16), c(16), 0, c(0), 0, c(0)) == _lib.IHT_EINVAL
+    assert lib.iht_threshold(c(0), c(0), c(0), c(0), 1.0, -1, 10, c(0), c(0), c(0), c(0), 0, c(0)) == _lib.IHT_EINVAL
+    assert lib.iht_solver_create(None, 0, None, None) == _lib.IHT_EINVAL
