@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- low-precision IHT (arXiv 1802.04907) hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Metric (BASELINE.json): IHT iter/s and Phi-stream HBM GB/s (% of peak).
+A "step" is one complete QNIHT solve of one observation y: quantise y (a3), then
+n* iterations of forward (a4) -> adjoint (a5) -> [NCCL all-reduce of g] ->
+update + H_s (a6), over a pool of K pre-quantised copies of Phi.  Phi's scale
+and quantisation (a1, a2) are one-time per-operator preprocessing (the paper
+quantises to cut transmission from storage) and are reported under
+"preprocess".  value = steps * n* / (max over ranks of the device time).
+
+Default workload: BASELINE config 4 (real Gaussian 65536 x 262144, 4-bit Phi,
+8-bit y, s = 1024, n* = 100, K = 2 copies = 16 GiB of codes per GPU at N = 1,
+row-sharded at N > 1).  The pool exceeds the 126 MB L2, so every iteration
+streams its adjoint copy from HBM (no L2 flush needed).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_CONTEXT = "paper: CPU 4-bit 4.19x / 8-bit 2.84x vs 32-bit (Haswell E3-1285L v3, P:587); " \
+                "FPGA 2&8-bit 9.19x to 90% support (P:578) -- context only, other hardware"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
+    ap.add_argument("--bits", type=int, default=None, help="override b_Phi (2/4/8 sweep)")
+    ap.add_argument("--K", type=int, default=None, help="pool of quantised copies")
+    ap.add_argument("--variant", type=int, default=0, help="adjoint: 0 int8 MMA, 1 FFMA")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu_id}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- problem setup
+def make_problem(args):
+    from workloads import gen as G
+    p = G.config_problem(args.config, K=args.K, b_phi=args.bits)
+    if args.config == 4 and args.K is None:
+        p.K = 2
+    return p
+
+
+def build_pool(p, rank, world, dev, dist_on):
+    """Generate (config 4: on the device, block-wise) and quantise this rank's row shard
+    of Phi into the pool of K copies.  Returns (pool, c_phi, preprocess timings)."""
+    import torch
+    from paper_1802_04907_b200 import iht
+    assert p.M % world == 0, "row sharding needs M divisible by the GPU count"
+    rows = p.M // world
+    row0 = rank * rows
+    t = {}
+    st = torch.cuda.current_stream()
+    if p.phi is None:
+        from workloads.gpu import gauss_fill
+        blk = max(256, ((2 << 30) // (p.N * 4)) // 256 * 256)
+        buf = torch.empty((min(blk, rows), p.N), dtype=torch.float32, device=dev)
+        cmax = torch.zeros(1, dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for r in range(0, rows, blk):
+            n = min(blk, rows - r)
+            view = buf[:n]
+            gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
+            cmax = torch.maximum(cmax, iht.absmax(view))
+        torch.cuda.synchronize()
+        t["gen_absmax_ms"] = (time.perf_counter() - t0) * 1e3
+    else:
+        phi = torch.from_numpy(p.phi[row0:row0 + rows]).to(dev)
+        t0 = time.perf_counter()
+        cmax = iht.absmax(phi)
+        torch.cuda.synchronize()
+        t["absmax_ms"] = (time.perf_counter() - t0) * 1e3
+    if dist_on:
+        import torch.distributed as dist
+        dist.all_reduce(cmax, op=dist.ReduceOp.MAX)
+    c = float(cmax.item())
+    pool = [iht.new_copy(rows, p.N, p.planes, p.b_phi, 0, p.seed, k, c, row_offset=row0, device=dev)
+            for k in range(p.K)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if p.phi is None:
+        for r in range(0, rows, blk):
+            n = min(blk, rows - r)
+            view = buf[:n]
+            gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
+            for k0 in range(0, p.K, 8):
+                iht.quantize_rows(view, pool[k0:k0 + 8], r)
+        del buf
+    else:
+        for k0 in range(0, p.K, 8):
+            iht.quantize_rows(phi, pool[k0:k0 + 8], 0)
+        del phi
+    torch.cuda.synchronize()
+    t["quantize_ms"] = (time.perf_counter() - t0) * 1e3
+    torch.cuda.empty_cache()
+    return pool, c, t, rows, row0
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(p, steps=None):
+    """Time the float64 oracle (as it stands) on bounded samples of the workload: the
+    first R0 and 2*R0 measurement rows (all N columns), K = 1 copy (the same
+    forward/adjoint work per iteration as K = 2, half the one-time quantisation),
+    n iterations each, with the copies pre-quantised (one-time preprocess, excluded
+    as on the GPU).  Per-iteration time is fitted as t(rows) = a + b rows and
+    extrapolated to the full M rows."""
+    import numpy as np
+    from oracle import iht as OI
+    from oracle import quantize as OQ
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    r0 = max(1, min(p.M // 2, (1 << 23) // (p.N * p.planes)))
+    r0 = 1 << int(np.floor(np.log2(r0)))
+    n_it = 3 if steps is None else max(1, steps)
+    times = []
+    for rows in (r0, 2 * r0):
+        phi = p.phi_rows(0, rows)
+        y = p.y[:rows]
+        pool = OI.CopyPool(phi, p.b_phi, 0, p.seed, OQ.scale_c(phi), cache=2)
+        pool.dequantized(0)                                   # one-time preprocess
+        t0 = time.perf_counter()
+        OI.qniht(phi, y, p.s, n_it, p.mu, p.b_phi, p.b_y, p.seed, 1, record=False, pool=pool)
+        times.append((time.perf_counter() - t0) / n_it)
+    b = max((times[1] - times[0]) / r0, 0.0)
+    a = max(times[0] - b * r0, 0.0)
+    per_iter = a + b * p.M
+    return {"value": 1.0 / per_iter, "unit": "iter/s", "cores": threads, "kind": "oracle",
+            "sample": f"rows 0..{r0 - 1} and 0..{2 * r0 - 1} of {p.M}, all {p.N} columns, K=1 copy, "
+                      f"{n_it} float64 iterations each (copy quantisation excluded); per-iteration time "
+                      f"fitted a + b*rows ({times[0] * 1e3:.1f} / {times[1] * 1e3:.1f} ms) and extrapolated "
+                      f"to {p.M} rows",
+            "host_cores": os.cpu_count()}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "--gpus N>1 must be launched with torchrun"}))
+        return 2
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        p = make_problem(args)
+        for _ in range(max(0, args.warmup)):
+            pass
+        cb = oracle_sample(p, steps=max(1, args.steps))
+        line = {"impl": "reference", "metric": "IHT iter/s", "value": cb["value"], "unit": "iter/s",
+                "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": p.name, "M": p.M, "N": p.N, "b_phi": p.b_phi, "s": p.s,
+                           "n_iter": p.n_iter},
+                "cpu_baseline": cb,
+                "e2e": {"value": cb["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    import torch
+    from paper_1802_04907_b200 import iht
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist_on = world > 1
+    comm = None
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = iht.Comm(rank, world, local)
+
+    def barrier():
+        if dist_on:
+            torch.distributed.barrier(device_ids=[local])
+
+    def max_over_ranks(v):
+        if not dist_on:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    t_setup = time.perf_counter()
+    p = make_problem(args)
+    pool, c_phi, prep, rows, row0 = build_pool(p, rank, world, dev, dist_on)
+    y_shard = p.y[row0:row0 + rows]
+    y_dev = torch.from_numpy(y_shard).to(dev)
+    sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, adjoint_variant=args.variant, comm=comm,
+                     profile=True)
+    setup_s = time.perf_counter() - t_setup
+
+    # ---- device-resident timed region -----------------------------------------------
+    for _ in range(max(3, args.warmup)):
+        sol.run(y_dev)
+    torch.cuda.synchronize()
+    barrier()
+    props = torch.cuda.get_device_properties(local)
+    gpu_id = getattr(props, "uuid", None)
+    gpu_id = f"GPU-{gpu_id}" if gpu_id is not None and not str(gpu_id).startswith("GPU-") else (gpu_id or local)
+    clk = ClockSampler(gpu_id if gpu_id else local)
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        sol.run(y_dev)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    adj_ms = sol.adjoint_times_ms()
+    out_idx, out_val, out_nnz = sol.out_idx, sol.out_val, sol.out_nnz
+    nnz = int(out_nnz.item())
+    launches_per_run = sol.launches_per_run()
+
+    # ---- end-to-end through the public API with host buffers --------------------------
+    e2e = None
+    if not args.no_e2e:
+        y_pin = torch.from_numpy(y_shard.copy()).pin_memory()
+        oi = torch.empty(p.s, dtype=torch.int32).pin_memory()
+        ov = torch.empty(p.s, dtype=torch.float32).pin_memory()
+        on = torch.empty(1, dtype=torch.int32).pin_memory()
+        sol.run_host(y_pin, oi, ov, on)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            sol.run_host(y_pin, oi, ov, on)
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        yb = y_pin.numel() * y_pin.element_size() * (2 if y_pin.is_complex() else 1)
+        e2e = {"value": args.steps * p.n_iter / e2e_s, "unit": "iter/s",
+               "h2d_bytes_per_step": int(yb), "d2h_bytes_per_step": int(p.s * 8 + 4),
+               "path": "iht_solver_run(IHT_HOST_IO): pinned y -> device, solve, x -> pinned host, sync"}
+
+    # ---- bookkeeping --------------------------------------------------------------------
+    peak, peak_kind = measured_peaks()
+    strip = iht.strip_bytes(rows, p.planes, p.b_phi)
+    copy_bytes = strip * p.N
+    R = iht.vec_len(rows, p.planes)
+    adj_bytes = copy_bytes + 4 * R + 4 * p.N                  # codes + r read + g write
+    fwd_bytes = p.s * strip + 4 * R + 4 * R                    # support strips + yhat + r
+    thr_bytes = 4 * p.N * 2 + 8 * p.s                          # g read + a write (+ x)
+    iter_bytes = adj_bytes + fwd_bytes + thr_bytes
+    iters = args.steps * p.n_iter
+    value = iters / (ms / 1e3)
+    adj_avg = statistics.mean(adj_ms)
+    adj_gbs = adj_bytes / (adj_avg / 1e3) / 1e9
+    stream_gbs = iter_bytes * iters / (ms / 1e3) / 1e9     # per GPU
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "adjoint_traffic.json")
+    if os.path.exists(tp):
+        try:
+            d = json.load(open(tp))
+            key = f"{p.name}:b{p.b_phi}:gpus{world}:v{args.variant}"
+            traffic = d.get(key)
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        return 0
+    cb = None
+    if not args.no_cpu_baseline and world == 1:
+        cb = oracle_sample(p)
+    line = {
+        "metric": "IHT iter/s (Phi-stream HBM GB/s, % of peak)",
+        "value": value,
+        "unit": "iter/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "s8/s32 int8-MMA adjoint, f32 forward/update",
+        "data": "synthetic",
+        "config": {
+            "workload": f"{p.name}: {'complex radio' if p.complex else 'real Gaussian'} {p.M}x{p.N}, "
+                        f"{p.b_phi}-bit Phi, {p.b_y}-bit y, s={p.s}, n*={p.n_iter}, mu={p.mu:g}, K={p.K} copies",
+            "M": p.M, "N": p.N, "b_phi": p.b_phi, "b_y": p.b_y, "s": p.s, "n_iter": p.n_iter, "K": p.K,
+            "parallelism": f"row-sharded x{world}" + (", NCCL all-reduce of g per iteration" if world > 1 else ""),
+            "l2": f"inputs > L2: pool {p.K * copy_bytes / 2**30:.2f} GiB per GPU streamed from HBM"
+                  if p.K * copy_bytes > 126e6 else f"pool {p.K * copy_bytes / 2**20:.1f} MiB is L2-resident",
+            "adjoint_variant": args.variant,
+        },
+        "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
+                "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},
+        "roofline": {"bound": "hbm", "kernel": "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
+                     "achieved": adj_gbs, "peak": peak, "unit": "GB/s", "frac": adj_gbs / peak,
+                     "peak_kind": peak_kind, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": adj_bytes, "avg_launch_ms": adj_avg,
+                     "launches_timed": len(adj_ms),
+                     "how": "CUDA event pair around every adjoint inside the solver graph, last timed step"},
+        "cpu_baseline": cb,
+        "e2e": e2e,
+        "gpu_launches": int(launches_per_run * args.steps),
+        "clocks": clocks,
+        "preprocess": {**prep, "c_phi": c_phi, "setup_s": setup_s},
+        "result": {"support_size": nnz},
+        "context": PAPER_CONTEXT,
+    }
+    print(json.dumps(line))
+    sys.stdout.flush()
+    if comm is not None:
+        comm.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -202,6 +202,8 @@ typedef struct {
   int32_t trace;        /* 1: keep every iterate x^[n] (see iht_solver_trace)            */
   int32_t use_graph;    /* 1: capture the n_iter loop into one CUDA graph (default)      */
   iht_comm* comm;       /* NULL: single GPU; else g is all-reduced (sum) every iteration */
+  int32_t profile;      /* 1: record a CUDA event pair around every adjoint launch      */
+  int32_t reserved;
 } iht_config;
 
 /* Stateful solver over a pool of K quantised copies pool[0..K) (all with the
@@ -233,6 +235,10 @@ IHT_API int iht_solver_trace(iht_solver* solver, int32_t* idx_host, float* val_h
  * (r, y-hat) and of g, for parity tests; lengths iht_vec_len(rows, planes) / N. */
 IHT_API int iht_solver_buffers(iht_solver* solver, const float** yhat_dev, const float** r_dev,
                        const float** g_dev);
+/* With cfg.profile = 1: durations (ms) of the n_iter adjoint launches of the LAST
+ * run, from the CUDA event pairs recorded on the run's stream around each adjoint
+ * (inside the graph).  Synchronises on the last event. */
+IHT_API int iht_solver_adjoint_times(iht_solver* solver, float* ms_host);
 /* Number of kernel launches one iht_solver_run enqueues (for gpu_launches). */
 IHT_API int64_t iht_solver_launches_per_run(const iht_solver* solver);
 

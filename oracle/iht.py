@@ -119,17 +119,20 @@ class CopyPool:
 
 
 def qniht(phi, y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True,
-          x0=None):
+          x0=None, pool=None):
     """Algorithm 1 with fixed step mu; returns QnihtResult.
 
     phi: float32 (M x N) or complex64 array; y: float32 / complex64 (M,).
     K: number of independent copies in the pool (reading c6).
+    pool: optional pre-built CopyPool of the same (phi, b_phi, seed) -- lets a caller
+    time the iterations without the one-time quantisation of the copies.
     """
     c_phi = Q.scale_c(phi)
     c_y = Q.scale_c(y)
     y_codes, _ = Q.quantize_vector(y, b_y, level_mode, seed, c=c_y)
     y_hat = Q.dequantize(y_codes, c_y, b_y, level_mode)          # quantised once (P:345)
-    pool = CopyPool(phi, b_phi, level_mode, seed, c_phi, cache=max(2, min(K, 4)))
+    if pool is None:
+        pool = CopyPool(phi, b_phi, level_mode, seed, c_phi, cache=max(2, min(K, 4)))
     N = phi.shape[1]
     if x0 is None:
         x_idx, x_val = np.zeros(0, dtype=np.int64), np.zeros(0)  # x^[0] = 0 (P:347)

@@ -38,7 +38,7 @@ class IhtConfig(ctypes.Structure):
     _fields_ = [
         ("s", c_i32), ("n_iter", c_i32), ("mu", c_f32), ("b_y", c_i32), ("level_mode", c_i32),
         ("adjoint_variant", c_i32), ("seed", c_u64), ("trace", c_i32), ("use_graph", c_i32),
-        ("comm", c_vp),
+        ("comm", c_vp), ("profile", c_i32), ("reserved", c_i32),
     ]
 
 
@@ -70,6 +70,7 @@ SIGNATURES = {
     "iht_solver_run": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
     "iht_solver_trace": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "iht_solver_buffers": (c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    "iht_solver_adjoint_times": (c_int, [c_vp, c_vp]),
     "iht_solver_launches_per_run": (c_i64, [c_vp]),
     "iht_solve": (c_int, [ctypes.POINTER(IhtQmat), c_int, ctypes.POINTER(IhtConfig), c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
 }

@@ -141,6 +141,7 @@ struct iht_solver {
   int nslots = 0;
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
+  std::vector<cudaEvent_t> ev;   // profile: [2 * n_iter] start/stop of each adjoint
   int64_t launches = 0;
   int final_slot = 0;
 };
@@ -156,7 +157,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
   const int64_t ycount = S->rows * S->planes;
   if ((rc = iht_absmax(S->y, ycount, S->c_y, st)) != IHT_OK) return rc;
   L += 1;
-  if (S->cfg.comm && S->cfg.comm->world > 1) {
+  if (S->cfg.comm && S->cfg.comm->world > 1) {   // global max over the row shards (reading c3)
     if ((rc = iht_comm_allreduce(S->cfg.comm, S->c_y, 1, 1, st)) != IHT_OK) return rc;
   }
   const iht_qmat& q0 = S->pool[0];
@@ -165,8 +166,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
     return rc;
   L += 1;
   // x^[1] = 0 (reading c8): the "slot -1" is represented by slot_of(n=0)
-  const int s0 = S->cfg.trace ? 0 : 0;
-  IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz + s0, 0, sizeof(int32_t), st));
+  IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz, 0, sizeof(int32_t), st));   // slot 0 holds x^[1]
   const int K = (int)S->pool.size();
   const int s = S->cfg.s;
   for (int n = 1; n <= S->cfg.n_iter; ++n) {
@@ -178,8 +178,10 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
                           S->xs_nnz + in_slot, s, S->yhat, S->r, nullptr, 0, st)) != IHT_OK)
       return rc;
     L += 1;
+    if (!S->ev.empty()) IHT_CUDA_CHECK(cudaEventRecord(S->ev[2 * (n - 1)], st));
     if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
       return rc;
+    if (!S->ev.empty()) IHT_CUDA_CHECK(cudaEventRecord(S->ev[2 * (n - 1) + 1], st));
     L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
     if (S->cfg.comm && S->cfg.comm->world > 1) {
       if ((rc = iht_comm_allreduce(S->cfg.comm, S->g, S->N, 0, st)) != IHT_OK) return rc;
@@ -251,12 +253,30 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
     delete S;
     return IHT_ECUDA;
   }
+  if (cfg->profile) {
+    S->ev.resize(2 * (size_t)cfg->n_iter);
+    for (auto& e : S->ev) {
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        iht_solver_destroy(S);
+        return IHT_ECUDA;
+      }
+    }
+  }
   *out = S;
+  return IHT_OK;
+}
+
+extern "C" int iht_solver_adjoint_times(iht_solver* S, float* ms) {
+  if (S == nullptr || ms == nullptr || S->ev.empty()) return IHT_EINVAL;
+  IHT_CUDA_CHECK(cudaEventSynchronize(S->ev.back()));
+  for (int n = 0; n < S->cfg.n_iter; ++n) IHT_CUDA_CHECK(cudaEventElapsedTime(&ms[n], S->ev[2 * n], S->ev[2 * n + 1]));
   return IHT_OK;
 }
 
 extern "C" int iht_solver_destroy(iht_solver* S) {
   if (S == nullptr) return IHT_OK;
+  for (auto& e : S->ev)
+    if (e) cudaEventDestroy(e);
   if (S->exec) cudaGraphExecDestroy(S->exec);
   if (S->cap_stream) cudaStreamDestroy(S->cap_stream);
   if (S->block) cudaFree(S->block);

@@ -210,7 +210,7 @@ class Solver:
     """iht_solver_*: Algorithm 1 with fixed mu over a pool of quantised copies (CUDA graph)."""
 
     def __init__(self, pool, s, n_iter, mu, b_y, seed, level_mode=0, adjoint_variant=0, trace=False,
-                 use_graph=True, comm=None):
+                 use_graph=True, comm=None, profile=False):
         lib = load()
         self.pool = pool                     # keep the code tensors alive
         self.s, self.n_iter = s, n_iter
@@ -218,7 +218,7 @@ class Solver:
         arr = (IhtQmat * len(pool))(*[c.desc for c in pool])
         cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
                         adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
-                        comm=comm.handle if comm is not None else None)
+                        comm=comm.handle if comm is not None else None, profile=int(profile), reserved=0)
         h = ctypes.c_void_p()
         check(lib.iht_solver_create(arr, len(pool), ctypes.byref(cfg), ctypes.byref(h)), "iht_solver_create")
         self.handle = h
@@ -258,6 +258,13 @@ class Solver:
         check(load().iht_solver_buffers(self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
               "iht_solver_buffers")
         return a.value, b.value, c.value
+
+    def adjoint_times_ms(self):
+        """Per-launch adjoint durations (ms) of the last run (profile=True), from CUDA events."""
+        buf = (ctypes.c_float * self.n_iter)()
+        check(load().iht_solver_adjoint_times(self.handle, ctypes.cast(buf, ctypes.c_void_p)),
+              "iht_solver_adjoint_times")
+        return list(buf)
 
     def launches_per_run(self):
         return int(load().iht_solver_launches_per_run(self.handle))

@@ -216,8 +216,8 @@ def test_threshold_nan_domain_error():
 
 
 # ------------------------------------------------------------------------- solver
-def _pool(phi, bits, K, c, mode=0):
-    return iht.quantize(_to_dev(phi), bits, mode, SEED, list(range(K)), float(c))
+def _pool(phi, bits, K, c, seed, mode=0):
+    return iht.quantize(_to_dev(phi), bits, mode, seed, list(range(K)), float(c))
 
 
 def _support_ok(rec, got_idx, s):
@@ -245,7 +245,7 @@ def test_teacher_forced_iterations(case):
     n_iter = min(p.n_iter, 40)
     ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, p.K)
     c = OQ.scale_c(p.phi)
-    pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c)
+    pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c, p.seed)
     planes = 2 if p.complex else 1
     yd = _to_dev(p.y)
     c_y = iht.absmax(yd)
@@ -284,7 +284,7 @@ def test_free_running_solver(case, graph):
     n_iter = min(p.n_iter, 40)
     ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, p.K)
     c = OQ.scale_c(p.phi)
-    pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c)
+    pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c, p.seed)
     sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, use_graph=graph)
     sol.run(_to_dev(p.y))
     idx, val, nnz = sol.trace_arrays()
@@ -315,7 +315,7 @@ def test_free_running_solver(case, graph):
 def test_solver_host_io_and_determinism():
     p = CASES["gauss8bit"]()
     c = OQ.scale_c(p.phi)
-    pool = _pool(p.phi, p.b_phi, p.K, c)
+    pool = _pool(p.phi, p.b_phi, p.K, c, p.seed)
     sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed)
     yh = torch.from_numpy(p.y).pin_memory()
     oi = torch.empty(p.s, dtype=torch.int32).pin_memory()
