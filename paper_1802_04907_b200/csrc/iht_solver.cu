@@ -146,8 +146,14 @@ struct iht_solver {
   int final_slot = 0;
 };
 
-static int slot_of(const iht_solver* S, int n) {   // slot holding x^[n+1] after iteration n
-  return S->cfg.trace ? n : (n & 1);
+// Event record that survives stream capture: inside a capture it becomes an event-record
+// node of the graph (cudaEventRecordExternal), so every replay re-records it.
+static cudaError_t record_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(st, &cs);
+  if (err != cudaSuccess) return err;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, st);
 }
 
 // Enqueue one complete run (absmax .. last threshold) on stream st; counts launches.
@@ -178,10 +184,10 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
                           S->xs_nnz + in_slot, s, S->yhat, S->r, nullptr, 0, st)) != IHT_OK)
       return rc;
     L += 1;
-    if (!S->ev.empty()) IHT_CUDA_CHECK(cudaEventRecord(S->ev[2 * (n - 1)], st));
+    if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[2 * (n - 1)], st));
     if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
       return rc;
-    if (!S->ev.empty()) IHT_CUDA_CHECK(cudaEventRecord(S->ev[2 * (n - 1) + 1], st));
+    if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[2 * (n - 1) + 1], st));
     L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
     if (S->cfg.comm && S->cfg.comm->world > 1) {
       if ((rc = iht_comm_allreduce(S->cfg.comm, S->g, S->N, 0, st)) != IHT_OK) return rc;
