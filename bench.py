@@ -313,7 +313,7 @@ def main():
     # ---- bookkeeping --------------------------------------------------------------------
     peak, peak_kind = measured_peaks()
     strip = iht.strip_bytes(rows, p.planes, p.b_phi)
-    copy_bytes = strip * p.N
+    copy_bytes = iht._lib.load().iht_qmat_bytes(rows, p.N, p.planes, p.b_phi)
     R = iht.vec_len(rows, p.planes)
     adj_bytes = copy_bytes + 4 * R + 4 * p.N                  # codes + r read + g write
     fwd_bytes = p.s * strip + 4 * R + 4 * R                    # support strips + yhat + r

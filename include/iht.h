@@ -32,11 +32,15 @@
  *   A length-R "stacked vector" (y-hat, r) holds plane p, row m at index
  *   p * rows_pad + m, with rows_pad = iht_rows_pad(rows) (rows rounded up to a
  *   multiple of 256); pad entries are 0.
- * - Column strips: quantised codes of column n occupy strip_bytes bytes at
- *   codes + n * strip_bytes; inside a strip, plane p starts at byte
- *   p * rows_pad * bits / 8 and row m's b-bit code sits at bit m*bits of that
- *   plane segment, little-endian, LSB first.  strip_bytes is a multiple of 32.
- *   Codes of pad rows are 0.
+ * - Column strips in 16-column tiles: the codes of column n form a logical strip
+ *   of strip_bytes bytes (plane p starts at strip byte p * rows_pad * bits / 8;
+ *   row m's b-bit code sits at bit m*bits of its plane segment, little-endian,
+ *   LSB first).  Strips are interleaved by 16-column tiles at 64-byte granularity
+ *   so that one k-step of a 16-column tile is 1 KiB of contiguous memory:
+ *     strip byte k of column n  ->  codes + (n/16)*16*strip_bytes + (k/64)*1024
+ *                                          + (n%16)*64 + k%64.
+ *   strip_bytes is a multiple of 64.  Codes of pad rows are 0; the bytes of pad
+ *   columns (n >= cols in the last tile) are unspecified and never read.
  */
 #ifndef IHT_H_
 #define IHT_H_
@@ -78,7 +82,7 @@ IHT_API const char* iht_last_cuda_error(void);
 IHT_API int64_t iht_rows_pad(int64_t rows);
 /* Bytes of one column strip: planes * iht_rows_pad(rows) * bits / 8.        */
 IHT_API int64_t iht_strip_bytes(int64_t rows, int planes, int bits);
-/* Bytes of one quantised copy: cols * iht_strip_bytes(rows, planes, bits).  */
+/* Bytes of one quantised copy: round_up(cols, 16) * iht_strip_bytes(...).    */
 IHT_API int64_t iht_qmat_bytes(int64_t rows, int64_t cols, int planes, int bits);
 /* Length of a stacked vector (y-hat, r): planes * iht_rows_pad(rows).        */
 IHT_API int64_t iht_vec_len(int64_t rows, int planes);
@@ -99,7 +103,7 @@ typedef struct {
   float scale_c;       /* c = max |component| over the WHOLE Phi, all shards */
   int32_t reserved;
   int64_t strip_bytes; /* must equal iht_strip_bytes(rows, planes, bits)             */
-  void* codes;         /* device, cols * strip_bytes bytes                           */
+  void* codes;         /* device, iht_qmat_bytes(rows, cols, planes, bits) bytes     */
 } iht_qmat;
 
 /* --------------------------------------------------------------- (a1) scale */

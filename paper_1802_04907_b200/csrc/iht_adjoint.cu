@@ -35,6 +35,15 @@ namespace iht {
 // =====================================================================================
 constexpr int kFfmaCols = 4;   // columns per warp
 
+// streaming 16-byte load that also asks L2 to fetch the surrounding 256-byte block
+__device__ __forceinline__ uint4 ld_stream_u4_l2pf(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -65,7 +74,7 @@ __global__ void __launch_bounds__(256) adjoint_ffma_kernel(const uint8_t* __rest
     uint4 w[kFfmaCols];
 #pragma unroll
     for (int c = 0; c < kFfmaCols; ++c)
-      w[c] = (c < ncol) ? ld_stream_u4(codes + (col0 + c) * strip_bytes + ch * 16) : make_uint4(0, 0, 0, 0);
+      w[c] = (c < ncol) ? ld_stream_u4(codes + tiled_offset(col0 + c, ch * 16, strip_bytes)) : make_uint4(0, 0, 0, 0);
     const float4* r4 = reinterpret_cast<const float4*>(r + ch * RPC);
 #pragma unroll
     for (int q = 0; q < RPC / 4; ++q) {
@@ -106,6 +115,7 @@ __global__ void __launch_bounds__(256) adjoint_ffma_kernel(const uint8_t* __rest
 constexpr int kMmaWarps = 16;          // warps per CTA
 constexpr int kChunkRows = 4096;       // rows per fixed-point chunk (int32-safe flush)
 constexpr int kMaxKR = 65536;          // rows of r limbs resident in shared memory per CTA
+constexpr int kPF = 4;                 // k-steps of codes in flight per lane (register ring)
 
 struct AdjArgs {
   const uint8_t* codes;
@@ -228,20 +238,42 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   for (int64_t task = (int64_t)blockIdx.x * kMmaWarps + warp; task < ntask; task += wstride) {
     const int64_t c0 = task * 16 + g8, c1 = c0 + 8;
     const bool v0 = c0 < a.N, v1 = c1 < a.N;
-    const uint8_t* p0 = a.codes + (v0 ? c0 : 0) * a.strip_bytes + kbyte0 + t * 16;
-    const uint8_t* p1 = a.codes + (v1 ? c1 : 0) * a.strip_bytes + kbyte0 + t * 16;
+    // tiled layout: k-step ks of this 16-column tile is 1 KiB contiguous; column g8 at +64*g8.
+    // Loads are unconditional (no value merges that would wait on them): columns past N
+    // read column 0 of the tile (results discarded) and prefetches past the last k-step
+    // re-read the last k-step.
+    const uint8_t* tile0 = a.codes + task * 16 * a.strip_bytes + (kbyte0 >> 6) * 1024 + t * 16;
+    const uint8_t* p0 = tile0 + (v0 ? g8 : 0) * 64;
+    const uint8_t* p1 = tile0 + (v1 ? g8 + 8 : 0) * 64;
     float accf0 = 0.0f, accf1 = 0.0f;     // lanes t == 0: columns c0, c1
-    uint4 A0 = v0 ? ld_stream_u4(p0) : make_uint4(0, 0, 0, 0);
-    uint4 A1 = v1 ? ld_stream_u4(p1) : make_uint4(0, 0, 0, 0);
+    const int last = nsteps - 1;
+    // register ring of kPF k-steps in flight per lane (plus the L2 256-byte prefetch)
+    uint4 ring0[kPF], ring1[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) {
+      const int64_t o = (int64_t)min(j, last) * 1024;
+      ring0[j] = ld_stream_u4_l2pf(p0 + o);
+      ring1[j] = ld_stream_u4_l2pf(p1 + o);
+    }
     int acc[4] = {0, 0, 0, 0};
-    for (int ks = 0; ks < nsteps; ++ks) {
-      // prefetch next k-step
-      uint4 N0 = make_uint4(0, 0, 0, 0), N1 = make_uint4(0, 0, 0, 0);
-      if (ks + 1 < nsteps) {
-        if (v0) N0 = ld_stream_u4(p0 + (int64_t)(ks + 1) * 64);
-        if (v1) N1 = ld_stream_u4(p1 + (int64_t)(ks + 1) * 64);
+    int cstep = 0, chunk = 0;                 // position inside the current fixed-point chunk
+
+    // one k-step on ring slot j: extract A fragments, optionally refill the slot, load B
+    // fragments from shared memory, 2P MMAs, flush the chunk when it ends
+    auto step = [&](uint4& s0, uint4& s1, int ks, bool refill) {
+      uint32_t af[NMMA][4];
+#pragma unroll
+      for (int u = 0; u < NMMA; ++u) {
+        af[u][0] = byte_reg<B>(s0, 2 * u);
+        af[u][1] = byte_reg<B>(s1, 2 * u);
+        af[u][2] = byte_reg<B>(s0, 2 * u + 1);
+        af[u][3] = byte_reg<B>(s1, 2 * u + 1);
       }
-      // B fragments for this k-step: limb g8, lane chunk (4 ks + t), 4P words
+      if (refill) {   // same registers, consumed above: nothing waits on this load for kPF steps
+        const int64_t o = (int64_t)min(ks + kPF, last) * 1024;
+        s0 = ld_stream_u4_l2pf(p0 + o);
+        s1 = ld_stream_u4_l2pf(p1 + o);
+      }
       uint32_t bw[4 * P];
       if (bload) {
         const uint4* bp = reinterpret_cast<const uint4*>(limb_n + (size_t)(ks * 4 + t) * (16 * P));
@@ -255,16 +287,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
       }
 #pragma unroll
-      for (int u = 0; u < NMMA; ++u) {
-        const uint32_t af[4] = {byte_reg<B>(A0, 2 * u), byte_reg<B>(A1, 2 * u),
-                                byte_reg<B>(A0, 2 * u + 1), byte_reg<B>(A1, 2 * u + 1)};
-        mma_u8s8(acc, af, bw[2 * u], bw[2 * u + 1]);
-      }
-      A0 = N0;
-      A1 = N1;
-      if ((ks + 1) % steps_per_chunk == 0 || ks + 1 == nsteps) {
+      for (int u = 0; u < NMMA; ++u) mma_u8s8(acc, af[u], bw[2 * u], bw[2 * u + 1]);
+      if (++cstep == steps_per_chunk || ks + 1 == nsteps) {
         // flush chunk: lane t=0 holds limbs 0,1 (cols 0,1); lane t=1 holds limb 2 (col 2)
-        const int c = ks / steps_per_chunk;
+        const int c = chunk++;
+        cstep = 0;
         const int l2r0 = __shfl_down_sync(0xffffffffu, acc[0], 1);
         const int l2r1 = __shfl_down_sync(0xffffffffu, acc[2], 1);
         if (t == 0) {
@@ -277,7 +304,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         }
         acc[0] = acc[1] = acc[2] = acc[3] = 0;
       }
+    };
+
+    const int nmain = nsteps / kPF * kPF;
+    for (int ks0 = 0; ks0 < nmain; ks0 += kPF) {
+#pragma unroll
+      for (int j = 0; j < kPF; ++j) step(ring0[j], ring1[j], ks0 + j, true);
     }
+#pragma unroll
+    for (int j = 0; j < kPF; ++j)          // drain: the last nsteps - nmain steps sit in slots 0..
+      if (nmain + j < nsteps) step(ring0[j], ring1[j], nmain + j, false);
     if (t == 0) {
       if (a.nK == 1) {
         if (v0) a.g[c0] = a.sigma * accf0;

@@ -7,14 +7,15 @@
 // streams s * R * b / 8 bytes (0.4% of the adjoint's bytes at config 4).
 //
 // Mapping: a CTA owns a window of 32 consecutive 32-bit code words of every strip
-// (32 * 32/b stacked rows); its 8 warps split the support round-robin (warp w takes
-// j = w, w+8, ...), each lane accumulates the 32/b rows of its word, and the 8
+// (32 * 32/b stacked rows); its 8 warps split the support in rounds of 8 columns
+// (loads issued before use), each lane accumulates the 32/b rows of its word, and the 8
 // partial sums are added in a fixed order through shared memory (deterministic).
 #include "iht_internal.cuh"
 
 namespace iht {
 
 constexpr int kFwdWarps = 8;
+constexpr int kFwdUnroll = 8;
 
 template <int B>
 __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(
@@ -37,17 +38,29 @@ __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(
 #pragma unroll
   for (int i = 0; i < CPW; ++i) acc[i] = 0.0f;
 
-  for (int j = warp; j < nnz; j += kFwdWarps) {
-    const int64_t col = __ldg(x_idx + j);
-    const float xv = __ldg(x_val + j);
-    if (live) {
-      const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(codes + col * strip_bytes) + word);
+  // kFwdUnroll support columns per round, their code words loaded before use
+  const int64_t kofs = (word >> 4) * 1024 + (word & 15) * 4;   // tiled offset of this word, sans column
+  for (int j0 = warp * kFwdUnroll; j0 < nnz; j0 += kFwdWarps * kFwdUnroll) {
+    uint32_t w[kFwdUnroll];
+    float xv[kFwdUnroll];
+#pragma unroll
+    for (int u = 0; u < kFwdUnroll; ++u) {
+      const int j = j0 + u;
+      const bool ok = j < nnz;
+      const int64_t col = ok ? __ldg(x_idx + j) : 0;
+      xv[u] = ok ? __ldg(x_val + j) : 0.0f;
+      w[u] = (ok && live) ? __ldg(reinterpret_cast<const uint32_t*>(
+                                codes + (col >> 4) * (16 * strip_bytes) + (col & 15) * 64 + kofs))
+                          : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kFwdUnroll; ++u) {
 #pragma unroll
       for (int i = 0; i < CPW; ++i) {
         // code -> float exactly: 2^23 + code, minus 2^23; q = 2 code - (L-1) exactly
-        const float cf = __int_as_float(0x4B000000u | ((w >> (i * B)) & MASK)) - 8388608.0f;
+        const float cf = __int_as_float(0x4B000000u | ((w[u] >> (i * B)) & MASK)) - 8388608.0f;
         const float q = __fmaf_rn(2.0f, cf, negLm1);
-        acc[i] = __fmaf_rn(xv, q, acc[i]);
+        acc[i] = __fmaf_rn(xv[u], q, acc[i]);   // xv = 0 for j >= nnz: adds +0, exact
       }
     }
   }

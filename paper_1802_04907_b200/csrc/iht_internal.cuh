@@ -30,6 +30,11 @@ __host__ __device__ inline int num_levels(int bits, int level_mode) {
 // number of 32-byte sectors (256/b rows) and of adjoint k-steps (512/b rows) for b >= 2.
 __host__ __device__ inline int64_t rows_pad(int64_t rows) { return (rows + 255) / 256 * 256; }
 
+// Tiled column-strip layout (iht.h): byte k of column n's logical strip.
+__host__ __device__ inline int64_t tiled_offset(int64_t n, int64_t k, int64_t strip_bytes) {
+  return (n >> 4) * (16 * strip_bytes) + (k >> 6) * 1024 + (n & 15) * 64 + (k & 63);
+}
+
 // ---------------------------------------------------------------- Philox4x32-10
 // Counter-based RNG of the Q-contract (reading c4); own implementation.
 struct u32x4 {

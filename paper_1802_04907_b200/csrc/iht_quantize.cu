@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(128) quantize_kernel(QuantArgs a) {
 
   for (int k = 0; k < a.ncopies; ++k) {
     const uint32_t cid = a.copy_id[k], k0 = a.key0[k], k1 = a.key1[k];
-    uint8_t* base = a.codes[k] + n0 * a.strip_bytes + m0 * B / 8;
+    uint8_t* cbase = a.codes[k];
 #pragma unroll 1
     for (int w = 0; w < 8; ++w) {
       uint32_t cur[P][4];
@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(128) quantize_kernel(QuantArgs a) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (j < ncol)
-            reinterpret_cast<uint32_t*>(base + j * a.strip_bytes + p * plane_bytes)[w] = cur[p][j];
+            *reinterpret_cast<uint32_t*>(cbase + tiled_offset(n0 + j, p * plane_bytes + m0 * B / 8 + 4 * w,
+                                                              a.strip_bytes)) = cur[p][j];
     }
   }
 }

@@ -47,7 +47,7 @@ extern "C" int64_t iht_strip_bytes(int64_t rows, int planes, int bits) {
 }
 extern "C" int64_t iht_qmat_bytes(int64_t rows, int64_t cols, int planes, int bits) {
   const int64_t sb = iht_strip_bytes(rows, planes, bits);
-  return (sb < 0 || cols <= 0) ? -1 : sb * cols;
+  return (sb < 0 || cols <= 0) ? -1 : sb * ((cols + 15) / 16 * 16);
 }
 extern "C" int64_t iht_vec_len(int64_t rows, int planes) {
   if (rows <= 0 || (planes != 1 && planes != 2)) return -1;
@@ -197,7 +197,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
                             S->xs_idx + (int64_t)out_slot * s, S->xs_val + (int64_t)out_slot * s,
                             S->xs_nnz + out_slot, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
       return rc;
-    L += 1;
+    L += 3;   // update+histogram, candidates, select
     S->final_slot = out_slot;
   }
   if (S->cfg.n_iter == 0) S->final_slot = 0;

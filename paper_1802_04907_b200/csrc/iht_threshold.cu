@@ -9,8 +9,16 @@
 // order like the magnitudes): 11 + 11 + 9 bits, three histogram passes, then an
 // ordered compaction that takes every key > T and the lowest-indexed ties == T.
 //
-// v0: one CTA of 1024 threads (N <= a few 10^5 makes this a few microseconds of L2
-// traffic).  a is materialised once in the workspace.
+// Three launches (all deterministic; integer atomics only):
+//   T1 thr_update_hist  (grid, 2048 entries per CTA): a = x + mu g into the workspace,
+//                        histogram of the top 11 key bits (global, int atomics)
+//   T2 thr_candidates   (grid): every CTA finds the same bin d1 holding the s-th largest
+//                        key and compacts, in index order, its entries with digit >= d1
+//                        into its own slot of the candidate buffer
+//   T3 thr_select       (1 CTA): gathers the candidates (a few thousand, index order) into
+//                        shared memory, finishes the radix select on them and writes the
+//                        ordered support.  If the candidates do not fit (massive ties,
+//                        mostly-zero a) it falls back to the full single-CTA select over a.
 #include "iht_internal.cuh"
 
 namespace iht {
@@ -59,79 +67,51 @@ __device__ void find_bin(const int* hist, int nbins, int target, int* d_out, int
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThrThreads, 1) threshold_kernel(
-    const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
-    int32_t max_nnz, const float* __restrict__ g, float mu, int s, int64_t N, float* __restrict__ a,
-    int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t* __restrict__ out_nnz) {
-  __shared__ int hist[2048];
-  __shared__ int scratch[kThrWarps];
-  __shared__ int wgt[kThrWarps], weq[kThrWarps], wtake[kThrWarps], wbase[kThrWarps];
-  __shared__ int sh_d, sh_above, sh_nan, sh_total;
+// Exact top-s of the n entries (idx(i), val(i)), i = 0..n-1, listed in increasing index
+// order: radix select of the s-th largest key, then ordered compaction (ties -> lowest
+// index, zeros never kept).  All 1024 threads of the CTA call it.  Writes out_*;
+// returns nothing; *out_nnz = total (or -1 when nan_flag).
+template <class Val, class Idx>
+__device__ void select_ordered(int n, int s, Val val, Idx idx, int32_t* __restrict__ out_idx,
+                               float* __restrict__ out_val, int32_t* __restrict__ out_nnz, int nan_flag,
+                               int* hist, int* scratch, int* wgt, int* weq, int* wtake, int* wbase, int* sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  // ---- a = x + mu g --------------------------------------------------------------------
-  int nnz = *x_nnz;
-  if (nnz < 0) {                 // poisoned input (earlier non-finite a): stays poisoned
-    if (tid == 0) *out_nnz = -1;
-    return;
-  }
-  nnz = min(nnz, max_nnz);
-  for (int64_t n = tid; n < N; n += kThrThreads) a[n] = __fmul_rn(mu, g[n]);
-  if (tid == 0) sh_nan = 0;
-  __syncthreads();
-  for (int j = tid; j < nnz; j += kThrThreads) {
-    const int64_t n = x_idx[j];
-    a[n] = __fadd_rn(x_val[j], a[n]);
-  }
-  __syncthreads();
-
-  if (s == 0) {                  // H_0 keeps nothing
-    if (tid == 0) *out_nnz = 0;
-    return;
-  }
-
-  // ---- radix select of the s-th largest key --------------------------------------------
-  unsigned int T = 0;        // threshold key
-  int need = 0;              // ties at T to take
-  const bool all = (int64_t)s >= N;
-  if (!all && s > 0) {
+  unsigned int T = 0;
+  int need = 0;
+  const bool all = s >= n;
+  if (!all) {
     unsigned int prefix = 0;
     int target = s;
-    int above_total = 0;
     const int shifts[3] = {20, 9, 0};
     const int widths[3] = {11, 11, 9};
     for (int pass = 0; pass < 3; ++pass) {
       const int nb = 1 << widths[pass];
       for (int b = tid; b < nb; b += kThrThreads) hist[b] = 0;
       __syncthreads();
-      const int sh = shifts[pass];
-      const unsigned int hi_shift = sh + widths[pass];   // bits above this digit must match prefix
-      for (int64_t n = tid; n < N; n += kThrThreads) {
-        const unsigned int key = __float_as_uint(a[n]) & 0x7FFFFFFFu;
-        if (pass == 0 && key > 0x7F800000u) sh_nan = 1;
+      const int sh_ = shifts[pass];
+      const unsigned int hi_shift = sh_ + widths[pass];
+      for (int i = tid; i < n; i += kThrThreads) {
+        const unsigned int key = __float_as_uint(val(i)) & 0x7FFFFFFFu;
         if (hi_shift >= 31 || (key >> hi_shift) == (prefix >> hi_shift))
-          atomicAdd(&hist[(key >> sh) & (nb - 1)], 1);
+          atomicAdd(&hist[(key >> sh_) & (nb - 1)], 1);
       }
       __syncthreads();
-      find_bin(hist, nb, target, &sh_d, &sh_above, scratch);
-      prefix |= (unsigned int)sh_d << sh;
-      above_total += sh_above;
-      target -= sh_above;
+      find_bin(hist, nb, target, &sh[0], &sh[1], scratch);
+      prefix |= (unsigned int)sh[0] << sh_;
+      target -= sh[1];
       __syncthreads();
     }
     T = prefix;
-    need = target;             // keys == T to take (>= 1)
-    (void)above_total;
+    need = target;
   }
-
-  // ---- ordered compaction --------------------------------------------------------------
-  const int64_t span = ((N + kThrWarps - 1) / kThrWarps + 31) / 32 * 32;
-  const int64_t lo = (int64_t)warp * span, hi = min64(N, lo + span);
+  // ordered compaction: warp w owns the contiguous range [lo, hi) of the list
+  const int span = ((n + kThrWarps - 1) / kThrWarps + 31) / 32 * 32;
+  const int lo = warp * span, hi = min(n, lo + span);
   int gt = 0, eq = 0;
-  for (int64_t n0 = lo; n0 < hi; n0 += 32) {
-    const int64_t n = n0 + lane;
-    const unsigned int key = n < hi ? (__float_as_uint(a[n]) & 0x7FFFFFFFu) : 0u;
-    const bool live = n < hi && key > 0u;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned int key = i < hi ? (__float_as_uint(val(i)) & 0x7FFFFFFFu) : 0u;
+    const bool live = i < hi && key > 0u;
     gt += __popc(__ballot_sync(0xffffffffu, live && (all || key > T)));
     eq += __popc(__ballot_sync(0xffffffffu, live && !all && key == T));
   }
@@ -149,17 +129,17 @@ __global__ void __launch_bounds__(kThrThreads, 1) threshold_kernel(
       wbase[w] = base;
       base += wgt[w] + tk;
     }
-    sh_total = base;
+    sh[2] = base;
   }
   __syncthreads();
   int run_sel = 0, run_eq = 0;
   const unsigned int lt = (1u << lane) - 1u;
   const int take = wtake[warp], base = wbase[warp];
-  for (int64_t n0 = lo; n0 < hi; n0 += 32) {
-    const int64_t n = n0 + lane;
-    const float av = n < hi ? a[n] : 0.0f;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const float av = i < hi ? val(i) : 0.0f;
     const unsigned int key = __float_as_uint(av) & 0x7FFFFFFFu;
-    const bool live = n < hi && key > 0u;
+    const bool live = i < hi && key > 0u;
     const bool is_gt = live && (all || key > T);
     const bool is_eq = live && !all && key == T;
     const unsigned int beq = __ballot_sync(0xffffffffu, is_eq);
@@ -168,13 +148,205 @@ __global__ void __launch_bounds__(kThrThreads, 1) threshold_kernel(
     const unsigned int bsel = __ballot_sync(0xffffffffu, sel);
     if (sel) {
       const int pos = base + run_sel + __popc(bsel & lt);
-      out_idx[pos] = (int32_t)n;
+      out_idx[pos] = (int32_t)idx(i);
       out_val[pos] = av;
     }
     run_sel += __popc(bsel);
     run_eq += __popc(beq);
   }
-  if (tid == 0) *out_nnz = sh_nan ? -1 : sh_total;
+  if (tid == 0) *out_nnz = nan_flag ? -1 : sh[2];
+}
+
+// ---------------------------------------------------------------------------- workspace
+constexpr int kTile = 2048;            // entries per CTA in T1 / T2
+constexpr int kTileThreads = 256;
+constexpr int kCandCap = 8192;         // candidates T3 keeps in shared memory
+constexpr int kHistBins = 2048;
+
+struct ThrWs {
+  float* a;          // [N]
+  int32_t* cidx;     // [N] per-tile candidate slots
+  float* cval;       // [N]
+  int* ccount;       // [ntiles]
+  int* hist;         // [kHistBins] global histogram of digit 1
+  int* flags;        // [0] nan
+};
+
+__host__ __device__ inline int64_t thr_ws_layout(int64_t N, char* base, ThrWs* w) {
+  auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+  const int64_t ntiles = (N + kTile - 1) / kTile;
+  int64_t off = 0;
+  if (w) w->hist = reinterpret_cast<int*>(base + off);
+  off += al(kHistBins * 4);
+  if (w) w->flags = reinterpret_cast<int*>(base + off);
+  off += al(16);
+  const int64_t clear_bytes = off;       // hist + flags are zeroed by the launcher
+  if (w) w->a = reinterpret_cast<float*>(base + off);
+  off += al(N * 4);
+  if (w) w->cidx = reinterpret_cast<int32_t*>(base + off);
+  off += al(N * 4);
+  if (w) w->cval = reinterpret_cast<float*>(base + off);
+  off += al(N * 4);
+  if (w) w->ccount = reinterpret_cast<int*>(base + off);
+  off += al(ntiles * 4);
+  (void)clear_bytes;
+  return off;
+}
+
+// T1: a = x + mu g, global histogram of key >> 20
+__global__ void __launch_bounds__(kTileThreads) thr_update_hist(
+    const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
+    int32_t max_nnz, const float* __restrict__ g, float mu, int64_t N, ThrWs w) {
+  __shared__ float as[kTile];
+  __shared__ int hist[kHistBins];
+  const int tid = threadIdx.x;
+  const int64_t start = (int64_t)blockIdx.x * kTile;
+  const int cnt = (int)min64(kTile, N - start);
+  for (int b = tid; b < kHistBins; b += kTileThreads) hist[b] = 0;
+  for (int i = tid; i < cnt; i += kTileThreads) as[i] = __fmul_rn(mu, g[start + i]);
+  int nnz = *x_nnz;
+  nnz = nnz < 0 ? 0 : min(nnz, max_nnz);
+  __syncthreads();
+  for (int j = tid; j < nnz; j += kTileThreads) {
+    const int64_t n = x_idx[j];
+    if (n >= start && n < start + cnt) as[n - start] = __fadd_rn(x_val[j], as[n - start]);
+  }
+  __syncthreads();
+  int nan = 0;
+  for (int i = tid; i < cnt; i += kTileThreads) {
+    const float v = as[i];
+    w.a[start + i] = v;
+    const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
+    nan |= key > 0x7F800000u;
+    atomicAdd(&hist[key >> 20], 1);
+  }
+  if (nan) atomicOr(&w.flags[0], 1);
+  __syncthreads();
+  for (int b = tid; b < kHistBins; b += kTileThreads)
+    if (hist[b]) atomicAdd(&w.hist[b], hist[b]);
+}
+
+// T2: bin d1 of the s-th largest key (same in every CTA), ordered per-tile compaction
+// of the entries with digit >= d1 (key > 0).
+__global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N, ThrWs w) {
+  __shared__ int sfx[kTileThreads];
+  __shared__ int d1s;
+  __shared__ int wcnt[kTileThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // thread t owns bins [8t, 8t+8); suffix sums over threads (descending bins)
+  int local = 0;
+  for (int b = tid * 8; b < tid * 8 + 8; ++b) local += w.hist[b];
+  sfx[tid] = local;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0, d = 0;
+    const int target = s < 1 ? 1 : s;
+    for (int t = kTileThreads - 1; t >= 0 && d == 0; --t) {
+      if (acc + sfx[t] >= target) {
+        for (int b = t * 8 + 7; b >= t * 8; --b) {
+          acc += w.hist[b];
+          if (acc >= target) { d = b; break; }
+        }
+        break;
+      }
+      acc += sfx[t];
+    }
+    d1s = d;
+  }
+  __syncthreads();
+  const unsigned int d1 = (unsigned int)d1s;
+  const int64_t start = (int64_t)blockIdx.x * kTile;
+  const int cnt = (int)min64(kTile, N - start);
+  // two passes over the tile (L1/L2 resident): count per warp, then write in order
+  const int per_warp = kTile / (kTileThreads / 32);       // 256 contiguous entries per warp
+  const int lo = warp * per_warp, hi = min(cnt, lo + per_warp);
+  int c = 0;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned int key = i < hi ? (__float_as_uint(w.a[start + i]) & 0x7FFFFFFFu) : 0u;
+    c += __popc(__ballot_sync(0xffffffffu, i < hi && key > 0u && (key >> 20) >= d1));
+  }
+  if (lane == 0) wcnt[warp] = c;
+  __syncthreads();
+  int base = 0;
+  for (int q = 0; q < warp; ++q) base += wcnt[q];
+  const unsigned int lt = (1u << lane) - 1u;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const float v = i < hi ? w.a[start + i] : 0.0f;
+    const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
+    const bool sel = i < hi && key > 0u && (key >> 20) >= d1;
+    const unsigned int b = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
+      const int pos = base + __popc(b & lt);
+      w.cidx[start + pos] = (int32_t)(start + i);
+      w.cval[start + pos] = v;
+    }
+    base += __popc(b);
+  }
+  if (tid == 0) {
+    int tot = 0;
+    for (int q = 0; q < kTileThreads / 32; ++q) tot += wcnt[q];
+    w.ccount[blockIdx.x] = tot;
+  }
+}
+
+// T3: gather candidates (index order) and finish the selection in one CTA.
+__global__ void __launch_bounds__(kThrThreads, 1) thr_select(
+    const int32_t* __restrict__ x_nnz, int s, int64_t N, ThrWs w, int32_t* __restrict__ out_idx,
+    float* __restrict__ out_val, int32_t* __restrict__ out_nnz) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  float* cval = reinterpret_cast<float*>(dsm + kCandCap * 4);
+  __shared__ int hist[2048];
+  __shared__ int scratch[kThrWarps];
+  __shared__ int wgt[kThrWarps], weq[kThrWarps], wtake[kThrWarps], wbase[kThrWarps];
+  __shared__ int sh[4];
+  __shared__ int tile_base[1025];
+  const int tid = threadIdx.x;
+  if (*x_nnz < 0) {                 // poisoned input (earlier non-finite a) stays poisoned
+    if (tid == 0) *out_nnz = -1;
+    return;
+  }
+  const int nan = w.flags[0];
+  if (s == 0 || nan) {              // H_0 keeps nothing; NaN -> domain error
+    if (tid == 0) *out_nnz = nan ? -1 : 0;
+    return;
+  }
+  const int ntiles = (int)((N + kTile - 1) / kTile);
+  // total candidates
+  int total = 0;
+  if (tid == 0) {
+    int acc = 0;
+    for (int t = 0; t < ntiles; ++t) acc += w.ccount[t];
+    sh[3] = acc;
+  }
+  __syncthreads();
+  total = sh[3];
+  const bool fits = total <= kCandCap && ntiles <= 1024 && (int64_t)s < N;
+  if (fits) {
+    if (tid == 0) {
+      int acc = 0;
+      for (int t = 0; t < ntiles; ++t) { tile_base[t] = acc; acc += w.ccount[t]; }
+    }
+    __syncthreads();
+    // gather: warp per tile, in order
+    for (int t = tid >> 5; t < ntiles; t += kThrWarps) {
+      const int c = w.ccount[t], b = tile_base[t];
+      const int64_t src = (int64_t)t * kTile;
+      for (int i = tid & 31; i < c; i += 32) {
+        cidx[b + i] = w.cidx[src + i];
+        cval[b + i] = w.cval[src + i];
+      }
+    }
+    __syncthreads();
+    select_ordered(total, s, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, out_idx, out_val,
+                   out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
+  } else {
+    const float* a = w.a;
+    select_ordered((int)N, s, [&](int i) { return a[i]; }, [&](int i) { return i; }, out_idx, out_val, out_nnz, 0,
+                   hist, scratch, wgt, weq, wtake, wbase, sh);
+  }
 }
 
 }  // namespace iht
@@ -183,7 +355,8 @@ using namespace iht;
 
 extern "C" int64_t iht_threshold_ws_bytes(int64_t N, int32_t s) {
   (void)s;
-  return N * (int64_t)sizeof(float);
+  if (N <= 0) return -1;
+  return thr_ws_layout(N, nullptr, nullptr);
 }
 
 extern "C" int iht_threshold(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz,
@@ -193,12 +366,24 @@ extern "C" int iht_threshold(const int32_t* x_idx, const float* x_val, const int
   if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr ||
       out_nnz == nullptr || s < 0 || N <= 0 || N > 0x7FFFFFFFll)
     return IHT_EINVAL;
-  if (ws == nullptr || ws_bytes < N * (int64_t)sizeof(float)) return IHT_EINVAL;
+  if (ws == nullptr || ws_bytes < thr_ws_layout(N, nullptr, nullptr)) return IHT_EINVAL;
   if (!isfinite(mu)) return IHT_EDOMAIN;
   cudaStream_t st = (cudaStream_t)stream;
+  ThrWs w{};
+  thr_ws_layout(N, static_cast<char*>(ws), &w);
+  static bool attr = false;
+  if (!attr) {
+    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
+    attr = true;
+  }
+  IHT_CUDA_CHECK(cudaMemsetAsync(w.hist, 0, reinterpret_cast<char*>(w.a) - reinterpret_cast<char*>(w.hist), st));
+  const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
   // max_nnz: the caller's x arrays hold at most s entries (x is an H_s output)
-  threshold_kernel<<<1, kThrThreads, 0, st>>>(x_idx, x_val, x_nnz, s, g, mu, s, N,
-                                              static_cast<float*>(ws), out_idx, out_val, out_nnz);
+  thr_update_hist<<<tiles, kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, s, g, mu, N, w);
+  IHT_LAUNCH_CHECK();
+  thr_candidates<<<tiles, kTileThreads, 0, st>>>(s, N, w);
+  IHT_LAUNCH_CHECK();
+  thr_select<<<1, kThrThreads, kCandCap * 8, st>>>(x_nnz, s, N, w, out_idx, out_val, out_nnz);
   IHT_LAUNCH_CHECK();
   return IHT_OK;
 }

@@ -81,7 +81,8 @@ def new_copy(rows, cols, planes, bits, level_mode, seed, copy_id, scale_c, row_o
              codes=None):
     sb = strip_bytes(rows, planes, bits)
     if codes is None:
-        codes = torch.empty(cols * sb, dtype=torch.uint8, device=device or "cuda")
+        codes = torch.empty(load().iht_qmat_bytes(rows, cols, planes, bits), dtype=torch.uint8,
+                            device=device or "cuda")
     d = IhtQmat(rows=rows, cols=cols, row_offset=row_offset, planes=planes, bits=bits, level_mode=level_mode,
                 copy_id=copy_id, seed=seed, scale_c=float(scale_c), reserved=0, strip_bytes=sb,
                 codes=codes.data_ptr())

@@ -6,11 +6,18 @@ def rows_pad(rows):
     return (rows + 255) // 256 * 256
 
 
+def detile(codes_u8, cols, sb):
+    """Tiled copy bytes -> per-column strips (cols, sb) (iht.h: 16-column tiles, 64-byte pieces)."""
+    ntiles = (cols + 15) // 16
+    arr = np.asarray(codes_u8, dtype=np.uint8)[: ntiles * 16 * sb].reshape(ntiles, sb // 64, 16, 64)
+    return arr.transpose(0, 2, 1, 3).reshape(ntiles * 16, sb)[:cols]
+
+
 def unpack_strips(codes_u8, rows, cols, planes, bits):
-    """Column-strip bytes (cols * strip_bytes) -> codes array (planes, rows, cols) (iht.h layout)."""
+    """Copy bytes -> codes array (planes, rows, cols) (iht.h layout)."""
     rp = rows_pad(rows)
     sb = planes * rp * bits // 8
-    strips = np.asarray(codes_u8, dtype=np.uint8).reshape(cols, sb)
+    strips = detile(codes_u8, cols, sb)
     out = np.empty((planes, rows, cols), dtype=np.uint8)
     per_byte = 8 // bits
     mask = (1 << bits) - 1
@@ -27,7 +34,7 @@ def pad_rows_of_strips(codes_u8, rows, cols, planes, bits):
     """The pad rows' codes (must be 0)."""
     rp = rows_pad(rows)
     sb = planes * rp * bits // 8
-    strips = np.asarray(codes_u8, dtype=np.uint8).reshape(cols, sb)
+    strips = detile(codes_u8, cols, sb)
     per_byte = 8 // bits
     mask = (1 << bits) - 1
     pads = []

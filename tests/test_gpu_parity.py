@@ -73,8 +73,9 @@ def test_quantize_rows_blockwise_equals_whole():
         r1 = min(M, r0 + 256)
         iht.quantize_rows(_to_dev(phi[r0:r1]), blk, r0)
     torch.cuda.synchronize()
-    for a, b in zip(whole, blk):
-        assert torch.equal(a.codes, b.codes)
+    for a, b in zip(whole, blk):          # compare the real columns (pad-column bytes are unspecified)
+        np.testing.assert_array_equal(unpack_strips(a.codes.cpu().numpy(), M, N, 1, 4),
+                                      unpack_strips(b.codes.cpu().numpy(), M, N, 1, 4))
 
 
 def test_absmax_nan():
