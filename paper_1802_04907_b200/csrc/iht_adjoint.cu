@@ -44,6 +44,11 @@ __device__ __forceinline__ uint4 ld_stream_u4_l2pf(const void* p) {
   return r;
 }
 
+// per-thread L2 prefetch of the cache line holding p (no registers / smem used)
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -114,8 +119,10 @@ __global__ void __launch_bounds__(256) adjoint_ffma_kernel(const uint8_t* __rest
 // =====================================================================================
 constexpr int kMmaWarps = 16;          // warps per CTA
 constexpr int kChunkRows = 4096;       // rows per fixed-point chunk (int32-safe flush)
-constexpr int kMaxKR = 65536;          // rows of r limbs resident in shared memory per CTA
-constexpr int kPF = 4;                 // k-steps of codes in flight per lane (register ring)
+constexpr int kMaxKR = 32768;          // rows of r limbs resident in shared memory per CTA
+constexpr int kReq = 2;                // k-steps (1 KiB tile-steps) per bulk request
+constexpr int kRing = 3;               // requests in flight per warp (shared-memory ring slots)
+constexpr int kSlot = kReq * 1024;     // bytes per ring slot
 
 struct AdjArgs {
   const uint8_t* codes;
@@ -140,17 +147,56 @@ __device__ __forceinline__ void mma_u8s8(int (&d)[4], const uint32_t (&a)[4], ui
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// Byte-register rho of a 16-byte code chunk: word rho / P, extraction rho % P;
-// byte i holds the code at chunk position pos(rho, i) = (rho/P)*(32/B) + rho%P + P*i.
+// Fragment register of a 16-byte code chunk: word v, bit-position j (0 <= j < P = 8/B).
+// The codes of bit-position j are masked IN PLACE (one LOP3, no shift): byte i holds
+// code * 2^{B j} for the code at chunk position pos(v, j, i) = v*(32/B) + j + P*i.
+// Each j accumulates in its own int32 accumulator, divided by 2^{B j} (exactly) at the
+// flush.  Limb words are stored per lane chunk at slot 4 j + v (MMA u = 2 j + m uses
+// words v = 2m, 2m+1 of bit-position j).
 template <int B>
-__device__ __forceinline__ uint32_t byte_reg(const uint4& w, int rho) {
-  constexpr int P = 8 / B;
+__device__ __forceinline__ uint32_t frag_reg(const uint4& w, int v, int j) {
   constexpr uint32_t M8 = ((1u << B) - 1u) * 0x01010101u;
-  const int v = rho / P, j = rho % P;
   const uint32_t word = v == 0 ? w.x : v == 1 ? w.y : v == 2 ? w.z : w.w;
-  return (word >> (B * j)) & M8;
+  return word & (M8 << (B * j));
 }
 
+// TMA-style bulk copy global -> shared completing on an mbarrier (transaction bytes)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(mbar), "r"(parity) : "memory");
+}
+
+// cp.async (LDGSTS) 16 bytes global -> shared, L2 only; one commit group per k-step
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr) {
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t smem_addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_addr));
+  return v;
+}
+
+// Shared-memory layout of the MMA kernel:
+//   [ring]  kMmaWarps x kRing slots x 1 KiB: each lane's two 16-byte code chunks of a k-step
+//           (a lane only ever reads back what it copied itself)
+//   [limbs] 3 planes x limb_stride bytes: r in 3 signed 8-bit limbs, permuted per lane chunk
+//   [Fc, Sc, red] per-chunk exponents, exact integer sums of r_int, reduction scratch
 template <int B>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs a) {
   constexpr int P = 8 / B;               // codes per byte
@@ -158,16 +204,65 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   constexpr int KSTEP = 4 * RPC;         // rows per warp k-step (4 lanes t)
   constexpr int NMMA = 2 * P;            // MMAs per k-step
   extern __shared__ __align__(16) uint8_t smem[];
-  // smem: [3 limb planes][KR bytes + pad] | chunk exponent F[KR/KC] | chunk sum S[KR/KC] (int64)
   const int nchunks = a.KR / a.KC;
-  uint8_t* limbs = smem;
-  int* Fc = reinterpret_cast<int*>(smem + 3 * a.limb_stride);
+  uint8_t* ring = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMmaWarps * kRing * kSlot);   // [warp][slot]
+  uint8_t* limbs = smem + kMmaWarps * kRing * kSlot + kMmaWarps * kRing * 8;
+  int* Fc = reinterpret_cast<int*>(limbs + 3 * a.limb_stride);
   long long* Sc = reinterpret_cast<long long*>(Fc + ((nchunks + 1) & ~1));
   float* red = reinterpret_cast<float*>(Sc + nchunks);     // [nchunks][kMmaWarps] scratch
 
   const int kr = blockIdx.y;
   const int64_t row0 = (int64_t)kr * a.KR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- work assignment; the first kRing k-steps are requested before the prologue ------
+  const int g8 = lane >> 2, t = lane & 3;
+  const int64_t ntask = (a.N + 15) / 16;
+  const int64_t wid = (int64_t)blockIdx.x * kMmaWarps + warp;
+  const int64_t wstride = (int64_t)gridDim.x * kMmaWarps;
+  const int nsteps = (int)(min64(a.KR, a.Rpad - row0) / KSTEP);     // last K-range may be short
+  const uint8_t* kbase = a.codes + (row0 * B / 8 >> 6) * 1024 + t * 16;   // K-range offset in a tile
+  auto task_ptr = [&](int64_t task, const uint8_t*& b0, const uint8_t*& b1) {
+    const uint8_t* b = kbase + task * 16 * a.strip_bytes;
+    const int64_t cc0 = task * 16 + g8;       // columns past N read column 0 of the tile
+    b0 = b + (cc0 < a.N ? g8 : 0) * 64;
+    b1 = b + (cc0 + 8 < a.N ? g8 + 8 : 0) * 64;
+  };
+  // the loop runs npad k-steps per task (nsteps rounded up to whole requests); a padded
+  // step multiplies whatever its smem half holds by zero limbs
+  const int npad = (nsteps + kReq - 1) / kReq * kReq;
+  const uint32_t ring_w = (uint32_t)__cvta_generic_to_shared(ring + warp * kRing * kSlot);
+  const uint32_t bar_w = (uint32_t)__cvta_generic_to_shared(bars + warp * kRing);
+  if (lane == 0)
+    for (int j = 0; j < kRing; ++j) mbar_init(bar_w + 8 * j, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  // request cursor (lane 0) over this warp's flat k-step sequence (task wid, wid + wstride,
+  // ...): each request is one bulk copy of kReq consecutive tile-steps (kReq x 1 KiB)
+  const uint8_t* kseg = a.codes + (row0 * B / 8 >> 6) * 1024;    // K-range offset inside a tile
+  int64_t rq_task = wid;
+  int rq_ks = 0;
+  const uint8_t* rq = kseg + rq_task * 16 * a.strip_bytes;
+  auto request = [&](int slot) {
+    if (rq_task < ntask) {
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)min(kReq, nsteps - rq_ks) * 1024;
+        const uint32_t bar = bar_w + 8 * slot;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(ring_w + slot * kSlot, rq, bytes, bar);
+      }
+      if ((rq_ks += kReq) < npad) {
+        rq += kSlot;
+      } else {
+        rq_ks = 0;
+        rq_task += wstride;
+        rq = kseg + rq_task * 16 * a.strip_bytes;
+      }
+    }
+  };
+#pragma unroll 1
+  for (int j = 0; j < kRing; ++j) request(j);
 
   // ---- prologue 1: per-chunk max |r| -> exponent F_c ---------------------------------
   for (int c = 0; c < nchunks; ++c) {
@@ -215,7 +310,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         l1w |= (uint32_t)(l1 & 255) << (8 * i);
         l2w |= (uint32_t)(l2 & 255) << (8 * i);
       }
-      const int off = ch * (16 * P) + rho * 4;
+      const int off = ch * (16 * P) + (4 * (rho % P) + rho / P) * 4;   // slot 4 j + v
       *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
       *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
       *reinterpret_cast<uint32_t*>(limbs + 2 * a.limb_stride + off) = l2w;
@@ -225,102 +320,90 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   }
   __syncthreads();
 
-  // ---- main loop: warp tasks of 16 columns over this K-range --------------------------
-  const int g8 = lane >> 2, t = lane & 3;
-  const int64_t ntask = (a.N + 15) / 16;
-  const int64_t wstride = (int64_t)gridDim.x * kMmaWarps;
-  const int nsteps = (int)(min64(a.KR, a.Rpad - row0) / KSTEP);   // last K-range may be short
-  const int steps_per_chunk = a.KC / KSTEP;
-  const uint8_t* limb_n = limbs + (g8 < 3 ? g8 : 0) * a.limb_stride;
+  // ---- main loop: tasks (16 columns x this K-range) -> fixed-point chunks -> k-steps.
+  //      Step ks (global step counter gs) lives in ring slot gs % kRing; after consuming it
+  //      the slot is refilled with the step kRing later (this task or the next one).
+  const int spc = a.KC / KSTEP;                            // k-steps per chunk
+  const uint32_t limb_n = (uint32_t)__cvta_generic_to_shared(limbs + (g8 < 3 ? g8 : 0) * a.limb_stride);
   const bool bload = g8 < 3;
-  const int64_t kbyte0 = row0 * B / 8;   // byte offset of this K-range inside a strip
-
-  for (int64_t task = (int64_t)blockIdx.x * kMmaWarps + warp; task < ntask; task += wstride) {
-    const int64_t c0 = task * 16 + g8, c1 = c0 + 8;
-    const bool v0 = c0 < a.N, v1 = c1 < a.N;
-    // tiled layout: k-step ks of this 16-column tile is 1 KiB contiguous; column g8 at +64*g8.
-    // Loads are unconditional (no value merges that would wait on them): columns past N
-    // read column 0 of the tile (results discarded) and prefetches past the last k-step
-    // re-read the last k-step.
-    const uint8_t* tile0 = a.codes + task * 16 * a.strip_bytes + (kbyte0 >> 6) * 1024 + t * 16;
-    const uint8_t* p0 = tile0 + (v0 ? g8 : 0) * 64;
-    const uint8_t* p1 = tile0 + (v1 ? g8 + 8 : 0) * 64;
+  int slot = 0;
+  uint32_t parity = 0;
+  for (int64_t task = wid; task < ntask; task += wstride) {
     float accf0 = 0.0f, accf1 = 0.0f;     // lanes t == 0: columns c0, c1
-    const int last = nsteps - 1;
-    // register ring of kPF k-steps in flight per lane (plus the L2 256-byte prefetch)
-    uint4 ring0[kPF], ring1[kPF];
+    for (int kc = 0, c = 0; kc < npad; kc += spc, ++c) {
+      const int kend = min(kc + spc, npad);
+      int acc[P][4];
 #pragma unroll
-    for (int j = 0; j < kPF; ++j) {
-      const int64_t o = (int64_t)min(j, last) * 1024;
-      ring0[j] = ld_stream_u4_l2pf(p0 + o);
-      ring1[j] = ld_stream_u4_l2pf(p1 + o);
-    }
-    int acc[4] = {0, 0, 0, 0};
-    int cstep = 0, chunk = 0;                 // position inside the current fixed-point chunk
-
-    // one k-step on ring slot j: extract A fragments, optionally refill the slot, load B
-    // fragments from shared memory, 2P MMAs, flush the chunk when it ends
-    auto step = [&](uint4& s0, uint4& s1, int ks, bool refill) {
-      uint32_t af[NMMA][4];
+      for (int j = 0; j < P; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
+      for (int ks0 = kc; ks0 < kend; ks0 += kReq) {
+        mbar_wait(bar_w + 8 * slot, parity);    // the kReq tile-steps of this request landed
 #pragma unroll
-      for (int u = 0; u < NMMA; ++u) {
-        af[u][0] = byte_reg<B>(s0, 2 * u);
-        af[u][1] = byte_reg<B>(s1, 2 * u);
-        af[u][2] = byte_reg<B>(s0, 2 * u + 1);
-        af[u][3] = byte_reg<B>(s1, 2 * u + 1);
-      }
-      if (refill) {   // same registers, consumed above: nothing waits on this load for kPF steps
-        const int64_t o = (int64_t)min(ks + kPF, last) * 1024;
-        s0 = ld_stream_u4_l2pf(p0 + o);
-        s1 = ld_stream_u4_l2pf(p1 + o);
-      }
-      uint32_t bw[4 * P];
-      if (bload) {
-        const uint4* bp = reinterpret_cast<const uint4*>(limb_n + (size_t)(ks * 4 + t) * (16 * P));
+        for (int h = 0; h < kReq; ++h) {
+          const int ks = ks0 + h;
+          const uint32_t src = ring_w + slot * kSlot + h * 1024 + g8 * 64 + t * 16;
+          const uint4 s0 = lds128(src), s1 = lds128(src + 512);
+          uint32_t bw[4 * P];
 #pragma unroll
-        for (int q = 0; q < P; ++q) {
-          const uint4 v = bp[q];
-          bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
+          for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
+          if (bload) {
+            const uint32_t bp = limb_n + (uint32_t)(ks * 4 + t) * (16 * P);
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+              const uint4 v = lds128(bp + 16 * q);
+              bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
+            }
+          }
+          uint32_t af[NMMA][4];          // MMA u = 2 j + m: words 2m (k-slots 0..15), 2m+1 (16..31)
+#pragma unroll
+          for (int j = 0; j < P; ++j)
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+              af[2 * j + m][0] = frag_reg<B>(s0, 2 * m, j);
+              af[2 * j + m][1] = frag_reg<B>(s1, 2 * m, j);
+              af[2 * j + m][2] = frag_reg<B>(s0, 2 * m + 1, j);
+              af[2 * j + m][3] = frag_reg<B>(s1, 2 * m + 1, j);
+            }
+          if (h == kReq - 1) {
+            __syncwarp();                        // every lane has its fragments: slot is free
+            request(slot);                       // refill it with the request kRing later
+          }
+#pragma unroll
+          for (int u = 0; u < NMMA; ++u) mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
         }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < NMMA; ++u) mma_u8s8(acc, af[u], bw[2 * u], bw[2 * u + 1]);
-      if (++cstep == steps_per_chunk || ks + 1 == nsteps) {
-        // flush chunk: lane t=0 holds limbs 0,1 (cols 0,1); lane t=1 holds limb 2 (col 2)
-        const int c = chunk++;
-        cstep = 0;
-        const int l2r0 = __shfl_down_sync(0xffffffffu, acc[0], 1);
-        const int l2r1 = __shfl_down_sync(0xffffffffu, acc[2], 1);
-        if (t == 0) {
-          const long long S = Sc[c];
-          const double sc = ldexp(1.0, -Fc[c]);
-          const long long V0 = (long long)acc[0] + 256ll * acc[1] + 65536ll * l2r0;
-          const long long V1 = (long long)acc[2] + 256ll * acc[3] + 65536ll * l2r1;
-          accf0 += (float)((double)(2 * V0 - (long long)(a.L - 1) * S) * sc);
-          accf1 += (float)((double)(2 * V1 - (long long)(a.L - 1) * S) * sc);
+        if (++slot == kRing) {
+          slot = 0;
+          parity ^= 1u;
         }
-        acc[0] = acc[1] = acc[2] = acc[3] = 0;
       }
-    };
-
-    const int nmain = nsteps / kPF * kPF;
-    for (int ks0 = 0; ks0 < nmain; ks0 += kPF) {
+      // flush chunk c: combine bit-positions exactly (every term of acc_j is a multiple of
+      // 2^{B j}); lane t=0 holds limbs 0,1 (cols 0,1), lane t=1 holds limb 2 (col 2)
+      int v00 = 0, v01 = 0, v10 = 0, v11 = 0;
 #pragma unroll
-      for (int j = 0; j < kPF; ++j) step(ring0[j], ring1[j], ks0 + j, true);
+      for (int j = 0; j < P; ++j) {
+        v00 += acc[j][0] >> (B * j);
+        v01 += acc[j][1] >> (B * j);
+        v10 += acc[j][2] >> (B * j);
+        v11 += acc[j][3] >> (B * j);
+      }
+      const int l2r0 = __shfl_down_sync(0xffffffffu, v00, 1);
+      const int l2r1 = __shfl_down_sync(0xffffffffu, v10, 1);
+      if (t == 0) {
+        const long long S = Sc[c];
+        const double sc = ldexp(1.0, -Fc[c]);
+        const long long V0 = (long long)v00 + 256ll * v01 + 65536ll * l2r0;
+        const long long V1 = (long long)v10 + 256ll * v11 + 65536ll * l2r1;
+        accf0 += (float)((double)(2 * V0 - (long long)(a.L - 1) * S) * sc);
+        accf1 += (float)((double)(2 * V1 - (long long)(a.L - 1) * S) * sc);
+      }
     }
-#pragma unroll
-    for (int j = 0; j < kPF; ++j)          // drain: the last nsteps - nmain steps sit in slots 0..
-      if (nmain + j < nsteps) step(ring0[j], ring1[j], nmain + j, false);
+    const int64_t c0 = task * 16 + g8, c1 = c0 + 8;
     if (t == 0) {
       if (a.nK == 1) {
-        if (v0) a.g[c0] = a.sigma * accf0;
-        if (v1) a.g[c1] = a.sigma * accf1;
+        if (c0 < a.N) a.g[c0] = a.sigma * accf0;
+        if (c1 < a.N) a.g[c1] = a.sigma * accf1;
       } else {
-        if (v0) a.g[(int64_t)kr * a.N + c0] = accf0;
-        if (v1) a.g[(int64_t)kr * a.N + c1] = accf1;
+        if (c0 < a.N) a.g[(int64_t)kr * a.N + c0] = accf0;
+        if (c1 < a.N) a.g[(int64_t)kr * a.N + c1] = accf1;
       }
     }
   }
@@ -348,16 +431,19 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   const int64_t warps_full = (int64_t)num_sms * kMmaWarps;
   // K-range: as large as fits (<= kMaxKR), but split K when there are too few column
   // tasks to give every warp of the GPU several tasks.
+  // K-ranges and chunks are whole multiples of 1024 rows so that every chunk holds a
+  // multiple of kPF k-steps for b = 2, 4, 8 (k-step = 512/b rows)
   int64_t KR = min64(Rpad, kMaxKR);
-  KR = (KR + 255) / 256 * 256;
-  while (KR > 1024 && ntask * ((Rpad + KR - 1) / KR) < 4 * warps_full) KR = (KR / 2 + 255) / 256 * 256;
+  KR = (KR + 1023) / 1024 * 1024;
+  while (KR > 1024 && ntask * ((Rpad + KR - 1) / KR) < 4 * warps_full) KR = (KR / 2 + 1023) / 1024 * 1024;
   p.KR = (int)KR;
-  p.KC = (int)min64(KR, kChunkRows);
-  while (p.KR % p.KC) p.KC -= 256;    // KC divides KR, multiple of 256
+  int d = 4;                            // KC = 1024 d <= kChunkRows, dividing KR
+  while ((KR / 1024) % d) --d;
+  p.KC = 1024 * d;
   p.nK = (int)((Rpad + KR - 1) / KR);
   p.limb_stride = p.KR + 64;
   const int nchunks = p.KR / p.KC;
-  p.smem = (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(long long) * nchunks +
+  p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(long long) * nchunks +
            sizeof(float) * nchunks * kMmaWarps;
   int per_sm = (int)(size_t)min64(4, (size_t)(227 * 1024) / p.smem);
   if (per_sm < 1) per_sm = 1;
