@@ -111,62 +111,6 @@ def make_problem(args):
     return p
 
 
-def build_pool(p, rank, world, dev, dist_on):
-    """Generate (config 4: on the device, block-wise) and quantise this rank's row shard
-    of Phi into the pool of K copies.  Returns (pool, c_phi, preprocess timings)."""
-    import torch
-    from paper_1802_04907_b200 import iht
-    assert p.M % world == 0, "row sharding needs M divisible by the GPU count"
-    rows = p.M // world
-    row0 = rank * rows
-    t = {}
-    st = torch.cuda.current_stream()
-    if p.phi is None:
-        from workloads.gpu import gauss_fill
-        blk = max(256, ((2 << 30) // (p.N * 4)) // 256 * 256)
-        buf = torch.empty((min(blk, rows), p.N), dtype=torch.float32, device=dev)
-        cmax = torch.zeros(1, dtype=torch.float32, device=dev)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for r in range(0, rows, blk):
-            n = min(blk, rows - r)
-            view = buf[:n]
-            gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
-            cmax = torch.maximum(cmax, iht.absmax(view))
-        torch.cuda.synchronize()
-        t["gen_absmax_ms"] = (time.perf_counter() - t0) * 1e3
-    else:
-        phi = torch.from_numpy(p.phi[row0:row0 + rows]).to(dev)
-        t0 = time.perf_counter()
-        cmax = iht.absmax(phi)
-        torch.cuda.synchronize()
-        t["absmax_ms"] = (time.perf_counter() - t0) * 1e3
-    if dist_on:
-        import torch.distributed as dist
-        dist.all_reduce(cmax, op=dist.ReduceOp.MAX)
-    c = float(cmax.item())
-    pool = [iht.new_copy(rows, p.N, p.planes, p.b_phi, 0, p.seed, k, c, row_offset=row0, device=dev)
-            for k in range(p.K)]
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if p.phi is None:
-        for r in range(0, rows, blk):
-            n = min(blk, rows - r)
-            view = buf[:n]
-            gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
-            for k0 in range(0, p.K, 8):
-                iht.quantize_rows(view, pool[k0:k0 + 8], r)
-        del buf
-    else:
-        for k0 in range(0, p.K, 8):
-            iht.quantize_rows(phi, pool[k0:k0 + 8], 0)
-        del phi
-    torch.cuda.synchronize()
-    t["quantize_ms"] = (time.perf_counter() - t0) * 1e3
-    torch.cuda.empty_cache()
-    return pool, c, t, rows, row0
-
-
 # ----------------------------------------------------------------------------- CPU oracle
 def oracle_sample(p, steps=None):
     """Time the float64 oracle (as it stands) on bounded samples of the workload: the
@@ -258,6 +202,7 @@ def main():
 
     t_setup = time.perf_counter()
     p = make_problem(args)
+    from paper_1802_04907_b200.problem import build_pool
     pool, c_phi, prep, rows, row0 = build_pool(p, rank, world, dev, dist_on)
     y_shard = p.y[row0:row0 + rows]
     y_dev = torch.from_numpy(y_shard).to(dev)

@@ -117,10 +117,10 @@ __global__ void __launch_bounds__(256) adjoint_ffma_kernel(const uint8_t* __rest
 // =====================================================================================
 // Variant 0: int8 mma.sync path
 // =====================================================================================
-constexpr int kMmaWarps = 16;          // warps per CTA
+constexpr int kMmaWarps = 8;           // warps per CTA
 constexpr int kChunkRows = 4096;       // rows per fixed-point chunk (int32-safe flush)
 constexpr int kMaxKR = 32768;          // rows of r limbs resident in shared memory per CTA
-constexpr int kReq = 2;                // k-steps (1 KiB tile-steps) per bulk request
+constexpr int kReq = 4;                // k-steps (1 KiB tile-steps) per bulk request
 constexpr int kRing = 3;               // requests in flight per warp (shared-memory ring slots)
 constexpr int kSlot = kReq * 1024;     // bytes per ring slot
 
@@ -196,7 +196,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t smem_addr) {
 //   [ring]  kMmaWarps x kRing slots x 1 KiB: each lane's two 16-byte code chunks of a k-step
 //           (a lane only ever reads back what it copied itself)
 //   [limbs] 3 planes x limb_stride bytes: r in 3 signed 8-bit limbs, permuted per lane chunk
-//   [Fc, Sc, red] per-chunk exponents, exact integer sums of r_int, reduction scratch
+//   [Fc, Sl, red] per-chunk exponents, exact per-limb integer sums of r_int, scratch
 template <int B>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs a) {
   constexpr int P = 8 / B;               // codes per byte
@@ -209,8 +209,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMmaWarps * kRing * kSlot);   // [warp][slot]
   uint8_t* limbs = smem + kMmaWarps * kRing * kSlot + kMmaWarps * kRing * 8;
   int* Fc = reinterpret_cast<int*>(limbs + 3 * a.limb_stride);
-  long long* Sc = reinterpret_cast<long long*>(Fc + ((nchunks + 1) & ~1));
-  float* red = reinterpret_cast<float*>(Sc + nchunks);     // [nchunks][kMmaWarps] scratch
+  int* Sl = Fc + ((nchunks + 1) & ~1);                     // [chunk][3] limb sums of r_int
+  float* red = reinterpret_cast<float*>(Sl + 3 * nchunks);  // [nchunks][kMmaWarps] scratch
 
   const int kr = blockIdx.y;
   const int64_t row0 = (int64_t)kr * a.KR;
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
     int e = 0;
     if (m > 0.0f) frexpf(m, &e);            // m in [2^{e-1}, 2^e)
     Fc[c] = (m > 0.0f) ? min(22 - e, 126) : 0;   // |r| 2^F < 2^22 (clamped for tiny r)
-    Sc[c] = 0;
+    Sl[3 * c] = Sl[3 * c + 1] = Sl[3 * c + 2] = 0;
   }
   __syncthreads();
   // ---- prologue 2: r -> three balanced signed 8-bit limbs, permuted per lane chunk -----
@@ -314,8 +314,16 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
       *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
       *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
       *reinterpret_cast<uint32_t*>(limbs + 2 * a.limb_stride + off) = l2w;
-      const long long sv = (long long)s0 + 256ll * s1 + 65536ll * s2;
-      atomicAdd(reinterpret_cast<unsigned long long*>(&Sc[c]), (unsigned long long)sv);
+      // the 32 items of a warp lie in one chunk (128 consecutive rows): one native int32
+      // atomic per limb and warp (|sum| <= 128 x 4096 per chunk)
+      s0 = __reduce_add_sync(0xffffffffu, s0);
+      s1 = __reduce_add_sync(0xffffffffu, s1);
+      s2 = __reduce_add_sync(0xffffffffu, s2);
+      if (lane == 0) {
+        atomicAdd(&Sl[3 * c], s0);
+        atomicAdd(&Sl[3 * c + 1], s1);
+        atomicAdd(&Sl[3 * c + 2], s2);
+      }
     }
   }
   __syncthreads();
@@ -388,7 +396,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
       const int l2r0 = __shfl_down_sync(0xffffffffu, v00, 1);
       const int l2r1 = __shfl_down_sync(0xffffffffu, v10, 1);
       if (t == 0) {
-        const long long S = Sc[c];
+        const long long S = (long long)Sl[3 * c] + 256ll * Sl[3 * c + 1] + 65536ll * Sl[3 * c + 2];
         const double sc = ldexp(1.0, -Fc[c]);
         const long long V0 = (long long)v00 + 256ll * v01 + 65536ll * l2r0;
         const long long V1 = (long long)v10 + 256ll * v11 + 65536ll * l2r1;
@@ -443,7 +451,7 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   p.nK = (int)((Rpad + KR - 1) / KR);
   p.limb_stride = p.KR + 64;
   const int nchunks = p.KR / p.KC;
-  p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(long long) * nchunks +
+  p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
            sizeof(float) * nchunks * kMmaWarps;
   int per_sm = (int)(size_t)min64(4, (size_t)(227 * 1024) / p.smem);
   if (per_sm < 1) per_sm = 1;

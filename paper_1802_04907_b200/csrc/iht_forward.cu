@@ -7,15 +7,15 @@
 // streams s * R * b / 8 bytes (0.4% of the adjoint's bytes at config 4).
 //
 // Mapping: a CTA owns a window of 32 consecutive 32-bit code words of every strip
-// (32 * 32/b stacked rows); its 8 warps split the support in rounds of 8 columns
+// (32 * 32/b stacked rows); its 16 warps split the support in rounds of 16 columns
 // (loads issued before use), each lane accumulates the 32/b rows of its word, and the 8
 // partial sums are added in a fixed order through shared memory (deterministic).
 #include "iht_internal.cuh"
 
 namespace iht {
 
-constexpr int kFwdWarps = 8;
-constexpr int kFwdUnroll = 8;
+constexpr int kFwdWarps = 16;
+constexpr int kFwdUnroll = 16;
 
 template <int B>
 __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(
 #pragma unroll
   for (int i = 0; i < CPW; ++i) part[warp][lane][i] = acc[i];
   __syncthreads();
-  // warp 0 combines the 8 partials in fixed order
+  // warp 0 combines the kFwdWarps partials in fixed order
   if (warp == 0 && live) {
 #pragma unroll
     for (int i = 0; i < CPW; ++i) {

@@ -1,0 +1,72 @@
+"""Set up a problem's quantised pool on the device (one-time per operator; not timed).
+
+Generates (config 4: on the device, block-wise, never resident) and quantises this
+rank's row shard of Phi into the pool of K copies, with the global scale c all-reduced
+across ranks (reading c3).  Used by bench.py and by the full-size parity tests, so the
+tests exercise exactly the configuration the bench times.
+"""
+import time
+
+
+def shard_rows(M, world, rank):
+    """Row shard of rank `rank` (north star: Phi sharded by rows).  Requires M % world == 0
+    and shards that are whole 256-row blocks (so the block-wise quantiser can write them)."""
+    if M % world:
+        raise ValueError("row sharding needs M divisible by the GPU count")
+    rows = M // world
+    return rows, rank * rows
+
+
+def build_pool(p, rank, world, dev, dist_on):
+    """Generate (config 4: on the device, block-wise) and quantise this rank's row shard
+    of Phi into the pool of K copies.  Returns (pool, c_phi, preprocess timings)."""
+    import torch
+    from . import iht
+    rows, row0 = shard_rows(p.M, world, rank)
+    t = {}
+    if p.phi is None:
+        from workloads.gpu import gauss_fill
+        blk = max(256, ((2 << 30) // (p.N * 4)) // 256 * 256)
+        buf = torch.empty((min(blk, rows), p.N), dtype=torch.float32, device=dev)
+        cmax = torch.zeros(1, dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for r in range(0, rows, blk):
+            n = min(blk, rows - r)
+            view = buf[:n]
+            gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
+            cmax = torch.maximum(cmax, iht.absmax(view))
+        torch.cuda.synchronize()
+        t["gen_absmax_ms"] = (time.perf_counter() - t0) * 1e3
+    else:
+        phi = torch.from_numpy(p.phi[row0:row0 + rows]).to(dev)
+        t0 = time.perf_counter()
+        cmax = iht.absmax(phi)
+        torch.cuda.synchronize()
+        t["absmax_ms"] = (time.perf_counter() - t0) * 1e3
+    if dist_on:
+        import torch.distributed as dist
+        dist.all_reduce(cmax, op=dist.ReduceOp.MAX)
+    c = float(cmax.item())
+    pool = [iht.new_copy(rows, p.N, p.planes, p.b_phi, 0, p.seed, k, c, row_offset=row0, device=dev)
+            for k in range(p.K)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if p.phi is None:
+        for r in range(0, rows, blk):
+            n = min(blk, rows - r)
+            view = buf[:n]
+            gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
+            for k0 in range(0, p.K, 8):
+                iht.quantize_rows(view, pool[k0:k0 + 8], r)
+        del buf
+    else:
+        for k0 in range(0, p.K, 8):
+            iht.quantize_rows(phi, pool[k0:k0 + 8], 0)
+        del phi
+    torch.cuda.synchronize()
+    t["quantize_ms"] = (time.perf_counter() - t0) * 1e3
+    torch.cuda.empty_cache()
+    return pool, c, t, rows, row0
+
+
