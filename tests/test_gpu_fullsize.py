@@ -62,7 +62,7 @@ def test_config2_codes_and_teacher_forced(config2):
     c_ref = OQ.scale_c(p.phi)
     assert np.float32(c) == c_ref
     copies = {}
-    for cid in (0, 1, 2):
+    for cid in (0, 1, 2, 3):           # iterations 1, 2 use copies 0..3 (adjoint 2n-2, forward 2n-1)
         ref, _ = OQ.quantize_matrix(p.phi, p.b_phi, 0, p.seed, cid, c=c_ref)
         got = _tile_codes(pool[cid], p.M, p.N, 1, p.b_phi, 0, p.M, 0, p.N)
         np.testing.assert_array_equal(got, ref)
