@@ -168,6 +168,18 @@ IHT_API int64_t iht_adjoint_ws_bytes(const iht_qmat* A);
 IHT_API int iht_adjoint(const iht_qmat* A, const float* r_dev, float* g_dev, int variant, void* ws_dev,
                 int64_t ws_bytes, void* stream);
 
+/* ------------------------------------------- (a7) batched adjoint (tcgen05) */
+/* B = nrhs observations sharing one Phi (BASELINE config 5): G[b][n] =
+ * Re(Phi-hat_A^H r_b)_n for all snapshots at once, as an int8 tcgen05 GEMM
+ * (kind::i8, M = 128 pixels, N = 2 nrhs): codes expanded to u8 in shared memory, r_b
+ * in per-snapshot block fixed point (two signed 8-bit limbs, 15 bits), exact int32
+ * accumulation in TMEM.  Tolerance class: the tensor-core path (1e-3, north star).
+ * R: nrhs stacked vectors [nrhs][iht_vec_len] (pads 0); G: [nrhs][cols] floats.
+ * Requires 2 nrhs a multiple of 16 and <= 256.  Workspace: iht_adjoint_batched_ws_bytes. */
+IHT_API int64_t iht_adjoint_batched_ws_bytes(const iht_qmat* A, int32_t nrhs);
+IHT_API int iht_adjoint_batched(const iht_qmat* A, const float* R_dev, int32_t nrhs, float* G_dev,
+                                void* ws_dev, int64_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------- (a6) update + H_s */
 /* a = x + mu g, then H_s: keep the s entries of largest |a|,
  * ties to the LOWEST index, zeros never kept (reading c15).  Output

@@ -59,6 +59,8 @@ SIGNATURES = {
     "iht_forward": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "iht_adjoint_ws_bytes": (c_i64, [ctypes.POINTER(IhtQmat)]),
     "iht_adjoint": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_vp, c_int, c_vp, c_i64, c_vp]),
+    "iht_adjoint_batched_ws_bytes": (c_i64, [ctypes.POINTER(IhtQmat), c_i32]),
+    "iht_adjoint_batched": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
     "iht_threshold_ws_bytes": (c_i64, [c_i64, c_i32]),
     "iht_threshold": (c_int, [c_vp, c_vp, c_vp, c_vp, c_f32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "iht_comm_unique_id": (c_int, [c_vp]),

@@ -1,0 +1,450 @@
+// (a7) batched observations sharing one Phi (BASELINE config 5): the adjoint of B
+// snapshots at once, G = sigma Q_A^T R (G: N x B, R: R_pad x B), as a tcgen05 GEMM.
+//
+// P:349 applied per snapshot; only here is the work a dense contraction (north star:
+// "for batched observations sharing one Phi, a tcgen05 tensor-core path").
+//
+// GEMM  D[n, j] = sum_k A[n, k] Bm[j, k]   (tcgen05.mma.cta_group::1.kind::i8, M=128,
+//       N = 2B, K = 32 per instruction, s32 accumulators in TMEM)
+//   A  = codes as u8 (pixels x stacked rows), expanded in shared memory from the packed
+//        tiled layout by converter warps into the canonical K-major SWIZZLE_128B layout;
+//   Bm = r in per-snapshot block fixed point, two signed 8-bit limbs per snapshot
+//        (column j = 2b + limb), prepared once per call as a pre-swizzled image.
+//   g[b][n] = sigma 2^{-F_b} (2 (D[n,2b] + 256 D[n,2b+1]) - (L-1) S_b)
+// Exact integer products/accumulation; the only rounding is r's 15-bit fixed point per
+// snapshot (tolerance 1e-3 on this path, north star) and the final float.
+//
+// K order inside a 16-byte u8 chunk is permuted (row(p) below) identically on A and B.
+//
+// Roles per CTA (320 threads): warps 0-3 convert packed codes -> u8 stage; warp 4 issues
+// the MMAs (one thread); warp 5 issues the bulk copies (packed codes, B image);
+// warps 6-9 run the epilogue (TMEM -> registers -> g).  TMEM is double-buffered so the
+// epilogue of tile t overlaps the MMAs of tile t+1.
+#include "iht_internal.cuh"
+
+namespace iht {
+
+constexpr int kBT = 128;               // pixels per GEMM tile (M)
+constexpr int kBStages = 3;            // A/B operand stages
+constexpr int kPkSlots = 4;            // packed-code staging slots
+constexpr int kBThreads = 320;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init2(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive2(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx2(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait2(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s2(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+// SWIZZLE_128B K-major shared-memory matrix descriptor (CUTLASS SmemDescriptor layout):
+// start>>4 [0,14), LBO>>4 [16,30) (=1, unused for swizzled K-major), SBO>>4 [32,46)
+// (=1024 B between 8-row groups), version 1 at bit 46, layout type 2 (SW128) at [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// instruction descriptor: kind::i8, A u8, B s8, D s32, both K-major, M, N
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// byte offset of (row, 16-byte K chunk q) in a K-major SW128 tile whose rows hold KBB
+// bytes: atoms of 128 rows x 128 B (16 KiB) along K, 8-row groups at 1024 B.
+__host__ __device__ inline uint32_t sw128_off(int row, int q, int rows_total) {
+  const int a = q >> 3, c = q & 7;
+  return (uint32_t)(a * rows_total * 128 + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4));
+}
+
+// K permutation inside a 16-byte u8 chunk (shared by A and B): position p (0..15) <-> row
+// offset (32/b) h + j + P i, with p = 4 (h P + j) + i (h: packed word, j: bit-position,
+// i: byte).
+__host__ __device__ inline int perm_row(int p, int bits) {
+  const int P = 8 / bits, cpw = 32 / bits;
+  const int i = p & 3, g = p >> 2;   // g = h P + j
+  const int h = g / P, j = g % P;
+  return cpw * h + j + P * i;
+}
+
+struct BatchArgs {
+  const uint8_t* codes;
+  int64_t strip_bytes;
+  int64_t N;
+  int Rpad;
+  int nkb;                 // K-blocks (tile-steps) = Rpad / (512/b)
+  int ntiles;              // ceil(N / 128)
+  int B;                   // snapshots (2B <= 256)
+  int L;
+  float sigma;
+  const uint8_t* bimg;     // [nkb][KBB*2B] pre-swizzled limb image
+  const int* Fb;           // [B] exponents
+  const int* Sb;           // [B][2] limb sums
+  float* g;                // [B][N]
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs a) {
+  constexpr int TS = BITS == 8 ? 2 : 1;  // tile-steps per K-block (>= 128 u8 bytes per row)
+  constexpr int KBR = TS * 512 / BITS;   // rows per K-block
+  constexpr int KBB = KBR;               // u8 bytes per row per K-block
+  constexpr int CH = KBB / 16;           // 16-byte chunks per row
+  constexpr int NKS = KBB / 32;          // MMAs (K = 32) per K-block
+  constexpr int PK = 8 * TS * 1024;      // packed bytes per K-block (8 column tiles x TS KiB)
+  constexpr int ASZ = kBT * KBB;         // A stage bytes
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int NB = 2 * a.B;                 // MMA N (snapshot-limb columns), multiple of 16
+  const int BSZ = NB * KBB;               // B stage bytes
+  uint8_t* sA = smem;                                   // [kBStages][ASZ]
+  uint8_t* sB = sA + kBStages * ASZ;                    // [kBStages][BSZ]  (BSZ multiple of 1024)
+  uint8_t* sP = sB + kBStages * BSZ;                    // [kPkSlots][PK]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kPkSlots * PK);
+  uint64_t* pk_full = bar;                  // [kPkSlots]  tx
+  uint64_t* pk_free = bar + kPkSlots;       // [kPkSlots]  4 converter warps
+  uint64_t* a_full = bar + 2 * kPkSlots;    // [kBStages]  4 converter warps
+  uint64_t* b_full = a_full + kBStages;     // [kBStages]  tx
+  uint64_t* st_free = b_full + kBStages;    // [kBStages]  tcgen05.commit
+  uint64_t* acc_full = st_free + kBStages;  // [2]         tcgen05.commit
+  uint64_t* acc_free = acc_full + 2;        // [2]         4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPkSlots; ++i) {
+      mbar_init2(smem_u32(&pk_full[i]), 1);
+      mbar_init2(smem_u32(&pk_free[i]), 4);
+    }
+    for (int i = 0; i < kBStages; ++i) {
+      mbar_init2(smem_u32(&a_full[i]), 4);
+      mbar_init2(smem_u32(&b_full[i]), 1);
+      mbar_init2(smem_u32(&st_free[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init2(smem_u32(&acc_full[i]), 1);
+      mbar_init2(smem_u32(&acc_free[i]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {   // TMEM: 2 accumulator buffers of NB columns (power of two >= 32)
+    const uint32_t cols = NB <= 64 ? 128 : (NB <= 128 ? 256 : 512);
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t acc_stride = NB <= 64 ? 64 : (NB <= 128 ? 128 : 256);   // columns per buffer
+
+  if (warp < 4) {
+    // ---------------------------------------------------------------- converters
+    const int n = warp * 32 + lane;              // pixel row inside the tile (0..127)
+    const int ct = n >> 4, cc = n & 15;           // column tile / column inside the tile
+    int64_t i = 0;                                // global K-block counter of this CTA
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      for (int kb = 0; kb < a.nkb; ++kb, ++i) {
+        const int ps = (int)(i % kPkSlots), ss = (int)(i % kBStages);
+        mbar_wait2(smem_u32(&pk_full[ps]), (uint32_t)((i / kPkSlots) & 1));
+        if (i >= kBStages) mbar_wait2(smem_u32(&st_free[ss]), (uint32_t)(((i - kBStages) / kBStages) & 1));
+        uint8_t* dst = sA + ss * ASZ;
+#pragma unroll
+        for (int ts = 0; ts < TS; ++ts) {
+          const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;   // 64 packed bytes
+          const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
+                               reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
+          const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
+                                  w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
+          constexpr int CHT = CH / TS;       // chunks per tile-step
+#pragma unroll
+          for (int qq = 0; qq < CHT; ++qq) {
+            const int q = ts * CHT + qq;
+            uint4 o;
+            if (BITS == 2) {            // chunk = packed word qq (16 codes)
+              const uint32_t x = w[qq];
+              o = make_uint4(x & 0x03030303u, (x >> 2) & 0x03030303u, (x >> 4) & 0x03030303u, (x >> 6) & 0x03030303u);
+            } else if (BITS == 4) {     // chunk = packed words 2qq, 2qq+1
+              const uint32_t x0 = w[2 * qq], x1 = w[2 * qq + 1];
+              o = make_uint4(x0 & 0x0F0F0F0Fu, (x0 >> 4) & 0x0F0F0F0Fu, x1 & 0x0F0F0F0Fu, (x1 >> 4) & 0x0F0F0F0Fu);
+            } else {                    // chunk = packed words 4qq..4qq+3 (bytes)
+              o = make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+            }
+            *reinterpret_cast<uint4*>(dst + sw128_off(n, q, kBT)) = o;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive2(smem_u32(&pk_free[ps]));
+          mbar_arrive2(smem_u32(&a_full[ss]));
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = idesc_i8(kBT, NB);
+    int64_t i = 0;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+      const int ab = t & 1;
+      if (t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dtm = tmem + ab * acc_stride;
+      for (int kb = 0; kb < a.nkb; ++kb, ++i) {
+        const int ss = (int)(i % kBStages);
+        const uint32_t ph = (uint32_t)((i / kBStages) & 1);
+        mbar_wait2(smem_u32(&a_full[ss]), ph);
+        mbar_wait2(smem_u32(&b_full[ss]), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t abase = smem_u32(sA + ss * ASZ), bbase = smem_u32(sB + ss * BSZ);
+#pragma unroll
+          for (int kk = 0; kk < NKS; ++kk) {
+            const uint64_t ad = sw128_desc(abase + (kk >> 2) * (kBT * 128) + (kk & 3) * 32);
+            const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (NB * 128) + (kk & 3) * 32);
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+                : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&st_free[ss]))
+                       : "memory");
+          if (kb == a.nkb - 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&acc_full[ab]))
+                         : "memory");
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------------------------------------------------------- producer
+    if (lane == 0) {
+      int64_t i = 0;
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        for (int kb = 0; kb < a.nkb; ++kb, ++i) {
+          const int ps = (int)(i % kPkSlots), ss = (int)(i % kBStages);
+          if (i >= kPkSlots) mbar_wait2(smem_u32(&pk_free[ps]), (uint32_t)(((i - kPkSlots) / kPkSlots) & 1));
+          mbar_expect_tx2(smem_u32(&pk_full[ps]), PK);
+          for (int ct = 0; ct < 8; ++ct) {
+            int64_t col_tile = (int64_t)tile * 8 + ct;                // 16-column tile index
+            const int64_t last_tile = (a.N + 15) / 16 - 1;
+            if (col_tile > last_tile) col_tile = last_tile;            // past N: any valid data
+            bulk_g2s2(smem_u32(sP + ps * PK + ct * (TS * 1024)),
+                      a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb * TS * 1024, TS * 1024,
+                      smem_u32(&pk_full[ps]));
+          }
+          if (i >= kBStages) mbar_wait2(smem_u32(&st_free[ss]), (uint32_t)(((i - kBStages) / kBStages) & 1));
+          mbar_expect_tx2(smem_u32(&b_full[ss]), (uint32_t)BSZ);
+          bulk_g2s2(smem_u32(sB + ss * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&b_full[ss]));
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 6-9)
+    const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
+    int t = 0;
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+      const int ab = t & 1;
+      mbar_wait2(smem_u32(&acc_full[ab]), (uint32_t)((t >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t n = (int64_t)tile * kBT + quarter * 32 + lane;
+      const uint32_t taddr = tmem + ab * acc_stride + ((uint32_t)(quarter * 32) << 16);
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (n < a.N) {
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const int b = (c0 + e) >> 1;
+            const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
+            const long long S = (long long)a.Sb[2 * b] + 256ll * a.Sb[2 * b + 1];
+            const double val = (double)(2 * V - (long long)(a.L - 1) * S) * ldexp(1.0, -a.Fb[b]);
+            a.g[(int64_t)b * a.N + n] = a.sigma * (float)val;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive2(smem_u32(&acc_free[ab]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 4) {
+    const uint32_t cols = NB <= 64 ? 128 : (NB <= 128 ? 256 : 512);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols) : "memory");
+  }
+}
+
+// Per-snapshot block fixed point of R (one CTA per snapshot): F_b from max |r|, two
+// balanced signed limbs written into the pre-swizzled image, exact limb sums S_b.
+template <int BITS>
+__global__ void batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nkb,
+                                     uint8_t* __restrict__ bimg, int* __restrict__ Fb, int* __restrict__ Sb) {
+  constexpr int KBR = (BITS == 8 ? 2 : 1) * 512 / BITS;
+  const int b = blockIdx.x;
+  const float* r = R + (int64_t)b * Rpad;
+  __shared__ float red[32];
+  __shared__ int ired[2][32];
+  __shared__ int Fs;
+  float m = 0.0f;
+  for (int i = threadIdx.x; i < Rpad; i += blockDim.x) m = fmaxf(m, fabsf(r[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mm = 0.0f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
+    int e = 0;
+    if (mm > 0.0f) frexpf(mm, &e);
+    Fs = mm > 0.0f ? min(14 - e, 126) : 0;          // |r| 2^F < 2^14 -> two limbs
+    Fb[b] = Fs;
+  }
+  __syncthreads();
+  const float scale = ldexpf(1.0f, Fs);
+  const int NB = 2 * B;
+  int s0 = 0, s1 = 0;
+  for (int row = threadIdx.x; row < nkb * KBR; row += blockDim.x) {
+    const float rv = row < Rpad ? r[row] : 0.0f;
+    const int ri = __float2int_rn(rv * scale);
+    const int l0 = ((ri + 128) & 255) - 128;
+    const int l1 = (ri - l0) >> 8;
+    s0 += l0;
+    s1 += l1;
+    // K position of this row inside its K-block (inverse of perm_row per 16-row chunk)
+    const int kb = row / KBR, rr = row % KBR;
+    const int q = rr >> 4;
+    int p = 0;
+    for (int pp = 0; pp < 16; ++pp)
+      if (perm_row(pp, BITS) == (rr & 15)) p = pp;
+    uint8_t* blk = bimg + (int64_t)kb * NB * KBR;
+    blk[sw128_off(2 * b, q, NB) + p] = (uint8_t)(l0 & 255);
+    blk[sw128_off(2 * b + 1, q, NB) + p] = (uint8_t)(l1 & 255);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ired[0][threadIdx.x >> 5] = s0;
+    ired[1][threadIdx.x >> 5] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a0 = 0, a1 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a0 += ired[0][w];
+      a1 += ired[1][w];
+    }
+    Sb[2 * b] = a0;
+    Sb[2 * b + 1] = a1;
+  }
+}
+
+static int kb_rows(int bits) { return (bits == 8 ? 2 : 1) * 512 / bits; }
+
+static size_t batched_smem(int bits, int B) {
+  const int KBB = kb_rows(bits), TS = bits == 8 ? 2 : 1;
+  return 1024 + (size_t)kBStages * kBT * KBB + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * TS * 1024 +
+         (size_t)(2 * kPkSlots + 3 * kBStages + 4) * 8 + 16;
+}
+
+}  // namespace iht
+
+using namespace iht;
+
+extern "C" int64_t iht_adjoint_batched_ws_bytes(const iht_qmat* A, int32_t nrhs) {
+  if (A == nullptr || nrhs <= 0) return -1;
+  const int64_t Rpad = A->planes * rows_pad(A->rows);
+  const int KBR = kb_rows(A->bits);
+  const int64_t nkb = (Rpad + KBR - 1) / KBR;
+  return nkb * 2 * nrhs * KBR + 256 + 3 * nrhs * 4 + 256;
+}
+
+extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nrhs, float* G, void* ws,
+                                   int64_t ws_bytes, void* stream) {
+  if (A == nullptr || R == nullptr || G == nullptr || nrhs <= 0) return IHT_EINVAL;
+  if (A->codes == nullptr || (A->bits != 2 && A->bits != 4 && A->bits != 8)) return IHT_EINVAL;
+  if (A->strip_bytes != iht_strip_bytes(A->rows, A->planes, A->bits)) return IHT_EINVAL;
+  if ((2 * nrhs) % 16 != 0 || 2 * nrhs > 256) return IHT_EUNSUPPORTED;   // MMA N = 2 nrhs
+  const int64_t Rpad = A->planes * rows_pad(A->rows);
+  const int L = num_levels(A->bits, A->level_mode);
+  if ((double)Rpad * (L - 1) * 128.0 >= 2147483647.0) return IHT_EUNSUPPORTED;   // int32 accumulator
+  const int64_t need = iht_adjoint_batched_ws_bytes(A, nrhs);
+  if (ws == nullptr || ws_bytes < need) return IHT_EINVAL;
+  const int KBR = kb_rows(A->bits);
+  const int nkb = (int)(Rpad / KBR);        // Rpad is a multiple of 256 rows per plane
+  if (nkb * KBR != Rpad) return IHT_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* bimg = static_cast<uint8_t*>(ws);
+  const int64_t bimg_bytes = (int64_t)nkb * 2 * nrhs * KBR;
+  int* Fb = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + (bimg_bytes + 255) / 256 * 256);
+  int* Sb = Fb + nrhs;
+  BatchArgs b{};
+  b.codes = static_cast<const uint8_t*>(A->codes);
+  b.strip_bytes = A->strip_bytes;
+  b.N = A->cols;
+  b.Rpad = (int)Rpad;
+  b.nkb = nkb;
+  b.ntiles = (int)((A->cols + kBT - 1) / kBT);
+  b.B = nrhs;
+  b.L = L;
+  b.sigma = A->scale_c / (float)(L - 1);
+  b.bimg = bimg;
+  b.Fb = Fb;
+  b.Sb = Sb;
+  b.g = G;
+  int dev = 0, sms = kNumSMs;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = batched_smem(A->bits, nrhs);
+  if (smem > 227 * 1024) return IHT_EUNSUPPORTED;
+#define IHT_BATCH(BB)                                                                                  \
+  do {                                                                                                 \
+    batched_limbs_kernel<BB><<<nrhs, 256, 0, st>>>(R, (int)Rpad, nrhs, nkb, bimg, Fb, Sb);            \
+    IHT_LAUNCH_CHECK();                                                                                \
+    static bool attr = false;                                                                          \
+    if (!attr) {                                                                                       \
+      IHT_CUDA_CHECK(cudaFuncSetAttribute(adjoint_batched_kernel<BB>,                                  \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));   \
+      attr = true;                                                                                     \
+    }                                                                                                  \
+    adjoint_batched_kernel<BB><<<min(b.ntiles, sms), kBThreads, smem, st>>>(b);                        \
+    IHT_LAUNCH_CHECK();                                                                                \
+  } while (0)
+  if (A->bits == 2) IHT_BATCH(2);
+  else if (A->bits == 4) IHT_BATCH(4);
+  else IHT_BATCH(8);
+#undef IHT_BATCH
+  return IHT_OK;
+}

@@ -15,7 +15,7 @@ import torch
 from . import _lib
 from ._lib import IhtConfig, IhtQmat, check, load
 
-__all__ = ["absmax", "quantize", "quantize_rows", "quantize_vec", "forward", "adjoint", "threshold", "Solver", "solve",
+__all__ = ["absmax", "quantize", "quantize_rows", "quantize_vec", "forward", "adjoint", "adjoint_batched", "threshold", "Solver", "solve",
            "Comm", "QCopy", "strip_bytes", "vec_len", "rows_pad"]
 
 
@@ -160,6 +160,20 @@ def adjoint(A, r, variant=0, stream=None, out=None):
     check(lib.iht_adjoint(ctypes.byref(A.desc), _ptr(r), _ptr(g), variant, _ptr(ws), ws_bytes, _stream(stream)),
           "iht_adjoint")
     return g
+
+
+def adjoint_batched(A, R, stream=None):
+    """(a7) G = Re(Phi-hat_A^H R) for B snapshots at once (tcgen05 int8 GEMM).
+    R: (B, vec_len) float32 CUDA tensor; returns G (B, N) float32."""
+    _require_cuda(R)
+    lib = load()
+    B = R.shape[0]
+    ws_bytes = lib.iht_adjoint_batched_ws_bytes(ctypes.byref(A.desc), B)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=R.device)
+    G = torch.empty((B, A.cols), dtype=torch.float32, device=R.device)
+    check(lib.iht_adjoint_batched(ctypes.byref(A.desc), _ptr(R), B, _ptr(G), _ptr(ws), ws_bytes, _stream(stream)),
+          "iht_adjoint_batched")
+    return G
 
 
 def threshold(x_idx, x_val, x_nnz, g, mu, s, stream=None):
