@@ -175,7 +175,7 @@ IHT_API int iht_adjoint(const iht_qmat* A, const float* r_dev, float* g_dev, int
  * in per-snapshot block fixed point (two signed 8-bit limbs, 15 bits), exact int32
  * accumulation in TMEM.  Tolerance class: the tensor-core path (1e-3, north star).
  * R: nrhs stacked vectors [nrhs][iht_vec_len] (pads 0); G: [nrhs][cols] floats.
- * Requires 2 nrhs a multiple of 16 and <= 256.  Workspace: iht_adjoint_batched_ws_bytes. */
+ * Requires 2 nrhs a multiple of 16 and <= 128.  Workspace: iht_adjoint_batched_ws_bytes. */
 IHT_API int64_t iht_adjoint_batched_ws_bytes(const iht_qmat* A, int32_t nrhs);
 IHT_API int iht_adjoint_batched(const iht_qmat* A, const float* R_dev, int32_t nrhs, float* G_dev,
                                 void* ws_dev, int64_t ws_bytes, void* stream);

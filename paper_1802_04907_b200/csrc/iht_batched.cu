@@ -109,13 +109,12 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   constexpr int CH = KBB / 16;           // 16-byte chunks per row
   constexpr int NKS = KBB / 32;          // MMAs (K = 32) per K-block
   constexpr int PK = 8 * TS * 1024;      // packed bytes per K-block (8 column tiles x TS KiB)
-  constexpr int ASZ = kBT * KBB;         // A stage bytes
+  constexpr int ACOLS = KBB / 4;         // TMEM columns of one A stage (4 u8 per column)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NB = 2 * a.B;                 // MMA N (snapshot-limb columns), multiple of 16
   const int BSZ = NB * KBB;               // B stage bytes
-  uint8_t* sA = smem;                                   // [kBStages][ASZ]
-  uint8_t* sB = sA + kBStages * ASZ;                    // [kBStages][BSZ]  (BSZ multiple of 1024)
+  uint8_t* sB = smem;                                   // [kBStages][BSZ]  (BSZ multiple of 1024)
   uint8_t* sP = sB + kBStages * BSZ;                    // [kPkSlots][PK]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kPkSlots * PK);
   uint64_t* pk_full = bar;                  // [kPkSlots]  tx
@@ -126,6 +125,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   uint64_t* acc_full = st_free + kBStages;  // [2]         tcgen05.commit
   uint64_t* acc_free = acc_full + 2;        // [2]         4 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
+  float* ep_scale = reinterpret_cast<float*>(tmem_slot + 4);            // [B] sigma 2^-F_b
+  long long* ep_off = reinterpret_cast<long long*>(ep_scale + 256);    // [B] (L-1) S_b
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -144,8 +145,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {   // TMEM: 2 accumulator buffers of NB columns (power of two >= 32)
-    const uint32_t cols = NB <= 64 ? 128 : (NB <= 128 ? 256 : 512);
+  if (warp == 4) {   // TMEM: 2 accumulator buffers (NB <= 128 columns each) + kBStages A stages
+    const uint32_t cols = 512;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(cols)
                  : "memory");
@@ -155,7 +156,13 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t acc_stride = NB <= 64 ? 64 : (NB <= 128 ? 128 : 256);   // columns per buffer
+  const uint32_t acc_stride = 128;                                      // columns per accumulator
+  const uint32_t a_col0 = 256;                                          // first A-stage column
+  for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
+    ep_scale[b] = a.sigma * ldexpf(1.0f, -a.Fb[b]);
+    ep_off[b] = (long long)(a.L - 1) * ((long long)a.Sb[2 * b] + 256ll * a.Sb[2 * b + 1]);
+  }
+  __syncthreads();
 
   if (warp < 4) {
     // ---------------------------------------------------------------- converters
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         const int ps = (int)(i % kPkSlots), ss = (int)(i % kBStages);
         mbar_wait2(smem_u32(&pk_full[ps]), (uint32_t)((i / kPkSlots) & 1));
         if (i >= kBStages) mbar_wait2(smem_u32(&st_free[ss]), (uint32_t)(((i - kBStages) / kBStages) & 1));
-        uint8_t* dst = sA + ss * ASZ;
+        uint32_t out[ACOLS];              // this pixel row's KBB u8 bytes, 4 per TMEM column
 #pragma unroll
         for (int ts = 0; ts < TS; ++ts) {
           const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;   // 64 packed bytes
@@ -175,24 +182,43 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                                reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
           const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
                                   w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
-          constexpr int CHT = CH / TS;       // chunks per tile-step
+          constexpr int CHT = CH / TS;       // 16-byte chunks per tile-step
 #pragma unroll
           for (int qq = 0; qq < CHT; ++qq) {
             const int q = ts * CHT + qq;
-            uint4 o;
             if (BITS == 2) {            // chunk = packed word qq (16 codes)
               const uint32_t x = w[qq];
-              o = make_uint4(x & 0x03030303u, (x >> 2) & 0x03030303u, (x >> 4) & 0x03030303u, (x >> 6) & 0x03030303u);
+              out[4 * q + 0] = x & 0x03030303u;
+              out[4 * q + 1] = (x >> 2) & 0x03030303u;
+              out[4 * q + 2] = (x >> 4) & 0x03030303u;
+              out[4 * q + 3] = (x >> 6) & 0x03030303u;
             } else if (BITS == 4) {     // chunk = packed words 2qq, 2qq+1
               const uint32_t x0 = w[2 * qq], x1 = w[2 * qq + 1];
-              o = make_uint4(x0 & 0x0F0F0F0Fu, (x0 >> 4) & 0x0F0F0F0Fu, x1 & 0x0F0F0F0Fu, (x1 >> 4) & 0x0F0F0F0Fu);
+              out[4 * q + 0] = x0 & 0x0F0F0F0Fu;
+              out[4 * q + 1] = (x0 >> 4) & 0x0F0F0F0Fu;
+              out[4 * q + 2] = x1 & 0x0F0F0F0Fu;
+              out[4 * q + 3] = (x1 >> 4) & 0x0F0F0F0Fu;
             } else {                    // chunk = packed words 4qq..4qq+3 (bytes)
-              o = make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+              out[4 * q + 0] = w[4 * qq];
+              out[4 * q + 1] = w[4 * qq + 1];
+              out[4 * q + 2] = w[4 * qq + 2];
+              out[4 * q + 3] = w[4 * qq + 3];
             }
-            *reinterpret_cast<uint4*>(dst + sw128_off(n, q, kBT)) = o;
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // A stage ss lives in TMEM columns a_col0 + ss * ACOLS .. ; lane = pixel row n
+        const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+        for (int c0 = 0; c0 < ACOLS; c0 += 16)
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                  ta + (uint32_t)c0),
+              "r"(out[c0]), "r"(out[c0 + 1]), "r"(out[c0 + 2]), "r"(out[c0 + 3]), "r"(out[c0 + 4]), "r"(out[c0 + 5]),
+              "r"(out[c0 + 6]), "r"(out[c0 + 7]), "r"(out[c0 + 8]), "r"(out[c0 + 9]), "r"(out[c0 + 10]),
+              "r"(out[c0 + 11]), "r"(out[c0 + 12]), "r"(out[c0 + 13]), "r"(out[c0 + 14]), "r"(out[c0 + 15])
+              : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
           mbar_arrive2(smem_u32(&pk_free[ps]));
@@ -217,16 +243,15 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         mbar_wait2(smem_u32(&b_full[ss]), ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          const uint32_t abase = smem_u32(sA + ss * ASZ), bbase = smem_u32(sB + ss * BSZ);
+          const uint32_t atm = tmem + a_col0 + (uint32_t)(ss * ACOLS), bbase = smem_u32(sB + ss * BSZ);
 #pragma unroll
           for (int kk = 0; kk < NKS; ++kk) {
-            const uint64_t ad = sw128_desc(abase + (kk >> 2) * (kBT * 128) + (kk & 3) * 32);
             const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (NB * 128) + (kk & 3) * 32);
             const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtm),
-                "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtm),
+                "r"(atm + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc), "r"(acc)
                 : "memory");
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -286,9 +311,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           for (int e = 0; e < 16; e += 2) {
             const int b = (c0 + e) >> 1;
             const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
-            const long long S = (long long)a.Sb[2 * b] + 256ll * a.Sb[2 * b + 1];
-            const double val = (double)(2 * V - (long long)(a.L - 1) * S) * ldexp(1.0, -a.Fb[b]);
-            a.g[(int64_t)b * a.N + n] = a.sigma * (float)val;
+            a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
           }
         }
       }
@@ -301,8 +324,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 4) {
-    const uint32_t cols = NB <= 64 ? 128 : (NB <= 128 ? 256 : 512);
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
 }
 
@@ -375,8 +397,8 @@ static int kb_rows(int bits) { return (bits == 8 ? 2 : 1) * 512 / bits; }
 
 static size_t batched_smem(int bits, int B) {
   const int KBB = kb_rows(bits), TS = bits == 8 ? 2 : 1;
-  return 1024 + (size_t)kBStages * kBT * KBB + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * TS * 1024 +
-         (size_t)(2 * kPkSlots + 3 * kBStages + 4) * 8 + 16;
+  return 1024 + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * TS * 1024 +
+         (size_t)(2 * kPkSlots + 3 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
 }
 
 }  // namespace iht
@@ -396,7 +418,7 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
   if (A == nullptr || R == nullptr || G == nullptr || nrhs <= 0) return IHT_EINVAL;
   if (A->codes == nullptr || (A->bits != 2 && A->bits != 4 && A->bits != 8)) return IHT_EINVAL;
   if (A->strip_bytes != iht_strip_bytes(A->rows, A->planes, A->bits)) return IHT_EINVAL;
-  if ((2 * nrhs) % 16 != 0 || 2 * nrhs > 256) return IHT_EUNSUPPORTED;   // MMA N = 2 nrhs
+  if ((2 * nrhs) % 16 != 0 || 2 * nrhs > 128) return IHT_EUNSUPPORTED;   // MMA N = 2 nrhs <= 128
   const int64_t Rpad = A->planes * rows_pad(A->rows);
   const int L = num_levels(A->bits, A->level_mode);
   if ((double)Rpad * (L - 1) * 128.0 >= 2147483647.0) return IHT_EUNSUPPORTED;   // int32 accumulator
