@@ -26,6 +26,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -39,13 +41,24 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--bits", type=int, default=None, help="override b_Phi (2/4/8 sweep)")
     ap.add_argument("--K", type=int, default=None, help="pool of quantised copies")
     ap.add_argument("--variant", type=int, default=0, help="adjoint: 0 int8 MMA, 1 FFMA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+def measured_tensor_peak_int8():
+    """Dense int8 tensor peak (TOP/s): the measured bf16 peak x the nominal int8/bf16 ratio
+    (4.5 / 2.25 = 2, B200_PROFILING.md).  Burst figure: the kernel is timed per launch."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return 2.0 * float(d["bf16_tflops"]), "measured bf16 x 2 (nominal int8/bf16 ratio)"
+    except Exception:
+        return 4500.0, "nominal"
 
 
 def measured_peaks():
@@ -130,10 +143,11 @@ def oracle_sample(p, steps=None):
     r0 = max(1, min(p.M // 2, (1 << 23) // (p.N * p.planes)))
     r0 = 1 << int(np.floor(np.log2(r0)))
     n_it = 3 if steps is None else max(1, steps)
+    B = p.meta.get("batch_y").shape[1] if "batch_y" in p.meta else 1
     times = []
     for rows in (r0, 2 * r0):
         phi = p.phi_rows(0, rows)
-        y = p.y[:rows]
+        y = p.meta["batch_y"][:rows, 0] if B > 1 else p.y[:rows]
         pool = OI.CopyPool(phi, p.b_phi, 0, p.seed, OQ.scale_c(phi), cache=2)
         pool.dequantized(0)                                   # one-time preprocess
         t0 = time.perf_counter()
@@ -141,12 +155,13 @@ def oracle_sample(p, steps=None):
         times.append((time.perf_counter() - t0) / n_it)
     b = max((times[1] - times[0]) / r0, 0.0)
     a = max(times[0] - b * r0, 0.0)
-    per_iter = a + b * p.M
+    per_iter = (a + b * p.M) * B
     return {"value": 1.0 / per_iter, "unit": "iter/s", "cores": threads, "kind": "oracle",
             "sample": f"rows 0..{r0 - 1} and 0..{2 * r0 - 1} of {p.M}, all {p.N} columns, K=1 copy, "
                       f"{n_it} float64 iterations each (copy quantisation excluded); per-iteration time "
                       f"fitted a + b*rows ({times[0] * 1e3:.1f} / {times[1] * 1e3:.1f} ms) and extrapolated "
-                      f"to {p.M} rows",
+                      f"to {p.M} rows" + (f", one snapshot timed and multiplied by the batch B={B} "
+                                          f"(the oracle runs snapshots independently)" if B > 1 else ""),
             "host_cores": os.cpu_count()}
 
 
@@ -202,12 +217,16 @@ def main():
 
     t_setup = time.perf_counter()
     p = make_problem(args)
+    B = p.meta["batch_y"].shape[1] if "batch_y" in p.meta else 1
     from paper_1802_04907_b200.problem import build_pool
-    pool, c_phi, prep, rows, row0 = build_pool(p, rank, world, dev, dist_on)
-    y_shard = p.y[row0:row0 + rows]
+    pool, c_phi, prep, rows, row0 = build_pool(p, rank, world, dev, dist_on, shard="cols" if B > 1 else "rows")
+    if B > 1:        # (B, M) observations, replicated on every column shard
+        y_shard = np.ascontiguousarray(p.meta["batch_y"].T)
+    else:
+        y_shard = p.y[row0:row0 + rows]
     y_dev = torch.from_numpy(y_shard).to(dev)
     sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, adjoint_variant=args.variant, comm=comm,
-                     profile=True)
+                     profile=True, nrhs=B)
     setup_s = time.perf_counter() - t_setup
 
     # ---- device-resident timed region -----------------------------------------------
@@ -234,16 +253,17 @@ def main():
     ms = max_over_ranks(e0.elapsed_time(e1))
     adj_ms = sol.adjoint_times_ms()
     out_idx, out_val, out_nnz = sol.out_idx, sol.out_val, sol.out_nnz
-    nnz = int(out_nnz.item())
+    nnz = [int(v) for v in out_nnz.cpu()]
     launches_per_run = sol.launches_per_run()
 
     # ---- end-to-end through the public API with host buffers --------------------------
     e2e = None
     if not args.no_e2e:
         y_pin = torch.from_numpy(y_shard.copy()).pin_memory()
-        oi = torch.empty(p.s, dtype=torch.int32).pin_memory()
-        ov = torch.empty(p.s, dtype=torch.float32).pin_memory()
-        on = torch.empty(1, dtype=torch.int32).pin_memory()
+        oshape = (B, p.s) if B > 1 else (p.s,)
+        oi = torch.empty(oshape, dtype=torch.int32).pin_memory()
+        ov = torch.empty(oshape, dtype=torch.float32).pin_memory()
+        on = torch.empty(B, dtype=torch.int32).pin_memory()
         sol.run_host(y_pin, oi, ov, on)
         barrier()
         t0 = time.perf_counter()
@@ -252,23 +272,35 @@ def main():
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         yb = y_pin.numel() * y_pin.element_size() * (2 if y_pin.is_complex() else 1)
         e2e = {"value": args.steps * p.n_iter / e2e_s, "unit": "iter/s",
-               "h2d_bytes_per_step": int(yb), "d2h_bytes_per_step": int(p.s * 8 + 4),
+               "h2d_bytes_per_step": int(yb), "d2h_bytes_per_step": int(B * (p.s * 8 + 4)),
                "path": "iht_solver_run(IHT_HOST_IO): pinned y -> device, solve, x -> pinned host, sync"}
 
     # ---- bookkeeping --------------------------------------------------------------------
     peak, peak_kind = measured_peaks()
+    ncols = pool[0].cols                                       # this rank's columns
     strip = iht.strip_bytes(rows, p.planes, p.b_phi)
-    copy_bytes = iht._lib.load().iht_qmat_bytes(rows, p.N, p.planes, p.b_phi)
+    copy_bytes = iht._lib.load().iht_qmat_bytes(rows, ncols, p.planes, p.b_phi)
     R = iht.vec_len(rows, p.planes)
-    adj_bytes = copy_bytes + 4 * R + 4 * p.N                  # codes + r read + g write
-    fwd_bytes = p.s * strip + 4 * R + 4 * R                    # support strips + yhat + r
-    thr_bytes = 4 * p.N * 2 + 8 * p.s                          # g read + a write (+ x)
+    adj_bytes = copy_bytes + B * (4 * R + 4 * ncols)          # codes + r read + g write
+    fwd_bytes = B * (p.s * strip + 4 * R + 4 * R)              # support strips + yhat + r
+    thr_bytes = B * (4 * ncols * 2 + 8 * p.s)                  # g read + a write (+ x)
     iter_bytes = adj_bytes + fwd_bytes + thr_bytes
     iters = args.steps * p.n_iter
     value = iters / (ms / 1e3)
     adj_avg = statistics.mean(adj_ms)
     adj_gbs = adj_bytes / (adj_avg / 1e3) / 1e9
     stream_gbs = iter_bytes * iters / (ms / 1e3) / 1e9     # per GPU
+    if B > 1:   # (a7) tensor-core bound: algorithmic int8 ops 2 R N B (one multiply-add per code per snapshot)
+        tpeak, tpeak_kind = measured_tensor_peak_int8()
+        adj_ops = 2.0 * R * ncols * B
+        roof = {"bound": "tensor", "kernel": "adjoint_batched_kernel (+ batched_limbs_kernel)",
+                "achieved": adj_ops / (adj_avg / 1e3) / 1e12, "peak": tpeak, "unit": "TOP/s",
+                "frac": adj_ops / (adj_avg / 1e3) / 1e12 / tpeak, "peak_kind": tpeak_kind,
+                "traffic": None, "algorithmic_ops_per_launch": adj_ops,
+                "executed_int8_ops_per_launch": 2 * adj_ops, "avg_launch_ms": adj_avg,
+                "launches_timed": len(adj_ms), "code_bytes_per_launch": copy_bytes,
+                "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside the "
+                       "solver graph, last timed step; ops = 2 R N B useful (x2 executed: two int8 limbs of r)"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "adjoint_traffic.json")
     if os.path.exists(tp):
@@ -295,20 +327,26 @@ def main():
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "s8/s32 int8-MMA adjoint, f32 forward/update",
+        "dtype": ("u8 x s8 -> s32 tcgen05 (kind::i8) batched adjoint" if B > 1 else
+                  "s8/s32 int8-MMA adjoint") + ", f32 forward/update",
         "data": "synthetic",
         "config": {
             "workload": f"{p.name}: {'complex radio' if p.complex else 'real Gaussian'} {p.M}x{p.N}, "
-                        f"{p.b_phi}-bit Phi, {p.b_y}-bit y, s={p.s}, n*={p.n_iter}, mu={p.mu:g}, K={p.K} copies",
+                        f"{p.b_phi}-bit Phi, {p.b_y}-bit y, s={p.s}, n*={p.n_iter}, mu={p.mu:g}, K={p.K} copies"
+                        + (f", B={B} snapshots per iteration (one iter = all B)" if B > 1 else ""),
             "M": p.M, "N": p.N, "b_phi": p.b_phi, "b_y": p.b_y, "s": p.s, "n_iter": p.n_iter, "K": p.K,
-            "parallelism": f"row-sharded x{world}" + (", NCCL all-reduce of g per iteration" if world > 1 else ""),
+            "batch": B,
+            "parallelism": (f"column-sharded x{world}" + (", NCCL all-reduce of r + all-gather of top-s candidates"
+                                                          if world > 1 else "") if B > 1 else
+                            f"row-sharded x{world}" + (", NCCL all-reduce of g per iteration" if world > 1 else "")),
             "l2": f"inputs > L2: pool {p.K * copy_bytes / 2**30:.2f} GiB per GPU streamed from HBM"
                   if p.K * copy_bytes > 126e6 else f"pool {p.K * copy_bytes / 2**20:.1f} MiB is L2-resident",
             "adjoint_variant": args.variant,
         },
         "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
                 "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},
-        "roofline": {"bound": "hbm", "kernel": "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
+        "roofline": roof if B > 1 else
+                    {"bound": "hbm", "kernel": "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
                      "achieved": adj_gbs, "peak": peak, "unit": "GB/s", "frac": adj_gbs / peak,
                      "peak_kind": peak_kind, "traffic": traffic,
                      "algorithmic_bytes_per_launch": adj_bytes, "avg_launch_ms": adj_avg,
@@ -319,7 +357,8 @@ def main():
         "gpu_launches": int(launches_per_run * args.steps),
         "clocks": clocks,
         "preprocess": {**prep, "c_phi": c_phi, "setup_s": setup_s},
-        "result": {"support_size": nnz},
+        "result": {"support_size": nnz if B > 1 else nnz[0]},
+        "snapshot_iter_per_s": value * B,
         "context": PAPER_CONTEXT,
     }
     print(json.dumps(line))

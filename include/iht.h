@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define IHT_ABI_VERSION 1
+#define IHT_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define IHT_API __attribute__((visibility("default")))
@@ -101,7 +101,10 @@ typedef struct {
   int32_t copy_id;     /* Philox counter word 2: which independent copy      */
   uint64_t seed;       /* Philox key                                                 */
   float scale_c;       /* c = max |component| over the WHOLE Phi, all shards */
-  int32_t reserved;
+  int32_t col_offset;  /* global index of this shard's first column (column sharding of
+                          the batched path); a multiple of 16; 0 otherwise.
+                          Philox counters use the global column col_offset + n, so codes
+                          do not depend on the sharding                               */
   int64_t strip_bytes; /* must equal iht_strip_bytes(rows, planes, bits)             */
   void* codes;         /* device, iht_qmat_bytes(rows, cols, planes, bits) bytes     */
 } iht_qmat;
@@ -113,6 +116,11 @@ typedef struct {
  * (device).  A NaN anywhere makes the result NaN (caller maps it to
  * IHT_EDOMAIN).  Deterministic. */
 IHT_API int iht_absmax(const float* src_dev, int64_t count, float* c_dev, void* stream);
+/* Batched form: nrhs independent vectors of `count` floats each, back to back in
+ * src_dev; c_dev[b] = max |src_dev[b * count + i]| (each observation has its own
+ * scale c_y, P:686 applied per snapshot). */
+IHT_API int iht_absmax_batched(const float* src_dev, int64_t count, int32_t nrhs, float* c_dev,
+                               void* stream);
 
 /* ------------------------------------------------------- (a2) quantise Phi */
 /* Stochastically quantise the rows x cols block src (row-major, row stride ld
@@ -122,9 +130,10 @@ IHT_API int iht_absmax(const float* src_dev, int64_t count, float* c_dev, void* 
  *   sf = fl32((L-1) / fl32(2c)); t = clamp(fl32(fl32(v + c) * sf), 0, L-1);
  *   i = floor t; code = L-1 if i = L-1 else i + (u < t - i),
  *   u = (w >> 8) 2^-24, w = Philox4x32-10 word (n & 3) of counter
- *   (n >> 2, row_offset + m, copy_id, (plane << 8) | 0), key (lo32 seed, hi32 seed).
+ *   (n >> 2, row_offset + m, copy_id, (plane << 8) | 0), key (lo32 seed, hi32 seed),
+ *   with n = col_offset + local column (global column index).
  * dst[k] describes copy k (same rows/cols/planes/bits/level_mode/scale_c/
- * row_offset for all k; own copy_id, seed, codes).  Errors: IHT_EINVAL on
+ * row_offset/col_offset for all k; own copy_id, seed, codes).  Errors: IHT_EINVAL on
  * inconsistent descriptors. */
 IHT_API int iht_quantize(const float* src_dev, int64_t ld, const iht_qmat* dst, int ncopies,
                  void* stream);
@@ -146,6 +155,14 @@ IHT_API int iht_quantize_rows(const float* src_dev, int64_t ld, const iht_qmat* 
 IHT_API int iht_quantize_vec(const float* y_dev, int64_t rows, int64_t row_offset, int planes, int bits,
                      int level_mode, uint64_t seed, const float* c_dev, float* yhat_dev,
                      uint8_t* codes_dev, void* stream);
+/* Batched form (config 5): nrhs observations y_b, each rows * planes floats (complex
+ * interleaved), back to back in y_dev; scales c_dev[b]; output yhat_dev [nrhs][vec_len].
+ * Snapshot b is column n = b of the observation matrix Y = [y_0 .. y_{B-1}]: element m
+ * of plane p draws word (b & 3) of counter (b >> 2, row_offset + m, 0, (p << 8) | 1),
+ * so b = 0 reproduces iht_quantize_vec exactly.  codes_dev (optional): [nrhs][planes*rows]. */
+IHT_API int iht_quantize_vec_batched(const float* y_dev, int64_t rows, int64_t row_offset, int planes,
+                                     int bits, int level_mode, uint64_t seed, const float* c_dev,
+                                     int32_t nrhs, float* yhat_dev, uint8_t* codes_dev, void* stream);
 
 /* ------------------------------------------------------------ (a4) forward */
 /* r = y-hat - Phi-hat_F x for s-sparse real x ("matrix times a sparse
@@ -157,6 +174,15 @@ IHT_API int64_t iht_forward_ws_bytes(const iht_qmat* F, int32_t max_nnz);
 IHT_API int iht_forward(const iht_qmat* F, const int32_t* x_idx_dev, const float* x_val_dev,
                 const int32_t* x_nnz_dev, int32_t max_nnz, const float* yhat_dev, float* r_dev,
                 void* ws_dev, int64_t ws_bytes, void* stream);
+/* Batched form (config 5): nrhs sparse iterates x_b (x_idx_dev / x_val_dev [nrhs][ldx],
+ * x_nnz_dev [nrhs], at most min(ldx, max_nnz) entries each, GLOBAL column indices),
+ * yhat_dev / r_dev [nrhs][vec_len].  Only support entries inside this shard's columns
+ * [F->col_offset, F->col_offset + F->cols) contribute (column sharding); yhat_dev may
+ * be NULL, giving the partial product r_b = -Phi-hat_F[:, S_b] x_b that the column-
+ * sharded solver all-reduces. */
+IHT_API int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx_dev, const float* x_val_dev,
+                                const int32_t* x_nnz_dev, int32_t ldx, int32_t max_nnz, int32_t nrhs,
+                                const float* yhat_dev, float* r_dev, void* stream);
 
 /* ------------------------------------------------------------ (a5) adjoint */
 /* g = Re(Phi-hat_A^H r) for all N columns: g_n = sigma_A sum_m
@@ -175,7 +201,10 @@ IHT_API int iht_adjoint(const iht_qmat* A, const float* r_dev, float* g_dev, int
  * in per-snapshot block fixed point (two signed 8-bit limbs, 15 bits), exact int32
  * accumulation in TMEM.  Tolerance class: the tensor-core path (1e-3, north star).
  * R: nrhs stacked vectors [nrhs][iht_vec_len] (pads 0); G: [nrhs][cols] floats.
- * Requires 2 nrhs a multiple of 16 and <= 128.  Workspace: iht_adjoint_batched_ws_bytes. */
+ * Any nrhs >= 1: snapshots run in chunks of <= 64 (one launch pair each), a chunk padded
+ * to a multiple of 8 with zero residuals inside the workspace (MMA N granularity 16).
+ * Workspace: iht_adjoint_batched_ws_bytes.  Errors: IHT_EUNSUPPORTED if the int32
+ * accumulator could overflow (rows * planes * (L-1) * 128 >= 2^31). */
 IHT_API int64_t iht_adjoint_batched_ws_bytes(const iht_qmat* A, int32_t nrhs);
 IHT_API int iht_adjoint_batched(const iht_qmat* A, const float* R_dev, int32_t nrhs, float* G_dev,
                                 void* ws_dev, int64_t ws_bytes, void* stream);
@@ -192,6 +221,29 @@ IHT_API int iht_threshold(const int32_t* x_idx_dev, const float* x_val_dev, cons
                   const float* g_dev, float mu, int32_t s, int64_t N, int32_t* out_idx_dev,
                   float* out_val_dev, int32_t* out_nnz_dev, void* ws_dev, int64_t ws_bytes,
                   void* stream);
+/* Batched form: nrhs independent selections (config 5, H_s per snapshot).  x_* as in
+ * iht_forward_batched (stride ldx, GLOBAL indices); g_dev [nrhs][N] holds the gradient of
+ * the N local columns [col_offset, col_offset + N); entries of x outside that range are
+ * ignored, output indices are global (col_offset + local).  out_idx_dev / out_val_dev
+ * [nrhs][ldo] (ldo >= s), out_nnz_dev [nrhs].  With col_offset = 0 and the whole N this
+ * is exactly nrhs calls of iht_threshold; on a column shard it yields the shard's local
+ * top-s candidates, whose merge over shards is the global H_s. */
+IHT_API int64_t iht_threshold_batched_ws_bytes(int64_t N, int32_t s, int32_t nrhs);
+IHT_API int iht_threshold_batched(const int32_t* x_idx_dev, const float* x_val_dev, const int32_t* x_nnz_dev,
+                                  int32_t ldx, const float* g_dev, float mu, int32_t s, int64_t N,
+                                  int64_t col_offset, int32_t nrhs, int32_t* out_idx_dev, float* out_val_dev,
+                                  int32_t ldo, int32_t* out_nnz_dev, void* ws_dev, int64_t ws_bytes,
+                                  void* stream);
+/* Merge of per-shard candidate lists into the global H_s (column-sharded batched path):
+ * for each snapshot b, the concatenation over shards p = 0..P-1 of shard p's list
+ * (cand_idx/cand_val[p * shard_stride + b * s + j], j < cand_nnz[p * shard_stride + b];
+ * shard p's indices increasing and below shard p+1's; strides in 4-byte elements) is
+ * thresholded to its top s (ties to the lowest index; P * s <= 8192), written to
+ * out_* [nrhs][s] and out_nnz [nrhs] (-1 if any shard reported -1). */
+IHT_API int iht_merge_candidates(const int32_t* cand_idx_dev, const float* cand_val_dev,
+                                 const int32_t* cand_nnz_dev, int64_t shard_stride, int32_t P, int32_t s,
+                                 int32_t nrhs, int32_t* out_idx_dev, float* out_val_dev, int32_t* out_nnz_dev,
+                                 void* stream);
 
 /* --------------------------------------------------------- multi-GPU comm */
 /* One NCCL communicator per rank (row-sharded Phi, north star).
@@ -205,6 +257,9 @@ IHT_API int iht_comm_create(int rank, int world, const void* id_host_128, int de
 IHT_API int iht_comm_destroy(iht_comm* comm);
 /* In-place sum / max all-reduce of `count` floats on the stream (test hook). */
 IHT_API int iht_comm_allreduce(iht_comm* comm, float* buf_dev, int64_t count, int op_max, void* stream);
+/* All-gather of `bytes` bytes per rank: recv_dev[p * bytes ..] = rank p's send_dev. */
+IHT_API int iht_comm_allgather(iht_comm* comm, const void* send_dev, void* recv_dev, int64_t bytes,
+                               void* stream);
 
 /* ------------------------------------------------------------ (b) solver */
 typedef struct {
@@ -219,7 +274,13 @@ typedef struct {
   int32_t use_graph;    /* 1: capture the n_iter loop into one CUDA graph (default)      */
   iht_comm* comm;       /* NULL: single GPU; else g is all-reduced (sum) every iteration */
   int32_t profile;      /* 1: record a CUDA event pair around every adjoint launch      */
-  int32_t reserved;
+  int32_t nrhs;         /* B independent observations sharing Phi (BASELINE config 5);
+                           0 or 1: one observation.  B > 1 runs the batched path: sparse
+                           forward per snapshot, the tcgen05 adjoint (iht_adjoint_batched),
+                           per-snapshot H_s.  With a communicator (world P >= 1) the
+                           batched path is COLUMN-sharded (pool[k].col_offset = rank N/P):
+                           forward partials all-reduced (sum), local H_s candidates
+                           all-gathered and merged                         */
 } iht_config;
 
 /* Stateful solver over a pool of K quantised copies pool[0..K) (all with the
@@ -239,16 +300,22 @@ IHT_API int iht_solver_destroy(iht_solver* solver);
  * (all-reduced max across ranks), y-hat = Q(y), then n_iter iterations of
  * forward -> adjoint -> [all-reduce g] -> update + H_s.  Writes the final
  * support (<= s indices, increasing) and values, and *out_nnz (device or host
- * per flags).  Returns IHT_EDOMAIN if a non-finite value reached H_s. */
+ * per flags).  Returns IHT_EDOMAIN if a non-finite value reached H_s.
+ * Batched (cfg.nrhs = B > 1): y holds B observations back to back ([B][rows * planes]
+ * floats; each snapshot has its own c_y and Q(y), iht_quantize_vec_batched), and the
+ * outputs are out_idx / out_val [B][s], out_nnz [B].  Column-sharded runs (P > 1) take
+ * the FULL y on every rank and return the same (replicated) x on every rank. */
 IHT_API int iht_solver_run(iht_solver* solver, const float* y, int flags, int32_t* out_idx,
                    float* out_val, int32_t* out_nnz, void* stream);
 /* Copy the recorded iterates (cfg.trace = 1) of the last run to host arrays:
  * idx_host/val_host of n_iter * s entries (row n-1 = x^[n+1] after iteration
- * n), nnz_host of n_iter entries.  Synchronises the stream. */
+ * n), nnz_host of n_iter entries; batched: n_iter * B * s and n_iter * B
+ * ([n-1][b][.]).  Synchronises the stream. */
 IHT_API int iht_solver_trace(iht_solver* solver, int32_t* idx_host, float* val_host, int32_t* nnz_host,
                      void* stream);
 /* Device pointers of the internal stacked vectors of the LAST iteration
- * (r, y-hat) and of g, for parity tests; lengths iht_vec_len(rows, planes) / N. */
+ * (r, y-hat) and of g, for parity tests; lengths iht_vec_len(rows, planes) / N
+ * (batched: [B][vec_len] and [B][N]). */
 IHT_API int iht_solver_buffers(iht_solver* solver, const float** yhat_dev, const float** r_dev,
                        const float** g_dev);
 /* With cfg.profile = 1: durations (ms) of the n_iter adjoint launches of the LAST

@@ -119,17 +119,19 @@ class CopyPool:
 
 
 def qniht(phi, y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True,
-          x0=None, pool=None):
+          x0=None, pool=None, snapshot=0):
     """Algorithm 1 with fixed step mu; returns QnihtResult.
 
     phi: float32 (M x N) or complex64 array; y: float32 / complex64 (M,).
     K: number of independent copies in the pool (reading c6).
     pool: optional pre-built CopyPool of the same (phi, b_phi, seed) -- lets a caller
     time the iterations without the one-time quantisation of the copies.
+    snapshot: index b of this observation among B sharing Phi (config 5); selects the
+    Philox column of its y-hat (oracle.quantize.quantize_vector).
     """
     c_phi = Q.scale_c(phi)
     c_y = Q.scale_c(y)
-    y_codes, _ = Q.quantize_vector(y, b_y, level_mode, seed, c=c_y)
+    y_codes, _ = Q.quantize_vector(y, b_y, level_mode, seed, c=c_y, snapshot=snapshot)
     y_hat = Q.dequantize(y_codes, c_y, b_y, level_mode)          # quantised once (P:345)
     if pool is None:
         pool = CopyPool(phi, b_phi, level_mode, seed, c_phi, cache=max(2, min(K, 4)))
@@ -153,6 +155,18 @@ def qniht(phi, y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True,
                                         margin_at_s(a, s)))
     res.x_idx, res.x_val = x_idx, x_val
     return res
+
+
+def qniht_batched(phi, Y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True):
+    """B independent observations sharing one Phi (BASELINE config 5): Algorithm 1 run
+    on each column y_b of Y (M x B) with the SAME pool of quantised copies (P:345, P:349
+    applied per snapshot); each snapshot has its own c_y and y-hat (snapshot b).  Returns
+    a list of QnihtResult."""
+    Y = np.asarray(Y)
+    c_phi = Q.scale_c(phi)
+    pool = CopyPool(phi, b_phi, level_mode, seed, c_phi, cache=max(2, min(K, 4)))
+    return [qniht(phi, Y[:, b], s, n_iter, mu, b_phi, b_y, seed, K, level_mode=level_mode, record=record,
+                  pool=pool, snapshot=b) for b in range(Y.shape[1])]
 
 
 def niht_fixed_full_precision(phi, y, s, n_iter, mu):

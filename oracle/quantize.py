@@ -134,15 +134,17 @@ def quantize_matrix(phi, bits, level_mode, seed, copy_id, c=None, row_offset=0, 
     return np.stack(out), np.float32(c)
 
 
-def quantize_vector(y, bits, level_mode, seed, c=None):
+def quantize_vector(y, bits, level_mode, seed, c=None, snapshot=0):
     """Quantize the observation vector once (Alg. 1 input y-hat):
-    n = 0, m = element index, copy 0, tag 1.  Returns (codes (planes, M), c)."""
+    n = snapshot, m = element index, copy 0, tag 1.  A batch of B observations sharing
+    Phi (BASELINE config 5) is the matrix Y = [y_0 .. y_{B-1}], observation b being its
+    column n = b; a single observation is snapshot 0.  Returns (codes (planes, M), c)."""
     y = np.asarray(y)
     if c is None:
         c = scale_c(y)
     M = y.shape[0]
     m = np.arange(M, dtype=np.uint64)
-    n = np.zeros(M, dtype=np.uint64)
+    n = np.full(M, snapshot, dtype=np.uint64)
     if np.iscomplexobj(y):
         planes = [y.real.astype(np.float32), y.imag.astype(np.float32)]
     else:

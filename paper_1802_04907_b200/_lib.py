@@ -28,7 +28,7 @@ class IhtQmat(ctypes.Structure):
     _fields_ = [
         ("rows", c_i64), ("cols", c_i64), ("row_offset", c_i64),
         ("planes", c_i32), ("bits", c_i32), ("level_mode", c_i32), ("copy_id", c_i32),
-        ("seed", c_u64), ("scale_c", c_f32), ("reserved", c_i32),
+        ("seed", c_u64), ("scale_c", c_f32), ("col_offset", c_i32),
         ("strip_bytes", c_i64), ("codes", c_vp),
     ]
 
@@ -38,7 +38,7 @@ class IhtConfig(ctypes.Structure):
     _fields_ = [
         ("s", c_i32), ("n_iter", c_i32), ("mu", c_f32), ("b_y", c_i32), ("level_mode", c_i32),
         ("adjoint_variant", c_i32), ("seed", c_u64), ("trace", c_i32), ("use_graph", c_i32),
-        ("comm", c_vp), ("profile", c_i32), ("reserved", c_i32),
+        ("comm", c_vp), ("profile", c_i32), ("nrhs", c_i32),
     ]
 
 
@@ -52,21 +52,31 @@ SIGNATURES = {
     "iht_qmat_bytes": (c_i64, [c_i64, c_i64, c_int, c_int]),
     "iht_vec_len": (c_i64, [c_i64, c_int]),
     "iht_absmax": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "iht_absmax_batched": (c_int, [c_vp, c_i64, c_i32, c_vp, c_vp]),
     "iht_quantize": (c_int, [c_vp, c_i64, ctypes.POINTER(IhtQmat), c_int, c_vp]),
     "iht_quantize_rows": (c_int, [c_vp, c_i64, ctypes.POINTER(IhtQmat), c_int, c_i64, c_i64, c_vp]),
     "iht_quantize_vec": (c_int, [c_vp, c_i64, c_i64, c_int, c_int, c_int, c_u64, c_vp, c_vp, c_vp, c_vp]),
+    "iht_quantize_vec_batched": (c_int, [c_vp, c_i64, c_i64, c_int, c_int, c_int, c_u64, c_vp, c_i32, c_vp, c_vp,
+                                         c_vp]),
     "iht_forward_ws_bytes": (c_i64, [ctypes.POINTER(IhtQmat), c_i32]),
     "iht_forward": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "iht_forward_batched": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp,
+                                    c_vp]),
     "iht_adjoint_ws_bytes": (c_i64, [ctypes.POINTER(IhtQmat)]),
     "iht_adjoint": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_vp, c_int, c_vp, c_i64, c_vp]),
     "iht_adjoint_batched_ws_bytes": (c_i64, [ctypes.POINTER(IhtQmat), c_i32]),
     "iht_adjoint_batched": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
     "iht_threshold_ws_bytes": (c_i64, [c_i64, c_i32]),
     "iht_threshold": (c_int, [c_vp, c_vp, c_vp, c_vp, c_f32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "iht_threshold_batched_ws_bytes": (c_i64, [c_i64, c_i32, c_i32]),
+    "iht_threshold_batched": (c_int, [c_vp, c_vp, c_vp, c_i32, c_vp, c_f32, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp,
+                                      c_i32, c_vp, c_vp, c_i64, c_vp]),
+    "iht_merge_candidates": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "iht_comm_unique_id": (c_int, [c_vp]),
     "iht_comm_create": (c_int, [c_int, c_int, c_vp, c_int, ctypes.POINTER(c_vp)]),
     "iht_comm_destroy": (c_int, [c_vp]),
     "iht_comm_allreduce": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
+    "iht_comm_allgather": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "iht_solver_create": (c_int, [ctypes.POINTER(IhtQmat), c_int, ctypes.POINTER(IhtConfig), ctypes.POINTER(c_vp)]),
     "iht_solver_destroy": (c_int, [c_vp]),
     "iht_solver_run": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),

@@ -16,18 +16,22 @@
 //
 // K order inside a 16-byte u8 chunk is permuted (row(p) below) identically on A and B.
 //
-// Roles per CTA (320 threads): warps 0-3 convert packed codes -> u8 stage; warp 4 issues
-// the MMAs (one thread); warp 5 issues the bulk copies (packed codes, B image);
-// warps 6-9 run the epilogue (TMEM -> registers -> g).  TMEM is double-buffered so the
-// epilogue of tile t overlaps the MMAs of tile t+1.
+// Roles per CTA (352 threads): warps 0-3 expand packed codes -> u8 A stages in TMEM
+// (tcgen05.st); warp 4 issues the MMAs (one thread); warp 5 bulk-copies the packed codes
+// (8 slots), warp 6 the r-limb image (4 stages), each on its own ring so neither waits for
+// the other; warps 7-10 run the epilogue (TMEM -> registers -> g).  The accumulators are
+// double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
+#include <stdlib.h>
+
 #include "iht_internal.cuh"
 
 namespace iht {
 
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
-constexpr int kBStages = 3;            // A/B operand stages
-constexpr int kPkSlots = 4;            // packed-code staging slots
-constexpr int kBThreads = 320;
+constexpr int kAStages = 3;            // A (expanded codes) stages in TMEM
+constexpr int kBStages = 4;            // B (r limbs) stages in shared memory
+constexpr int kPkSlots = 8;            // packed-code staging slots
+constexpr int kBThreads = 352;         // 11 warps (roles above)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -92,7 +96,9 @@ struct BatchArgs {
   int Rpad;
   int nkb;                 // K-blocks (tile-steps) = Rpad / (512/b)
   int ntiles;              // ceil(N / 128)
-  int B;                   // snapshots (2B <= 256)
+  int B;                   // MMA snapshots (padded to a multiple of 8; 2B <= 128)
+  int Breal;               // snapshots actually written (<= B)
+  int probe;               // 0; profiling probes (IHT_BATCHED_PROBE): 1 no B copies, 2 no MMAs, 4 no TMEM stores
   int L;
   float sigma;
   const uint8_t* bimg;     // [nkb][KBB*2B] pre-swizzled limb image
@@ -117,12 +123,13 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   uint8_t* sB = smem;                                   // [kBStages][BSZ]  (BSZ multiple of 1024)
   uint8_t* sP = sB + kBStages * BSZ;                    // [kPkSlots][PK]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kPkSlots * PK);
-  uint64_t* pk_full = bar;                  // [kPkSlots]  tx
-  uint64_t* pk_free = bar + kPkSlots;       // [kPkSlots]  4 converter warps
-  uint64_t* a_full = bar + 2 * kPkSlots;    // [kBStages]  4 converter warps
-  uint64_t* b_full = a_full + kBStages;     // [kBStages]  tx
-  uint64_t* st_free = b_full + kBStages;    // [kBStages]  tcgen05.commit
-  uint64_t* acc_full = st_free + kBStages;  // [2]         tcgen05.commit
+  uint64_t* pk_full = bar;                        // [kPkSlots]  tx
+  uint64_t* pk_free = pk_full + kPkSlots;         // [kPkSlots]  4 converter warps
+  uint64_t* a_full = pk_free + kPkSlots;          // [kAStages]  4 converter warps
+  uint64_t* a_free = a_full + kAStages;           // [kAStages]  tcgen05.commit
+  uint64_t* b_full = a_free + kAStages;           // [kBStages]  tx
+  uint64_t* b_free = b_full + kBStages;           // [kBStages]  tcgen05.commit
+  uint64_t* acc_full = b_free + kBStages;         // [2]         tcgen05.commit
   uint64_t* acc_free = acc_full + 2;        // [2]         4 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   float* ep_scale = reinterpret_cast<float*>(tmem_slot + 4);            // [B] sigma 2^-F_b
@@ -134,10 +141,13 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       mbar_init2(smem_u32(&pk_full[i]), 1);
       mbar_init2(smem_u32(&pk_free[i]), 4);
     }
-    for (int i = 0; i < kBStages; ++i) {
+    for (int i = 0; i < kAStages; ++i) {
       mbar_init2(smem_u32(&a_full[i]), 4);
+      mbar_init2(smem_u32(&a_free[i]), 1);
+    }
+    for (int i = 0; i < kBStages; ++i) {
       mbar_init2(smem_u32(&b_full[i]), 1);
-      mbar_init2(smem_u32(&st_free[i]), 1);
+      mbar_init2(smem_u32(&b_free[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init2(smem_u32(&acc_full[i]), 1);
@@ -145,7 +155,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {   // TMEM: 2 accumulator buffers (NB <= 128 columns each) + kBStages A stages
+  if (warp == 4) {   // TMEM: 2 accumulator buffers (NB <= 128 columns each) + kAStages A stages
     const uint32_t cols = 512;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(cols)
@@ -168,12 +178,12 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     // ---------------------------------------------------------------- converters
     const int n = warp * 32 + lane;              // pixel row inside the tile (0..127)
     const int ct = n >> 4, cc = n & 15;           // column tile / column inside the tile
-    int64_t i = 0;                                // global K-block counter of this CTA
+    int ps = 0, ss = 0;
+    uint32_t pph = 0, sph = 0;                    // phase bits of pk_full / a_free
+    bool a_wrapped = false;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-      for (int kb = 0; kb < a.nkb; ++kb, ++i) {
-        const int ps = (int)(i % kPkSlots), ss = (int)(i % kBStages);
-        mbar_wait2(smem_u32(&pk_full[ps]), (uint32_t)((i / kPkSlots) & 1));
-        if (i >= kBStages) mbar_wait2(smem_u32(&st_free[ss]), (uint32_t)(((i - kBStages) / kBStages) & 1));
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        mbar_wait2(smem_u32(&pk_full[ps]), pph);
         uint32_t out[ACOLS];              // this pixel row's KBB u8 bytes, 4 per TMEM column
 #pragma unroll
         for (int ts = 0; ts < TS; ++ts) {
@@ -206,10 +216,14 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));   // packed slot consumed (registers hold it)
+        if (a_wrapped) mbar_wait2(smem_u32(&a_free[ss]), sph ^ 1u);
         // A stage ss lives in TMEM columns a_col0 + ss * ACOLS .. ; lane = pixel row n
         const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
         for (int c0 = 0; c0 < ACOLS; c0 += 16)
+          if (!(a.probe & 4))
           asm volatile(
               "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
                   ta + (uint32_t)c0),
@@ -220,30 +234,32 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive2(smem_u32(&pk_free[ps]));
-          mbar_arrive2(smem_u32(&a_full[ss]));
-        }
+        if (lane == 0) mbar_arrive2(smem_u32(&a_full[ss]));
+        if (++ps == kPkSlots) { ps = 0; pph ^= 1u; }
+        if (++ss == kAStages) { ss = 0; sph ^= 1u; a_wrapped = true; }
       }
     }
   } else if (warp == 4) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = idesc_i8(kBT, NB);
-    int64_t i = 0;
+    int as = 0, bs = 0;
+    uint32_t aph = 0, bph = 0;
     int t = 0;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
       const int ab = t & 1;
       if (t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dtm = tmem + ab * acc_stride;
-      for (int kb = 0; kb < a.nkb; ++kb, ++i) {
-        const int ss = (int)(i % kBStages);
-        const uint32_t ph = (uint32_t)((i / kBStages) & 1);
-        mbar_wait2(smem_u32(&a_full[ss]), ph);
-        mbar_wait2(smem_u32(&b_full[ss]), ph);
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        mbar_wait2(smem_u32(&a_full[as]), aph);
+        mbar_wait2(smem_u32(&b_full[bs]), bph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0) {
-          const uint32_t atm = tmem + a_col0 + (uint32_t)(ss * ACOLS), bbase = smem_u32(sB + ss * BSZ);
+        if (lane == 0 && (a.probe & 2)) {          // probe: no tensor work, release the stages at once
+          mbar_arrive2(smem_u32(&a_free[as]));
+          mbar_arrive2(smem_u32(&b_free[bs]));
+          if (kb == a.nkb - 1) mbar_arrive2(smem_u32(&acc_full[ab]));
+        } else if (lane == 0) {
+          const uint32_t atm = tmem + a_col0 + (uint32_t)(as * ACOLS), bbase = smem_u32(sB + bs * BSZ);
 #pragma unroll
           for (int kk = 0; kk < NKS; ++kk) {
             const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (NB * 128) + (kk & 3) * 32);
@@ -255,7 +271,10 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                 : "memory");
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(&st_free[ss]))
+                           smem_u32(&a_free[as]))
+                       : "memory");
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&b_free[bs]))
                        : "memory");
           if (kb == a.nkb - 1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -263,33 +282,53 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                          : "memory");
         }
         __syncwarp();
+        if (++as == kAStages) { as = 0; aph ^= 1u; }
+        if (++bs == kBStages) { bs = 0; bph ^= 1u; }
       }
     }
   } else if (warp == 5) {
-    // ---------------------------------------------------------------- producer
+    // ---------------------------------------------------------------- packed-code producer
     if (lane == 0) {
-      int64_t i = 0;
+      int ps = 0;
+      uint32_t ph = 0;
+      bool wrapped = false;
+      const int64_t last_tile = (a.N + 15) / 16 - 1;
       for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-        for (int kb = 0; kb < a.nkb; ++kb, ++i) {
-          const int ps = (int)(i % kPkSlots), ss = (int)(i % kBStages);
-          if (i >= kPkSlots) mbar_wait2(smem_u32(&pk_free[ps]), (uint32_t)(((i - kPkSlots) / kPkSlots) & 1));
+        for (int kb = 0; kb < a.nkb; ++kb) {
+          if (wrapped) mbar_wait2(smem_u32(&pk_free[ps]), ph ^ 1u);
           mbar_expect_tx2(smem_u32(&pk_full[ps]), PK);
           for (int ct = 0; ct < 8; ++ct) {
             int64_t col_tile = (int64_t)tile * 8 + ct;                // 16-column tile index
-            const int64_t last_tile = (a.N + 15) / 16 - 1;
             if (col_tile > last_tile) col_tile = last_tile;            // past N: any valid data
             bulk_g2s2(smem_u32(sP + ps * PK + ct * (TS * 1024)),
                       a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb * TS * 1024, TS * 1024,
                       smem_u32(&pk_full[ps]));
           }
-          if (i >= kBStages) mbar_wait2(smem_u32(&st_free[ss]), (uint32_t)(((i - kBStages) / kBStages) & 1));
-          mbar_expect_tx2(smem_u32(&b_full[ss]), (uint32_t)BSZ);
-          bulk_g2s2(smem_u32(sB + ss * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&b_full[ss]));
+          if (++ps == kPkSlots) { ps = 0; ph ^= 1u; wrapped = true; }
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------------------------------------------------------- r-limb (B) producer
+    if (lane == 0) {
+      int bs = 0;
+      uint32_t ph = 0;
+      bool wrapped = false;
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        for (int kb = 0; kb < a.nkb; ++kb) {
+          if (wrapped) mbar_wait2(smem_u32(&b_free[bs]), ph ^ 1u);
+          if ((a.probe & 1) && wrapped) {
+            mbar_arrive2(smem_u32(&b_full[bs]));                 // probe: reuse the stale stage
+          } else {
+            mbar_expect_tx2(smem_u32(&b_full[bs]), (uint32_t)BSZ);
+            bulk_g2s2(smem_u32(sB + bs * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&b_full[bs]));
+          }
+          if (++bs == kBStages) { bs = 0; ph ^= 1u; wrapped = true; }
         }
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 6-9)
+    // ---------------------------------------------------------------- epilogue (warps 7-10)
     const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
     int t = 0;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
@@ -311,7 +350,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           for (int e = 0; e < 16; e += 2) {
             const int b = (c0 + e) >> 1;
             const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
-            a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
+            if (b < a.Breal) a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
           }
         }
       }
@@ -331,16 +370,17 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
 // Per-snapshot block fixed point of R (one CTA per snapshot): F_b from max |r|, two
 // balanced signed limbs written into the pre-swizzled image, exact limb sums S_b.
 template <int BITS>
-__global__ void batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nkb,
+__global__ void batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nreal, int nkb,
                                      uint8_t* __restrict__ bimg, int* __restrict__ Fb, int* __restrict__ Sb) {
   constexpr int KBR = (BITS == 8 ? 2 : 1) * 512 / BITS;
-  const int b = blockIdx.x;
-  const float* r = R + (int64_t)b * Rpad;
+  const int b = blockIdx.x;                 // b >= nreal: zero padding snapshot (MMA N granularity)
+  const float* r = R + (int64_t)(b < nreal ? b : 0) * Rpad;
   __shared__ float red[32];
   __shared__ int ired[2][32];
   __shared__ int Fs;
   float m = 0.0f;
-  for (int i = threadIdx.x; i < Rpad; i += blockDim.x) m = fmaxf(m, fabsf(r[i]));
+  if (b < nreal)
+    for (int i = threadIdx.x; i < Rpad; i += blockDim.x) m = fmaxf(m, fabsf(r[i]));
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -357,7 +397,7 @@ __global__ void batched_limbs_kernel(const float* __restrict__ R, int Rpad, int 
   const int NB = 2 * B;
   int s0 = 0, s1 = 0;
   for (int row = threadIdx.x; row < nkb * KBR; row += blockDim.x) {
-    const float rv = row < Rpad ? r[row] : 0.0f;
+    const float rv = (row < Rpad && b < nreal) ? r[row] : 0.0f;
     const int ri = __float2int_rn(rv * scale);
     const int l0 = ((ri + 128) & 255) - 128;
     const int l1 = (ri - l0) >> 8;
@@ -398,19 +438,36 @@ static int kb_rows(int bits) { return (bits == 8 ? 2 : 1) * 512 / bits; }
 static size_t batched_smem(int bits, int B) {
   const int KBB = kb_rows(bits), TS = bits == 8 ? 2 : 1;
   return 1024 + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * TS * 1024 +
-         (size_t)(2 * kPkSlots + 3 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
+         (size_t)(2 * kPkSlots + 2 * kAStages + 2 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
 }
 
 }  // namespace iht
 
 using namespace iht;
 
+static constexpr int kMaxChunk = 64;     // snapshots per GEMM launch (MMA N = 2 * 64 = 128)
+
+static int chunk_pad(int32_t nrhs) {      // padded snapshots of the widest chunk
+  const int c = nrhs < kMaxChunk ? nrhs : kMaxChunk;
+  return (c + 7) / 8 * 8;
+}
+
 extern "C" int64_t iht_adjoint_batched_ws_bytes(const iht_qmat* A, int32_t nrhs) {
   if (A == nullptr || nrhs <= 0) return -1;
   const int64_t Rpad = A->planes * rows_pad(A->rows);
   const int KBR = kb_rows(A->bits);
   const int64_t nkb = (Rpad + KBR - 1) / KBR;
-  return nkb * 2 * nrhs * KBR + 256 + 3 * nrhs * 4 + 256;
+  const int bp = chunk_pad(nrhs);
+  return nkb * 2 * bp * KBR + 256 + 3 * bp * 4 + 256;
+}
+
+static int probe_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IHT_BATCHED_PROBE");   // profiling only: see BatchArgs::probe
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nrhs, float* G, void* ws,
@@ -418,7 +475,6 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
   if (A == nullptr || R == nullptr || G == nullptr || nrhs <= 0) return IHT_EINVAL;
   if (A->codes == nullptr || (A->bits != 2 && A->bits != 4 && A->bits != 8)) return IHT_EINVAL;
   if (A->strip_bytes != iht_strip_bytes(A->rows, A->planes, A->bits)) return IHT_EINVAL;
-  if ((2 * nrhs) % 16 != 0 || 2 * nrhs > 128) return IHT_EUNSUPPORTED;   // MMA N = 2 nrhs <= 128
   const int64_t Rpad = A->planes * rows_pad(A->rows);
   const int L = num_levels(A->bits, A->level_mode);
   if ((double)Rpad * (L - 1) * 128.0 >= 2147483647.0) return IHT_EUNSUPPORTED;   // int32 accumulator
@@ -428,32 +484,40 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
   const int nkb = (int)(Rpad / KBR);        // Rpad is a multiple of 256 rows per plane
   if (nkb * KBR != Rpad) return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  const int bp_max = chunk_pad(nrhs);
   uint8_t* bimg = static_cast<uint8_t*>(ws);
-  const int64_t bimg_bytes = (int64_t)nkb * 2 * nrhs * KBR;
+  const int64_t bimg_bytes = (int64_t)nkb * 2 * bp_max * KBR;
   int* Fb = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + (bimg_bytes + 255) / 256 * 256);
-  int* Sb = Fb + nrhs;
-  BatchArgs b{};
-  b.codes = static_cast<const uint8_t*>(A->codes);
-  b.strip_bytes = A->strip_bytes;
-  b.N = A->cols;
-  b.Rpad = (int)Rpad;
-  b.nkb = nkb;
-  b.ntiles = (int)((A->cols + kBT - 1) / kBT);
-  b.B = nrhs;
-  b.L = L;
-  b.sigma = A->scale_c / (float)(L - 1);
-  b.bimg = bimg;
-  b.Fb = Fb;
-  b.Sb = Sb;
-  b.g = G;
+  int* Sb = Fb + bp_max;
   int dev = 0, sms = kNumSMs;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = batched_smem(A->bits, nrhs);
-  if (smem > 227 * 1024) return IHT_EUNSUPPORTED;
+  if (batched_smem(A->bits, bp_max) > 227 * 1024) return IHT_EUNSUPPORTED;
+  // chunks of <= 64 snapshots; each padded to a multiple of 8 (MMA N = 2 B, multiple of 16)
+  for (int c0 = 0; c0 < nrhs; c0 += kMaxChunk) {
+    const int nb = nrhs - c0 < kMaxChunk ? nrhs - c0 : kMaxChunk;
+    const int bp = (nb + 7) / 8 * 8;
+    BatchArgs b{};
+    b.codes = static_cast<const uint8_t*>(A->codes);
+    b.strip_bytes = A->strip_bytes;
+    b.N = A->cols;
+    b.Rpad = (int)Rpad;
+    b.nkb = nkb;
+    b.ntiles = (int)((A->cols + kBT - 1) / kBT);
+    b.B = bp;
+    b.Breal = nb;
+    b.probe = probe_flags();
+    b.L = L;
+    b.sigma = A->scale_c / (float)(L - 1);
+    b.bimg = bimg;
+    b.Fb = Fb;
+    b.Sb = Sb;
+    b.g = G + (int64_t)c0 * A->cols;
+    const float* Rc = R + (int64_t)c0 * Rpad;
+    const size_t smem = batched_smem(A->bits, bp);
 #define IHT_BATCH(BB)                                                                                  \
   do {                                                                                                 \
-    batched_limbs_kernel<BB><<<nrhs, 256, 0, st>>>(R, (int)Rpad, nrhs, nkb, bimg, Fb, Sb);            \
+    batched_limbs_kernel<BB><<<bp, 256, 0, st>>>(Rc, (int)Rpad, bp, nb, nkb, bimg, Fb, Sb);           \
     IHT_LAUNCH_CHECK();                                                                                \
     static bool attr = false;                                                                          \
     if (!attr) {                                                                                       \
@@ -464,9 +528,10 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     adjoint_batched_kernel<BB><<<min(b.ntiles, sms), kBThreads, smem, st>>>(b);                        \
     IHT_LAUNCH_CHECK();                                                                                \
   } while (0)
-  if (A->bits == 2) IHT_BATCH(2);
-  else if (A->bits == 4) IHT_BATCH(4);
-  else IHT_BATCH(8);
+    if (A->bits == 2) IHT_BATCH(2);
+    else if (A->bits == 4) IHT_BATCH(4);
+    else IHT_BATCH(8);
 #undef IHT_BATCH
+  }
   return IHT_OK;
 }

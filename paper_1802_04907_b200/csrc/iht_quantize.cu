@@ -15,6 +15,8 @@ namespace iht {
 // ------------------------------------------------------------------ absmax
 __global__ void absmax_kernel(const float* __restrict__ src, int64_t count,
                               unsigned int* __restrict__ out) {
+  src += (int64_t)blockIdx.y * count;     // batched: one vector per grid row
+  out += blockIdx.y;
   unsigned int m = 0;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -46,6 +48,7 @@ struct QuantArgs {
   int64_t ld;           // row stride in (complex) elements
   int64_t rows, cols, row_offset, strip_bytes, rows_pad;
   int64_t row_begin, row_end;   // local rows quantised by this call (src rows row_begin..row_end)
+  int64_t col_quad0;            // col_offset / 4: global column quad of local column 0
   int64_t qblocks;              // column-quad blocks per sector row of the grid
   float c;
   int level_mode;
@@ -95,7 +98,8 @@ __global__ void __launch_bounds__(128) quantize_kernel(QuantArgs a) {
             for (int p = 0; p < P; ++p) v[p][j] = (j < ncol) ? __ldg(row + j * P + p) : 0.0f;
 #pragma unroll
           for (int p = 0; p < P; ++p) {
-            const u32x4 r = philox4x32_10(u32x4{(uint32_t)g, mg, cid, (uint32_t)(p << 8)}, k0, k1);
+            const u32x4 r =
+                philox4x32_10(u32x4{(uint32_t)(a.col_quad0 + g), mg, cid, (uint32_t)(p << 8)}, k0, k1);
             cur[p][0] |= q_contract(v[p][0], a.c, sf, L, r.x) << (cc * B);
             cur[p][1] |= q_contract(v[p][1], a.c, sf, L, r.y) << (cc * B);
             cur[p][2] |= q_contract(v[p][2], a.c, sf, L, r.z) << (cc * B);
@@ -122,8 +126,12 @@ __global__ void quantize_vec_kernel(const float* __restrict__ y, int64_t rows, i
                                     uint8_t* __restrict__ codes, int64_t rpad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rpad) return;
+  const uint32_t b = blockIdx.y;          // snapshot = column n of Y (word n & 3 of counter n >> 2)
+  y += (int64_t)b * rows * P;
+  yhat += (int64_t)b * P * rpad;
+  if (codes) codes += (int64_t)b * P * rows;
   const int L = num_levels(bits, level_mode);
-  const float c = *c_dev;
+  const float c = c_dev[b];
   const float sf = q_scale_factor(c, L);
   const float sigma = __fdiv_rn(c, (float)(L - 1));
 #pragma unroll
@@ -131,9 +139,10 @@ __global__ void quantize_vec_kernel(const float* __restrict__ y, int64_t rows, i
     float out = 0.0f;
     if (i < rows) {
       const float v = y[i * P + p];
-      const u32x4 w = philox4x32_10(u32x4{0u, (uint32_t)(row_offset + i), 0u, (uint32_t)((p << 8) | 1)},
+      const u32x4 w = philox4x32_10(u32x4{b >> 2, (uint32_t)(row_offset + i), 0u, (uint32_t)((p << 8) | 1)},
                                     k0, k1);
-      const uint32_t code = q_contract(v, c, sf, L, w.x);
+      const uint32_t word = (b & 3) == 0 ? w.x : (b & 3) == 1 ? w.y : (b & 3) == 2 ? w.z : w.w;
+      const uint32_t code = q_contract(v, c, sf, L, word);
       if (codes) codes[p * rows + i] = (uint8_t)code;
       out = __fmul_rn(sigma, (float)(2 * (int)code - (L - 1)));
     }
@@ -145,17 +154,23 @@ __global__ void quantize_vec_kernel(const float* __restrict__ y, int64_t rows, i
 
 using namespace iht;
 
-extern "C" int iht_absmax(const float* src, int64_t count, float* c_dev, void* stream) {
-  if (count < 0 || c_dev == nullptr || (count > 0 && src == nullptr)) return IHT_EINVAL;
+extern "C" int iht_absmax_batched(const float* src, int64_t count, int32_t nrhs, float* c_dev, void* stream) {
+  if (count < 0 || nrhs <= 0 || nrhs > 65535 || c_dev == nullptr || (count > 0 && src == nullptr))
+    return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  IHT_CUDA_CHECK(cudaMemsetAsync(c_dev, 0, sizeof(float), st));
+  IHT_CUDA_CHECK(cudaMemsetAsync(c_dev, 0, sizeof(float) * nrhs, st));
   if (count == 0) return IHT_OK;
   const int threads = 256;
   const int64_t want = ceil_div<int64_t>(count, (int64_t)threads * 16);
-  const int blocks = (int)min64(max64(want, 1), (int64_t)kNumSMs * 8);
-  absmax_kernel<<<blocks, threads, 0, st>>>(src, count, reinterpret_cast<unsigned int*>(c_dev));
+  const int blocks = (int)min64(max64(want, 1), max64(1, (int64_t)kNumSMs * 8 / nrhs));
+  // (the kernel takes the vectorised path only when its vector is 16-byte aligned)
+  absmax_kernel<<<dim3(blocks, nrhs), threads, 0, st>>>(src, count, reinterpret_cast<unsigned int*>(c_dev));
   IHT_LAUNCH_CHECK();
   return IHT_OK;
+}
+
+extern "C" int iht_absmax(const float* src, int64_t count, float* c_dev, void* stream) {
+  return iht_absmax_batched(src, count, 1, c_dev, stream);
 }
 
 static bool qmat_valid(const iht_qmat& q) {
@@ -166,6 +181,7 @@ static bool qmat_valid(const iht_qmat& q) {
   if (q.strip_bytes != iht_strip_bytes(q.rows, q.planes, q.bits)) return false;
   if (q.codes == nullptr || (reinterpret_cast<uintptr_t>(q.codes) & 15)) return false;
   if (q.row_offset + q.rows > 0xFFFFFFFFll) return false;
+  if (q.col_offset < 0 || (q.col_offset & 15)) return false;
   return true;
 }
 
@@ -182,10 +198,10 @@ extern "C" int iht_quantize_rows(const float* src, int64_t ld, const iht_qmat* d
     const iht_qmat& d = dst[k];
     if (!qmat_valid(d) || d.rows != d0.rows || d.cols != d0.cols || d.planes != d0.planes ||
         d.bits != d0.bits || d.level_mode != d0.level_mode || d.scale_c != d0.scale_c ||
-        d.row_offset != d0.row_offset)
+        d.row_offset != d0.row_offset || d.col_offset != d0.col_offset)
       return IHT_EINVAL;
   }
-  if (d0.cols / 4 >= (int64_t)0xFFFFFFFF) return IHT_EINVAL;
+  if ((d0.col_offset + d0.cols) / 4 >= (int64_t)0xFFFFFFFF) return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const int RPS = 256 / d0.bits;
   const int64_t rp = rows_pad(d0.rows);
@@ -205,6 +221,7 @@ extern "C" int iht_quantize_rows(const float* src, int64_t ld, const iht_qmat* d
     a.rows_pad = rp;
     a.row_begin = row_begin;
     a.row_end = row_begin + nrows;
+    a.col_quad0 = d0.col_offset / 4;
     a.qblocks = qblocks;
     a.c = d0.scale_c;
     a.level_mode = d0.level_mode;
@@ -237,7 +254,15 @@ extern "C" int iht_quantize(const float* src, int64_t ld, const iht_qmat* dst, i
 extern "C" int iht_quantize_vec(const float* y, int64_t rows, int64_t row_offset, int planes, int bits,
                                 int level_mode, uint64_t seed, const float* c_dev, float* yhat,
                                 uint8_t* codes, void* stream) {
+  return iht_quantize_vec_batched(y, rows, row_offset, planes, bits, level_mode, seed, c_dev, 1, yhat, codes,
+                                  stream);
+}
+
+extern "C" int iht_quantize_vec_batched(const float* y, int64_t rows, int64_t row_offset, int planes, int bits,
+                                        int level_mode, uint64_t seed, const float* c_dev, int32_t nrhs,
+                                        float* yhat, uint8_t* codes, void* stream) {
   if (y == nullptr || c_dev == nullptr || yhat == nullptr || rows <= 0 || row_offset < 0) return IHT_EINVAL;
+  if (nrhs <= 0 || nrhs > 65535) return IHT_EINVAL;
   if ((planes != 1 && planes != 2) || bits < 2 || bits > 8 || (level_mode != 0 && level_mode != 1))
     return IHT_EINVAL;
   if (row_offset + rows > 0xFFFFFFFFll) return IHT_EINVAL;
@@ -247,10 +272,10 @@ extern "C" int iht_quantize_vec(const float* y, int64_t rows, int64_t row_offset
   const unsigned blocks = (unsigned)ceil_div<int64_t>(rp, threads);
   const uint32_t k0 = (uint32_t)(seed & 0xFFFFFFFFull), k1 = (uint32_t)(seed >> 32);
   if (planes == 1)
-    quantize_vec_kernel<1><<<blocks, threads, 0, st>>>(y, rows, row_offset, bits, level_mode, k0, k1, c_dev,
+    quantize_vec_kernel<1><<<dim3(blocks, nrhs), threads, 0, st>>>(y, rows, row_offset, bits, level_mode, k0, k1, c_dev,
                                                        yhat, codes, rp);
   else
-    quantize_vec_kernel<2><<<blocks, threads, 0, st>>>(y, rows, row_offset, bits, level_mode, k0, k1, c_dev,
+    quantize_vec_kernel<2><<<dim3(blocks, nrhs), threads, 0, st>>>(y, rows, row_offset, bits, level_mode, k0, k1, c_dev,
                                                        yhat, codes, rp);
   IHT_LAUNCH_CHECK();
   return IHT_OK;

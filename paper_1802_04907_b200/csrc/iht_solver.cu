@@ -63,6 +63,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
@@ -78,7 +79,9 @@ bool load_nccl() {
   g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
-  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce;
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce &&
+              g_nccl.AllGather;
   return g_nccl.ok;
 }
 }  // namespace
@@ -124,20 +127,41 @@ extern "C" int iht_comm_allreduce(iht_comm* comm, float* buf, int64_t count, int
   return IHT_OK;
 }
 
+extern "C" int iht_comm_allgather(iht_comm* comm, const void* send, void* recv, int64_t bytes, void* stream) {
+  if (comm == nullptr || send == nullptr || recv == nullptr || bytes < 0) return IHT_EINVAL;
+  if (g_nccl.AllGather(send, recv, (size_t)bytes, ncclUint8, comm->comm, (cudaStream_t)stream) != ncclSuccess)
+    return IHT_ENCCL;
+  return IHT_OK;
+}
+
 // ------------------------------------------------------------------ solver
+// Modes (fixed at create):
+//   single  (nrhs <= 1): GEMV adjoint; with a communicator of world P > 1 the rows are
+//           sharded and g is all-reduced (north star).
+//   batched (nrhs = B > 1, BASELINE config 5): per-snapshot sparse forward, tcgen05
+//           adjoint (chunks of <= 64 snapshots inside iht_adjoint_batched), per-snapshot
+//           H_s; with a communicator the COLUMNS are sharded: forward partials
+//           all-reduced, local top-s candidates all-gathered and merged.
+
 struct iht_solver {
   std::vector<iht_qmat> pool;
   iht_config cfg;
   int64_t rows, N, vlen;
   int planes;
+  int B = 1;                           // snapshots
+  bool batched = false, rowshard = false, colshard = false;
+  int world = 1, rank = 0;
   // device buffers (one allocation)
   void* block = nullptr;
   float *y = nullptr, *c_y = nullptr, *yhat = nullptr, *r = nullptr, *g = nullptr;
   void *ws_adj = nullptr, *ws_thr = nullptr;
   int64_t ws_adj_bytes = 0, ws_thr_bytes = 0;
-  int32_t* xs_idx = nullptr;   // [nslots][s]
-  float* xs_val = nullptr;     // [nslots][s]
-  int32_t* xs_nnz = nullptr;   // [nslots]
+  int32_t* xs_idx = nullptr;   // [nslots][B][s]
+  float* xs_val = nullptr;     // [nslots][B][s]
+  int32_t* xs_nnz = nullptr;   // [nslots][B]
+  int32_t* cand_send = nullptr;   // column shards: idx [B][s] | val [B][s] | nnz [B]
+  int32_t* cand_recv = nullptr;   // [P][same]
+  int64_t cand_words = 0;
   int nslots = 0;
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -161,43 +185,75 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
   int64_t L = 0;
   int rc;
   const int64_t ycount = S->rows * S->planes;
-  if ((rc = iht_absmax(S->y, ycount, S->c_y, st)) != IHT_OK) return rc;
+  const int B = S->B, s = S->cfg.s;
+  if ((rc = iht_absmax_batched(S->y, ycount, B, S->c_y, st)) != IHT_OK) return rc;
   L += 1;
-  if (S->cfg.comm && S->cfg.comm->world > 1) {   // global max over the row shards (reading c3)
+  if (S->rowshard) {   // global max over the row shards (reading c3)
     if ((rc = iht_comm_allreduce(S->cfg.comm, S->c_y, 1, 1, st)) != IHT_OK) return rc;
   }
   const iht_qmat& q0 = S->pool[0];
-  if ((rc = iht_quantize_vec(S->y, S->rows, q0.row_offset, S->planes, S->cfg.b_y, S->cfg.level_mode,
-                             S->cfg.seed, S->c_y, S->yhat, nullptr, st)) != IHT_OK)
+  if ((rc = iht_quantize_vec_batched(S->y, S->rows, q0.row_offset, S->planes, S->cfg.b_y, S->cfg.level_mode,
+                                     S->cfg.seed, S->c_y, B, S->yhat, nullptr, st)) != IHT_OK)
     return rc;
   L += 1;
-  // x^[1] = 0 (reading c8): the "slot -1" is represented by slot_of(n=0)
-  IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz, 0, sizeof(int32_t), st));   // slot 0 holds x^[1]
+  // x^[1] = 0 (reading c8): slot 0 holds x^[1]
+  IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz, 0, sizeof(int32_t) * B, st));
   const int K = (int)S->pool.size();
-  const int s = S->cfg.s;
+  const int64_t xslot = (int64_t)B * s;
   for (int n = 1; n <= S->cfg.n_iter; ++n) {
     const int in_slot = S->cfg.trace ? (n - 1) : ((n - 1) & 1);
     const int out_slot = S->cfg.trace ? n : (n & 1);
     const iht_qmat& A = S->pool[(2 * n - 2) % K];   // Phi-hat_{2n-1} (1-based), adjoint
     const iht_qmat& F = S->pool[(2 * n - 1) % K];   // Phi-hat_{2n}, forward
-    if ((rc = iht_forward(&F, S->xs_idx + (int64_t)in_slot * s, S->xs_val + (int64_t)in_slot * s,
-                          S->xs_nnz + in_slot, s, S->yhat, S->r, nullptr, 0, st)) != IHT_OK)
-      return rc;
+    const int32_t* xi = S->xs_idx + in_slot * xslot;
+    const float* xv = S->xs_val + in_slot * xslot;
+    const int32_t* xn = S->xs_nnz + (int64_t)in_slot * B;
+    int32_t* oi = S->xs_idx + out_slot * xslot;
+    float* ov = S->xs_val + out_slot * xslot;
+    int32_t* on = S->xs_nnz + (int64_t)out_slot * B;
+    // (a4) forward: r_b = y-hat_b - Phi-hat_F x_b  (column shards: partial, then summed)
+    const float* yh = (S->colshard && S->rank != 0) ? nullptr : S->yhat;
+    if ((rc = iht_forward_batched(&F, xi, xv, xn, s, s, B, yh, S->r, st)) != IHT_OK) return rc;
     L += 1;
+    if (S->colshard) {
+      if ((rc = iht_comm_allreduce(S->cfg.comm, S->r, (int64_t)B * S->vlen, 0, st)) != IHT_OK) return rc;
+    }
+    // (a5) adjoint
     if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[2 * (n - 1)], st));
-    if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
-      return rc;
+    if (!S->batched) {
+      if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
+        return rc;
+      L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
+    } else {
+      if ((rc = iht_adjoint_batched(&A, S->r, B, S->g, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK) return rc;
+      L += 2 * ((B + 63) / 64);
+    }
     if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[2 * (n - 1) + 1], st));
-    L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
-    if (S->cfg.comm && S->cfg.comm->world > 1) {
+    if (S->rowshard) {
       if ((rc = iht_comm_allreduce(S->cfg.comm, S->g, S->N, 0, st)) != IHT_OK) return rc;
     }
-    if ((rc = iht_threshold(S->xs_idx + (int64_t)in_slot * s, S->xs_val + (int64_t)in_slot * s,
-                            S->xs_nnz + in_slot, S->g, S->cfg.mu, s, S->N,
-                            S->xs_idx + (int64_t)out_slot * s, S->xs_val + (int64_t)out_slot * s,
-                            S->xs_nnz + out_slot, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
-      return rc;
-    L += 3;   // update+histogram, candidates, select
+    // (a6) update + H_s
+    if (!S->colshard) {
+      if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
+                                      S->ws_thr_bytes, st)) != IHT_OK)
+        return rc;
+      L += 3;
+    } else {
+      int32_t* ci = S->cand_send;
+      float* cv = reinterpret_cast<float*>(S->cand_send + xslot);
+      int32_t* cn = S->cand_send + 2 * xslot;
+      if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, q0.col_offset, B, ci, cv, s, cn,
+                                      S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+        return rc;
+      L += 3;
+      if ((rc = iht_comm_allgather(S->cfg.comm, S->cand_send, S->cand_recv, S->cand_words * 4, st)) != IHT_OK)
+        return rc;
+      if ((rc = iht_merge_candidates(S->cand_recv, reinterpret_cast<const float*>(S->cand_recv + xslot),
+                                     S->cand_recv + 2 * xslot, S->cand_words, S->world, s, B, oi, ov, on, st)) !=
+          IHT_OK)
+        return rc;
+      L += 1;
+    }
     S->final_slot = out_slot;
   }
   if (S->cfg.n_iter == 0) S->final_slot = 0;
@@ -207,19 +263,28 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
 
 extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* cfg, iht_solver** out) {
   if (pool == nullptr || K < 1 || cfg == nullptr || out == nullptr) return IHT_EINVAL;
-  if (cfg->s < 0 || cfg->n_iter < 0 || !isfinite(cfg->mu)) return IHT_EINVAL;
+  if (cfg->s < 0 || cfg->n_iter < 0 || !isfinite(cfg->mu) || cfg->nrhs < 0) return IHT_EINVAL;
   if (cfg->b_y < 2 || cfg->b_y > 8 || (cfg->level_mode != 0 && cfg->level_mode != 1)) return IHT_EINVAL;
   if (cfg->adjoint_variant != 0 && cfg->adjoint_variant != 1) return IHT_EINVAL;
   const iht_qmat& q0 = pool[0];
   for (int k = 0; k < K; ++k) {
     const iht_qmat& q = pool[k];
     if (q.codes == nullptr || q.rows != q0.rows || q.cols != q0.cols || q.planes != q0.planes ||
-        q.bits != q0.bits || q.row_offset != q0.row_offset ||
+        q.bits != q0.bits || q.row_offset != q0.row_offset || q.col_offset != q0.col_offset ||
         q.strip_bytes != iht_strip_bytes(q.rows, q.planes, q.bits))
       return IHT_EINVAL;
   }
-  if (cfg->s > q0.rows * (cfg->comm ? cfg->comm->world : 1) * q0.planes || cfg->s > q0.cols)
-    return IHT_EINVAL;  // s <= M
+  const int world = cfg->comm ? cfg->comm->world : 1;
+  const int B = cfg->nrhs > 1 ? cfg->nrhs : 1;
+  const bool batched = B > 1;
+  if (batched && cfg->adjoint_variant != 0) return IHT_EUNSUPPORTED;
+  if (batched && cfg->comm && (q0.row_offset != 0 || q0.col_offset != (int64_t)cfg->comm->rank * q0.cols))
+    return IHT_EINVAL;   // column shards of equal width, rank-ordered
+  if (!batched && q0.col_offset != 0) return IHT_EINVAL;
+  const int64_t Mg = batched ? q0.rows : q0.rows * world;          // global rows
+  const int64_t Ng = batched ? q0.cols * world : q0.cols;          // global columns
+  if (cfg->s > Mg * q0.planes || cfg->s > Ng) return IHT_EINVAL;   // s <= M
+  if (batched && cfg->comm && (int64_t)world * cfg->s > 8192) return IHT_EUNSUPPORTED;
   iht_solver* S = new iht_solver();
   S->pool.assign(pool, pool + K);
   S->cfg = *cfg;
@@ -227,17 +292,27 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
   S->N = q0.cols;
   S->planes = q0.planes;
   S->vlen = iht_vec_len(q0.rows, q0.planes);
-  S->ws_adj_bytes = iht_adjoint_ws_bytes(&q0);
-  S->ws_thr_bytes = iht_threshold_ws_bytes(S->N, cfg->s);
+  S->B = B;
+  S->batched = batched;
+  S->world = world;
+  S->rank = cfg->comm ? cfg->comm->rank : 0;
+  S->rowshard = !batched && world > 1;
+  S->colshard = batched && cfg->comm != nullptr;   // any world size (world 1 exercises the same path)
+  S->ws_adj_bytes = batched ? iht_adjoint_batched_ws_bytes(&q0, B) : iht_adjoint_ws_bytes(&q0);
+  S->ws_thr_bytes = iht_threshold_batched_ws_bytes(S->N, cfg->s, B);
   S->nslots = cfg->trace ? cfg->n_iter + 1 : 2;
   const int s = cfg->s > 0 ? cfg->s : 1;
+  S->cand_words = S->colshard ? 2 * (int64_t)B * s + B : 0;
   auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
   const int64_t ycount = q0.rows * q0.planes;
-  const int64_t sz_y = al(ycount * 4), sz_c = al(4), sz_v = al(S->vlen * 4), sz_g = al(S->N * 4),
+  const int64_t sz_y = al((int64_t)B * ycount * 4), sz_c = al((int64_t)B * 4),
+                sz_v = al((int64_t)B * S->vlen * 4), sz_g = al((int64_t)B * S->N * 4),
                 sz_wa = al(S->ws_adj_bytes), sz_wt = al(S->ws_thr_bytes),
-                sz_xi = al((int64_t)S->nslots * s * 4), sz_xv = al((int64_t)S->nslots * s * 4),
-                sz_xn = al((int64_t)S->nslots * 4);
-  const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_xi + sz_xv + sz_xn;
+                sz_xi = al((int64_t)S->nslots * B * s * 4), sz_xv = al((int64_t)S->nslots * B * s * 4),
+                sz_xn = al((int64_t)S->nslots * B * 4), sz_cs = al(S->cand_words * 4),
+                sz_cr = al(S->cand_words * 4 * world);
+  const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_xi + sz_xv + sz_xn +
+                        (S->colshard ? sz_cs + sz_cr : 0);
   if (cudaMalloc(&S->block, total) != cudaSuccess) {
     delete S;
     return IHT_ENOMEM;
@@ -253,6 +328,11 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
   S->xs_idx = reinterpret_cast<int32_t*>(p); p += sz_xi;
   S->xs_val = reinterpret_cast<float*>(p); p += sz_xv;
   S->xs_nnz = reinterpret_cast<int32_t*>(p); p += sz_xn;
+  if (S->colshard) {
+    S->cand_send = reinterpret_cast<int32_t*>(p); p += sz_cs;
+    S->cand_recv = reinterpret_cast<int32_t*>(p); p += sz_cr;
+  }
+  // zero everything once (pad rows of the stacked vectors stay 0)
   if (cudaMemset(S->block, 0, total) != cudaSuccess ||
       cudaStreamCreateWithFlags(&S->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
     cudaFree(S->block);
@@ -292,18 +372,16 @@ extern "C" int iht_solver_destroy(iht_solver* S) {
 
 static int ensure_graph(iht_solver* S) {
   if (S->exec) return IHT_OK;
-  cudaGraph_t graph;
   IHT_CUDA_CHECK(cudaStreamBeginCapture(S->cap_stream, cudaStreamCaptureModeThreadLocal));
   int64_t L = 0;
   const int rc = enqueue_run(S, S->cap_stream, &L);
-  cudaGraph_t g2;
-  const cudaError_t e = cudaStreamEndCapture(S->cap_stream, &g2);
+  cudaGraph_t graph;
+  const cudaError_t e = cudaStreamEndCapture(S->cap_stream, &graph);
   if (rc != IHT_OK) {
-    if (e == cudaSuccess) cudaGraphDestroy(g2);
+    if (e == cudaSuccess) cudaGraphDestroy(graph);
     return rc;
   }
   IHT_CUDA_CHECK(e);
-  graph = g2;
   const cudaError_t ei = cudaGraphInstantiate(&S->exec, graph, 0);
   cudaGraphDestroy(graph);
   IHT_CUDA_CHECK(ei);
@@ -317,7 +395,7 @@ extern "C" int iht_solver_run(iht_solver* S, const float* y, int flags, int32_t*
     return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const bool host = (flags & IHT_HOST_IO) != 0;
-  const int64_t ycount = S->rows * S->planes;
+  const int64_t ycount = S->rows * S->planes * S->B;
   IHT_CUDA_CHECK(cudaMemcpyAsync(S->y, y, ycount * sizeof(float),
                                  host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
   int rc;
@@ -329,17 +407,18 @@ extern "C" int iht_solver_run(iht_solver* S, const float* y, int flags, int32_t*
     if ((rc = enqueue_run(S, st, &L)) != IHT_OK) return rc;
     S->launches = L;
   }
-  const int s = S->cfg.s;
+  const int64_t xs = (int64_t)S->B * S->cfg.s;
   const int fs = S->final_slot;
   const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  if (s > 0) {
-    IHT_CUDA_CHECK(cudaMemcpyAsync(out_idx, S->xs_idx + (int64_t)fs * s, s * sizeof(int32_t), kind, st));
-    IHT_CUDA_CHECK(cudaMemcpyAsync(out_val, S->xs_val + (int64_t)fs * s, s * sizeof(float), kind, st));
+  if (xs > 0) {
+    IHT_CUDA_CHECK(cudaMemcpyAsync(out_idx, S->xs_idx + fs * xs, xs * sizeof(int32_t), kind, st));
+    IHT_CUDA_CHECK(cudaMemcpyAsync(out_val, S->xs_val + fs * xs, xs * sizeof(float), kind, st));
   }
-  IHT_CUDA_CHECK(cudaMemcpyAsync(out_nnz, S->xs_nnz + fs, sizeof(int32_t), kind, st));
+  IHT_CUDA_CHECK(cudaMemcpyAsync(out_nnz, S->xs_nnz + (int64_t)fs * S->B, S->B * sizeof(int32_t), kind, st));
   if (host) {
     IHT_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (*out_nnz < 0) return IHT_EDOMAIN;
+    for (int b = 0; b < S->B; ++b)
+      if (out_nnz[b] < 0) return IHT_EDOMAIN;
   }
   return IHT_OK;
 }
@@ -348,15 +427,16 @@ extern "C" int iht_solver_trace(iht_solver* S, int32_t* idx_host, float* val_hos
                                 void* stream) {
   if (S == nullptr || !S->cfg.trace) return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  const int s = S->cfg.s, n = S->cfg.n_iter;
+  const int n = S->cfg.n_iter;
+  const int64_t xs = (int64_t)S->B * S->cfg.s;
   if (n == 0) return IHT_OK;
-  if (s > 0) {
-    IHT_CUDA_CHECK(cudaMemcpyAsync(idx_host, S->xs_idx + s, (size_t)n * s * sizeof(int32_t),
+  if (xs > 0) {
+    IHT_CUDA_CHECK(cudaMemcpyAsync(idx_host, S->xs_idx + xs, (size_t)n * xs * sizeof(int32_t),
                                    cudaMemcpyDeviceToHost, st));
-    IHT_CUDA_CHECK(cudaMemcpyAsync(val_host, S->xs_val + s, (size_t)n * s * sizeof(float),
+    IHT_CUDA_CHECK(cudaMemcpyAsync(val_host, S->xs_val + xs, (size_t)n * xs * sizeof(float),
                                    cudaMemcpyDeviceToHost, st));
   }
-  IHT_CUDA_CHECK(cudaMemcpyAsync(nnz_host, S->xs_nnz + 1, (size_t)n * sizeof(int32_t),
+  IHT_CUDA_CHECK(cudaMemcpyAsync(nnz_host, S->xs_nnz + S->B, (size_t)n * S->B * sizeof(int32_t),
                                  cudaMemcpyDeviceToHost, st));
   IHT_CUDA_CHECK(cudaStreamSynchronize(st));
   return IHT_OK;

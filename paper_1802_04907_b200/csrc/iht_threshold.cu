@@ -19,6 +19,9 @@
 //                        shared memory, finishes the radix select on them and writes the
 //                        ordered support.  If the candidates do not fit (massive ties,
 //                        mostly-zero a) it falls back to the full single-CTA select over a.
+// Batched (config 5): grid row blockIdx.y (T3: blockIdx.x) = snapshot b, each with its own
+// x_b, g_b, workspace slice and output; a column shard adds col_offset to every index.
+// iht_merge_candidates (T4, 1 CTA per snapshot) merges the shards' local top-s lists.
 #include "iht_internal.cuh"
 
 namespace iht {
@@ -170,34 +173,57 @@ struct ThrWs {
   int* ccount;       // [ntiles]
   int* hist;         // [kHistBins] global histogram of digit 1
   int* flags;        // [0] nan
+  int64_t hdr_stride, body_stride;   // bytes between consecutive snapshots' slices
 };
 
-__host__ __device__ inline int64_t thr_ws_layout(int64_t N, char* base, ThrWs* w) {
-  auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+// Workspace: [nrhs] headers (hist + flags, zeroed by one memset), then [nrhs] bodies.
+__host__ __device__ inline int64_t al256(int64_t b) { return (b + 255) / 256 * 256; }
+__host__ __device__ inline int64_t thr_hdr_bytes() { return al256(kHistBins * 4) + al256(16); }
+__host__ __device__ inline int64_t thr_body_bytes(int64_t N) {
   const int64_t ntiles = (N + kTile - 1) / kTile;
-  int64_t off = 0;
-  if (w) w->hist = reinterpret_cast<int*>(base + off);
-  off += al(kHistBins * 4);
-  if (w) w->flags = reinterpret_cast<int*>(base + off);
-  off += al(16);
-  const int64_t clear_bytes = off;       // hist + flags are zeroed by the launcher
-  if (w) w->a = reinterpret_cast<float*>(base + off);
-  off += al(N * 4);
-  if (w) w->cidx = reinterpret_cast<int32_t*>(base + off);
-  off += al(N * 4);
-  if (w) w->cval = reinterpret_cast<float*>(base + off);
-  off += al(N * 4);
-  if (w) w->ccount = reinterpret_cast<int*>(base + off);
-  off += al(ntiles * 4);
-  (void)clear_bytes;
-  return off;
+  return 3 * al256(N * 4) + al256(ntiles * 4);
+}
+__host__ __device__ inline int64_t thr_ws_layout(int64_t N, int nrhs, char* base, ThrWs* w) {
+  const int64_t hdr = thr_hdr_bytes(), body = thr_body_bytes(N);
+  if (w) {
+    w->hist = reinterpret_cast<int*>(base);
+    w->flags = reinterpret_cast<int*>(base + al256(kHistBins * 4));
+    char* b0 = base + nrhs * hdr;
+    w->a = reinterpret_cast<float*>(b0);
+    w->cidx = reinterpret_cast<int32_t*>(b0 + al256(N * 4));
+    w->cval = reinterpret_cast<float*>(b0 + 2 * al256(N * 4));
+    w->ccount = reinterpret_cast<int*>(b0 + 3 * al256(N * 4));
+    w->hdr_stride = hdr;
+    w->body_stride = body;
+  }
+  return nrhs * (hdr + body);
+}
+
+// Slice of snapshot b.
+__device__ __forceinline__ ThrWs thr_at(const ThrWs& w, int b) {
+  ThrWs o = w;
+  auto adv = [](auto* p, int64_t bytes) { return reinterpret_cast<decltype(p)>(reinterpret_cast<char*>(p) + bytes); };
+  o.hist = adv(w.hist, b * w.hdr_stride);
+  o.flags = adv(w.flags, b * w.hdr_stride);
+  o.a = adv(w.a, b * w.body_stride);
+  o.cidx = adv(w.cidx, b * w.body_stride);
+  o.cval = adv(w.cval, b * w.body_stride);
+  o.ccount = adv(w.ccount, b * w.body_stride);
+  return o;
 }
 
 // T1: a = x + mu g, global histogram of key >> 20
 __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
-    int32_t max_nnz, const float* __restrict__ g, float mu, int64_t N, ThrWs w) {
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, int64_t N, int64_t col_offset,
+    ThrWs w0) {
   __shared__ float as[kTile];
+  const int bq = blockIdx.y;
+  const ThrWs w = thr_at(w0, bq);
+  x_idx += (int64_t)bq * ldx;
+  x_val += (int64_t)bq * ldx;
+  x_nnz += bq;
+  g += (int64_t)bq * N;
   __shared__ int hist[kHistBins];
   const int tid = threadIdx.x;
   const int64_t start = (int64_t)blockIdx.x * kTile;
@@ -208,7 +234,7 @@ __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
   nnz = nnz < 0 ? 0 : min(nnz, max_nnz);
   __syncthreads();
   for (int j = tid; j < nnz; j += kTileThreads) {
-    const int64_t n = x_idx[j];
+    const int64_t n = (int64_t)x_idx[j] - col_offset;   // local column (column shards)
     if (n >= start && n < start + cnt) as[n - start] = __fadd_rn(x_val[j], as[n - start]);
   }
   __syncthreads();
@@ -228,7 +254,8 @@ __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
 
 // T2: bin d1 of the s-th largest key (same in every CTA), ordered per-tile compaction
 // of the entries with digit >= d1 (key > 0).
-__global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N, ThrWs w) {
+__global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N, int64_t col_offset, ThrWs w0) {
+  const ThrWs w = thr_at(w0, blockIdx.y);
   __shared__ int sfx[kTileThreads];
   __shared__ int d1s;
   __shared__ int wcnt[kTileThreads / 32];
@@ -279,7 +306,7 @@ __global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N,
     const unsigned int b = __ballot_sync(0xffffffffu, sel);
     if (sel) {
       const int pos = base + __popc(b & lt);
-      w.cidx[start + pos] = (int32_t)(start + i);
+      w.cidx[start + pos] = (int32_t)(col_offset + start + i);
       w.cval[start + pos] = v;
     }
     base += __popc(b);
@@ -293,8 +320,14 @@ __global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N,
 
 // T3: gather candidates (index order) and finish the selection in one CTA.
 __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
-    const int32_t* __restrict__ x_nnz, int s, int64_t N, ThrWs w, int32_t* __restrict__ out_idx,
-    float* __restrict__ out_val, int32_t* __restrict__ out_nnz) {
+    const int32_t* __restrict__ x_nnz, int s, int64_t N, int64_t col_offset, ThrWs w0,
+    int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz) {
+  const int bq = blockIdx.x;
+  const ThrWs w = thr_at(w0, bq);
+  x_nnz += bq;
+  out_idx += (int64_t)bq * ldo;
+  out_val += (int64_t)bq * ldo;
+  out_nnz += bq;
   extern __shared__ __align__(16) unsigned char dsm[];
   int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
   float* cval = reinterpret_cast<float*>(dsm + kCandCap * 4);
@@ -344,46 +377,132 @@ __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
                    out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
   } else {
     const float* a = w.a;
-    select_ordered((int)N, s, [&](int i) { return a[i]; }, [&](int i) { return i; }, out_idx, out_val, out_nnz, 0,
-                   hist, scratch, wgt, weq, wtake, wbase, sh);
+    const int c0 = (int)col_offset;
+    select_ordered((int)N, s, [&](int i) { return a[i]; }, [&](int i) { return c0 + i; }, out_idx, out_val,
+                   out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
   }
+}
+
+// T4: merge of the shards' local top-s lists (column-sharded batched path): the global
+// top-s is contained in the union of the local top-s (same tie rule), and the shards'
+// lists concatenated in shard order are in increasing global index order.
+__global__ void __launch_bounds__(kThrThreads, 1) thr_merge(
+    const int32_t* __restrict__ cidx_g, const float* __restrict__ cval_g, const int32_t* __restrict__ cnnz_g,
+    int64_t stride, int P, int s, int nrhs, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
+    int32_t* __restrict__ out_nnz) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  float* cval = reinterpret_cast<float*>(dsm + kCandCap * 4);
+  __shared__ int hist[2048];
+  __shared__ int scratch[kThrWarps];
+  __shared__ int wgt[kThrWarps], weq[kThrWarps], wtake[kThrWarps], wbase[kThrWarps];
+  __shared__ int sh[4];
+  __shared__ int base[1025];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  out_idx += (int64_t)b * s;
+  out_val += (int64_t)b * s;
+  if (tid == 0) {
+    int acc = 0, bad = 0;
+    for (int p = 0; p < P; ++p) {
+      const int c = cnnz_g[(int64_t)p * stride + b];
+      bad |= c < 0;
+      base[p] = acc;
+      acc += c < 0 ? 0 : min(c, s);
+    }
+    sh[3] = bad ? -1 : acc;
+  }
+  __syncthreads();
+  const int total = sh[3];
+  if (total < 0 || s == 0) {
+    if (tid == 0) out_nnz[b] = total < 0 ? -1 : 0;
+    return;
+  }
+  for (int p = tid >> 5; p < P; p += kThrWarps) {
+    const int c = min(cnnz_g[(int64_t)p * stride + b], s);
+    const int64_t src = (int64_t)p * stride + (int64_t)b * s;
+    for (int i = tid & 31; i < c; i += 32) {
+      cidx[base[p] + i] = cidx_g[src + i];
+      cval[base[p] + i] = cval_g[src + i];
+    }
+  }
+  __syncthreads();
+  select_ordered(total, s, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, out_idx, out_val,
+                 out_nnz + b, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
 }
 
 }  // namespace iht
 
 using namespace iht;
 
-extern "C" int64_t iht_threshold_ws_bytes(int64_t N, int32_t s) {
+extern "C" int64_t iht_threshold_batched_ws_bytes(int64_t N, int32_t s, int32_t nrhs) {
   (void)s;
-  if (N <= 0) return -1;
-  return thr_ws_layout(N, nullptr, nullptr);
+  if (N <= 0 || nrhs <= 0) return -1;
+  return thr_ws_layout(N, nrhs, nullptr, nullptr);
+}
+
+extern "C" int64_t iht_threshold_ws_bytes(int64_t N, int32_t s) { return iht_threshold_batched_ws_bytes(N, s, 1); }
+
+static bool g_thr_attr = false;
+
+static int thr_attrs() {
+  if (!g_thr_attr) {
+    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
+    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
+    g_thr_attr = true;
+  }
+  return IHT_OK;
+}
+
+extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                                     const float* g, float mu, int32_t s, int64_t N, int64_t col_offset,
+                                     int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo,
+                                     int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream) {
+  if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr ||
+      s < 0 || N <= 0 || N > 0x7FFFFFFFll || nrhs <= 0 || nrhs > 65535 || ldo < s || ldx < 0 ||
+      col_offset < 0 || col_offset + N > 0x7FFFFFFFll)
+    return IHT_EINVAL;
+  if (ldx > 0 && (x_idx == nullptr || x_val == nullptr)) return IHT_EINVAL;
+  if (ws == nullptr || ws_bytes < thr_ws_layout(N, nrhs, nullptr, nullptr)) return IHT_EINVAL;
+  if (!isfinite(mu)) return IHT_EDOMAIN;
+  int rc;
+  if ((rc = thr_attrs()) != IHT_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  ThrWs w{};
+  thr_ws_layout(N, nrhs, static_cast<char*>(ws), &w);
+  IHT_CUDA_CHECK(cudaMemsetAsync(ws, 0, nrhs * thr_hdr_bytes(), st));
+  const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
+  // max_nnz: the caller's x arrays hold at most min(ldx, s) entries (x is an H_s output)
+  const int32_t max_nnz = ldx < s ? ldx : s;
+  thr_update_hist<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, N,
+                                                              col_offset, w);
+  IHT_LAUNCH_CHECK();
+  thr_candidates<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(s, N, col_offset, w);
+  IHT_LAUNCH_CHECK();
+  thr_select<<<nrhs, kThrThreads, kCandCap * 8, st>>>(x_nnz, s, N, col_offset, w, out_idx, out_val, ldo, out_nnz);
+  IHT_LAUNCH_CHECK();
+  return IHT_OK;
 }
 
 extern "C" int iht_threshold(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz,
                              const float* g, float mu, int32_t s, int64_t N, int32_t* out_idx,
                              float* out_val, int32_t* out_nnz, void* ws, int64_t ws_bytes,
                              void* stream) {
-  if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr ||
-      out_nnz == nullptr || s < 0 || N <= 0 || N > 0x7FFFFFFFll)
+  return iht_threshold_batched(x_idx, x_val, x_nnz, s, g, mu, s, N, 0, 1, out_idx, out_val, s > 0 ? s : 0,
+                               out_nnz, ws, ws_bytes, stream);
+}
+
+extern "C" int iht_merge_candidates(const int32_t* cand_idx, const float* cand_val, const int32_t* cand_nnz,
+                                    int64_t shard_stride, int32_t P, int32_t s, int32_t nrhs, int32_t* out_idx,
+                                    float* out_val, int32_t* out_nnz, void* stream) {
+  if (cand_idx == nullptr || cand_val == nullptr || cand_nnz == nullptr || out_idx == nullptr ||
+      out_val == nullptr || out_nnz == nullptr || P <= 0 || P > 1024 || s < 0 || nrhs <= 0 || nrhs > 65535 ||
+      (P > 1 && shard_stride < (int64_t)nrhs * s))
     return IHT_EINVAL;
-  if (ws == nullptr || ws_bytes < thr_ws_layout(N, nullptr, nullptr)) return IHT_EINVAL;
-  if (!isfinite(mu)) return IHT_EDOMAIN;
-  cudaStream_t st = (cudaStream_t)stream;
-  ThrWs w{};
-  thr_ws_layout(N, static_cast<char*>(ws), &w);
-  static bool attr = false;
-  if (!attr) {
-    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
-    attr = true;
-  }
-  IHT_CUDA_CHECK(cudaMemsetAsync(w.hist, 0, reinterpret_cast<char*>(w.a) - reinterpret_cast<char*>(w.hist), st));
-  const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
-  // max_nnz: the caller's x arrays hold at most s entries (x is an H_s output)
-  thr_update_hist<<<tiles, kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, s, g, mu, N, w);
-  IHT_LAUNCH_CHECK();
-  thr_candidates<<<tiles, kTileThreads, 0, st>>>(s, N, w);
-  IHT_LAUNCH_CHECK();
-  thr_select<<<1, kThrThreads, kCandCap * 8, st>>>(x_nnz, s, N, w, out_idx, out_val, out_nnz);
+  if ((int64_t)P * s > kCandCap) return IHT_EUNSUPPORTED;
+  int rc;
+  if ((rc = thr_attrs()) != IHT_OK) return rc;
+  thr_merge<<<nrhs, kThrThreads, kCandCap * 8, (cudaStream_t)stream>>>(cand_idx, cand_val, cand_nnz, shard_stride, P, s, nrhs,
+                                                                      out_idx, out_val, out_nnz);
   IHT_LAUNCH_CHECK();
   return IHT_OK;
 }

@@ -15,8 +15,9 @@ import torch
 from . import _lib
 from ._lib import IhtConfig, IhtQmat, check, load
 
-__all__ = ["absmax", "quantize", "quantize_rows", "quantize_vec", "forward", "adjoint", "adjoint_batched", "threshold", "Solver", "solve",
-           "Comm", "QCopy", "strip_bytes", "vec_len", "rows_pad"]
+__all__ = ["absmax", "absmax_batched", "quantize", "quantize_rows", "quantize_vec", "quantize_vec_batched", "forward",
+           "forward_batched", "adjoint", "adjoint_batched", "threshold", "threshold_batched", "merge_candidates",
+           "Solver", "solve", "Comm", "QCopy", "strip_bytes", "vec_len", "rows_pad"]
 
 
 def _stream(stream=None):
@@ -78,13 +79,13 @@ class QCopy:
 
 
 def new_copy(rows, cols, planes, bits, level_mode, seed, copy_id, scale_c, row_offset=0, device=None,
-             codes=None):
+             codes=None, col_offset=0):
     sb = strip_bytes(rows, planes, bits)
     if codes is None:
         codes = torch.empty(load().iht_qmat_bytes(rows, cols, planes, bits), dtype=torch.uint8,
                             device=device or "cuda")
     d = IhtQmat(rows=rows, cols=cols, row_offset=row_offset, planes=planes, bits=bits, level_mode=level_mode,
-                copy_id=copy_id, seed=seed, scale_c=float(scale_c), reserved=0, strip_bytes=sb,
+                copy_id=copy_id, seed=seed, scale_c=float(scale_c), col_offset=col_offset, strip_bytes=sb,
                 codes=codes.data_ptr())
     return QCopy(d, codes)
 
@@ -100,16 +101,30 @@ def absmax(src, stream=None):
     return out
 
 
-def quantize(phi, bits, level_mode, seed, copy_ids, scale_c, row_offset=0, stream=None):
+def absmax_batched(src, stream=None):
+    """(a1) per-row c_b = max |src[b]| of a (B, n) float32 / complex64 CUDA tensor; returns (B,) floats."""
+    _require_cuda(src)
+    flat = torch.view_as_real(src) if src.is_complex() else src
+    if not flat.is_contiguous():
+        raise ValueError("absmax_batched needs a contiguous tensor")
+    B = flat.shape[0]
+    out = torch.empty(B, dtype=torch.float32, device=src.device)
+    check(load().iht_absmax_batched(_ptr(flat), flat.numel() // B, B, _ptr(out), _stream(stream)),
+          "iht_absmax_batched")
+    return out
+
+
+def quantize(phi, bits, level_mode, seed, copy_ids, scale_c, row_offset=0, stream=None, col_offset=0):
     """(a2) quantise a (rows x cols) float32 or complex64 CUDA matrix into len(copy_ids)
-    independent copies in one pass; returns a list of QCopy."""
+    independent copies in one pass; returns a list of QCopy.  col_offset: global index of
+    column 0 (column shards; a multiple of 16)."""
     _require_cuda(phi)
     planes = 2 if phi.is_complex() else 1
     rows, cols = phi.shape
     if phi.stride(1) != 1:
         raise ValueError("phi must be row-major (unit column stride)")
-    copies = [new_copy(rows, cols, planes, bits, level_mode, seed, cid, scale_c, row_offset, phi.device)
-              for cid in copy_ids]
+    copies = [new_copy(rows, cols, planes, bits, level_mode, seed, cid, scale_c, row_offset, phi.device,
+                       col_offset=col_offset) for cid in copy_ids]
     arr = (IhtQmat * len(copies))(*[c.desc for c in copies])
     base = torch.view_as_real(phi) if planes == 2 else phi
     check(load().iht_quantize(_ptr(base), phi.stride(0), arr, len(copies), _stream(stream)), "iht_quantize")
@@ -138,6 +153,31 @@ def quantize_vec(y, bits, level_mode, seed, c_dev, row_offset=0, with_codes=Fals
     check(load().iht_quantize_vec(_ptr(base), rows, row_offset, planes, bits, level_mode, seed, _ptr(c_dev),
                                   _ptr(yhat), _ptr(codes), _stream(stream)), "iht_quantize_vec")
     return yhat, codes
+
+
+def quantize_vec_batched(Y, bits, level_mode, seed, c_dev, row_offset=0, with_codes=False, stream=None):
+    """(a3) batched: Y (B, rows) float32 / complex64; snapshot b is column n = b of the
+    observation matrix.  Returns (yhat (B, vec_len) float32, codes (B, planes*rows) or None)."""
+    _require_cuda(Y, c_dev)
+    planes = 2 if Y.is_complex() else 1
+    B, rows = Y.shape
+    base = torch.view_as_real(Y).contiguous() if planes == 2 else Y.contiguous()
+    yhat = torch.empty((B, vec_len(rows, planes)), dtype=torch.float32, device=Y.device)
+    codes = torch.empty((B, planes * rows), dtype=torch.uint8, device=Y.device) if with_codes else None
+    check(load().iht_quantize_vec_batched(_ptr(base), rows, row_offset, planes, bits, level_mode, seed, _ptr(c_dev),
+                                          B, _ptr(yhat), _ptr(codes), _stream(stream)), "iht_quantize_vec_batched")
+    return yhat, codes
+
+
+def forward_batched(F, x_idx, x_val, x_nnz, yhat, stream=None):
+    """(a4) batched: x_idx / x_val (B, ldx), x_nnz (B,) int32, yhat (B, vec_len) or None
+    (partial product of a column shard); returns r (B, vec_len)."""
+    _require_cuda(x_idx, x_val, x_nnz)
+    B, ldx = x_idx.shape
+    r = torch.empty((B, vec_len(F.rows, F.planes)), dtype=torch.float32, device=x_idx.device)
+    check(load().iht_forward_batched(ctypes.byref(F.desc), _ptr(x_idx), _ptr(x_val), _ptr(x_nnz), ldx, ldx, B,
+                                     _ptr(yhat), _ptr(r), _stream(stream)), "iht_forward_batched")
+    return r
 
 
 def forward(F, x_idx, x_val, x_nnz, yhat, max_nnz=None, stream=None):
@@ -191,6 +231,48 @@ def threshold(x_idx, x_val, x_nnz, g, mu, s, stream=None):
     return oi, ov, on
 
 
+def threshold_batched(x_idx, x_val, x_nnz, G, mu, s, col_offset=0, stream=None):
+    """(a6) batched H_s per snapshot: x_idx / x_val (B, ldx) (global indices), x_nnz (B,),
+    G (B, N) local gradients of columns [col_offset, col_offset + N).  Returns
+    (idx (B, s), val (B, s), nnz (B,)) with global indices."""
+    _require_cuda(x_idx, x_val, x_nnz, G)
+    lib = load()
+    B, N = G.shape
+    ldx = x_idx.shape[1]
+    ws_bytes = lib.iht_threshold_batched_ws_bytes(N, s, B)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=G.device)
+    ldo = max(s, 1)
+    oi = torch.empty((B, ldo), dtype=torch.int32, device=G.device)
+    ov = torch.empty((B, ldo), dtype=torch.float32, device=G.device)
+    on = torch.empty(B, dtype=torch.int32, device=G.device)
+    check(lib.iht_threshold_batched(_ptr(x_idx), _ptr(x_val), _ptr(x_nnz), ldx, _ptr(G), float(mu), s, N, col_offset,
+                                    B, _ptr(oi), _ptr(ov), ldo, _ptr(on), _ptr(ws), ws_bytes, _stream(stream)),
+          "iht_threshold_batched")
+    return oi, ov, on
+
+
+def merge_candidates(cand_idx, cand_val, cand_nnz, s, stream=None):
+    """Global H_s from per-shard lists: cand_idx / cand_val (P, B, s), cand_nnz (P, B)."""
+    _require_cuda(cand_idx, cand_val, cand_nnz)
+    P, B, _ = cand_idx.shape
+    if cand_nnz.shape != (P, B):
+        raise ValueError("cand_nnz must be (P, B)")
+    # the C call takes one shard stride for all three arrays: repack into [P][idx | val | nnz]
+    words = 2 * B * s + B
+    pack = torch.empty((P, words), dtype=torch.int32, device=cand_idx.device)
+    pack[:, :B * s] = cand_idx.reshape(P, B * s)
+    pack[:, B * s:2 * B * s] = cand_val.reshape(P, B * s).view(torch.int32)
+    pack[:, 2 * B * s:] = cand_nnz
+    oi = torch.empty((B, max(s, 1)), dtype=torch.int32, device=cand_idx.device)
+    ov = torch.empty((B, max(s, 1)), dtype=torch.float32, device=cand_idx.device)
+    on = torch.empty(B, dtype=torch.int32, device=cand_idx.device)
+    base = pack.data_ptr()
+    check(load().iht_merge_candidates(ctypes.c_void_p(base), ctypes.c_void_p(base + 4 * B * s),
+                                      ctypes.c_void_p(base + 8 * B * s), words, P, s, B, _ptr(oi), _ptr(ov), _ptr(on),
+                                      _stream(stream)), "iht_merge_candidates")
+    return oi, ov, on
+
+
 class Comm:
     """NCCL communicator of libiht (iht_comm_*); unique id broadcast via torch.distributed."""
 
@@ -215,6 +297,13 @@ class Comm:
               "iht_comm_allreduce")
         return t
 
+    def allgather(self, t, stream=None):
+        """All-gather of a contiguous CUDA tensor: returns (world, *t.shape)."""
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        check(load().iht_comm_allgather(self.handle, _ptr(t), _ptr(out), t.numel() * t.element_size(),
+                                        _stream(stream)), "iht_comm_allgather")
+        return out
+
     def close(self):
         if self.handle:
             load().iht_comm_destroy(self.handle)
@@ -222,25 +311,29 @@ class Comm:
 
 
 class Solver:
-    """iht_solver_*: Algorithm 1 with fixed mu over a pool of quantised copies (CUDA graph)."""
+    """iht_solver_*: Algorithm 1 with fixed mu over a pool of quantised copies (CUDA graph).
+    nrhs = B > 1: B observations sharing Phi (config 5); run() takes y of shape (B, rows)
+    and the outputs are (B, s) / (B,)."""
 
     def __init__(self, pool, s, n_iter, mu, b_y, seed, level_mode=0, adjoint_variant=0, trace=False,
-                 use_graph=True, comm=None, profile=False):
+                 use_graph=True, comm=None, profile=False, nrhs=1):
         lib = load()
         self.pool = pool                     # keep the code tensors alive
         self.s, self.n_iter = s, n_iter
         self.trace = trace
+        self.nrhs = max(1, nrhs)
         arr = (IhtQmat * len(pool))(*[c.desc for c in pool])
         cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
                         adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
-                        comm=comm.handle if comm is not None else None, profile=int(profile), reserved=0)
+                        comm=comm.handle if comm is not None else None, profile=int(profile), nrhs=self.nrhs)
         h = ctypes.c_void_p()
         check(lib.iht_solver_create(arr, len(pool), ctypes.byref(cfg), ctypes.byref(h)), "iht_solver_create")
         self.handle = h
         self.device = pool[0].codes.device
-        self.out_idx = torch.empty(max(s, 1), dtype=torch.int32, device=self.device)
-        self.out_val = torch.empty(max(s, 1), dtype=torch.float32, device=self.device)
-        self.out_nnz = torch.empty(1, dtype=torch.int32, device=self.device)
+        shape = (self.nrhs, max(s, 1)) if self.nrhs > 1 else (max(s, 1),)
+        self.out_idx = torch.empty(shape, dtype=torch.int32, device=self.device)
+        self.out_val = torch.empty(shape, dtype=torch.float32, device=self.device)
+        self.out_nnz = torch.empty(self.nrhs, dtype=torch.int32, device=self.device)
 
     def run(self, y, stream=None):
         """Device y (float32 or complex64 CUDA tensor of this shard's rows): enqueue a solve;
@@ -260,10 +353,12 @@ class Solver:
         return out_idx, out_val, out_nnz
 
     def trace_arrays(self, stream=None):
-        """Recorded iterates x^[2..n*+1]: (idx[n_iter, s], val[n_iter, s], nnz[n_iter]) numpy-like CPU tensors."""
-        idx = torch.empty((self.n_iter, max(self.s, 1)), dtype=torch.int32)
-        val = torch.empty((self.n_iter, max(self.s, 1)), dtype=torch.float32)
-        nnz = torch.empty(self.n_iter, dtype=torch.int32)
+        """Recorded iterates x^[2..n*+1]: (idx[n_iter, s], val[n_iter, s], nnz[n_iter]) CPU tensors
+        (batched: [n_iter, B, s] and [n_iter, B])."""
+        lead = (self.n_iter, self.nrhs) if self.nrhs > 1 else (self.n_iter,)
+        idx = torch.empty(lead + (max(self.s, 1),), dtype=torch.int32)
+        val = torch.empty(lead + (max(self.s, 1),), dtype=torch.float32)
+        nnz = torch.empty(lead, dtype=torch.int32)
         check(load().iht_solver_trace(self.handle, _ptr(idx), _ptr(val), _ptr(nnz), _stream(stream)),
               "iht_solver_trace")
         return idx, val, nnz

@@ -7,6 +7,8 @@ tests exercise exactly the configuration the bench times.
 """
 import time
 
+import numpy as np
+
 
 def shard_rows(M, world, rank):
     """Row shard of rank `rank` (north star: Phi sharded by rows).  Requires M % world == 0
@@ -17,11 +19,23 @@ def shard_rows(M, world, rank):
     return rows, rank * rows
 
 
-def build_pool(p, rank, world, dev, dist_on):
-    """Generate (config 4: on the device, block-wise) and quantise this rank's row shard
-    of Phi into the pool of K copies.  Returns (pool, c_phi, preprocess timings)."""
+def shard_cols(N, world, rank):
+    """Column shard of rank `rank` (batched path): equal widths, multiples of 16
+    (the tiled code layout and the quantiser's Philox column quads)."""
+    if N % (16 * world):
+        raise ValueError("column sharding needs N divisible by 16 x the GPU count")
+    cols = N // world
+    return cols, rank * cols
+
+
+def build_pool(p, rank, world, dev, dist_on, shard="rows"):
+    """Generate (config 4: on the device, block-wise) and quantise this rank's shard of Phi
+    (row shard, or column shard for the batched path) into the pool of K copies.
+    Returns (pool, c_phi, preprocess timings, rows, row0)."""
     import torch
     from . import iht
+    if shard == "cols":
+        return _build_pool_cols(p, rank, world, dev, dist_on)
     rows, row0 = shard_rows(p.M, world, rank)
     t = {}
     if p.phi is None:
@@ -70,3 +84,32 @@ def build_pool(p, rank, world, dev, dist_on):
     return pool, c, t, rows, row0
 
 
+
+
+def _build_pool_cols(p, rank, world, dev, dist_on):
+    import torch
+    from . import iht
+    if p.phi is None:
+        raise ValueError("column sharding needs a materialised Phi")
+    cols, col0 = shard_cols(p.N, world, rank)
+    t = {}
+    phi = torch.from_numpy(np.ascontiguousarray(p.phi[:, col0:col0 + cols])).to(dev)   # (M, cols) row-major
+    t0 = time.perf_counter()
+    cmax = iht.absmax(phi)
+    torch.cuda.synchronize()
+    t["absmax_ms"] = (time.perf_counter() - t0) * 1e3
+    if dist_on:
+        import torch.distributed as dist
+        dist.all_reduce(cmax, op=dist.ReduceOp.MAX)
+    c = float(cmax.item())
+    pool = [iht.new_copy(p.M, cols, p.planes, p.b_phi, 0, p.seed, k, c, device=dev, col_offset=col0)
+            for k in range(p.K)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k0 in range(0, p.K, 8):
+        iht.quantize_rows(phi, pool[k0:k0 + 8], 0)
+    torch.cuda.synchronize()
+    t["quantize_ms"] = (time.perf_counter() - t0) * 1e3
+    del phi
+    torch.cuda.empty_cache()
+    return pool, c, t, p.M, 0

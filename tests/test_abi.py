@@ -44,7 +44,7 @@ def test_no_undeclared_signature():
 
 
 def test_sizes_and_strings(lib):
-    assert lib.iht_abi_version() == 1
+    assert lib.iht_abi_version() == 2
     assert lib.iht_rows_pad(1) == 256 and lib.iht_rows_pad(256) == 256 and lib.iht_rows_pad(257) == 512
     assert lib.iht_strip_bytes(65536, 1, 4) == 32768            # config 4: 32 KiB strips
     assert lib.iht_strip_bytes(4096, 1, 2) == 1024              # config 2
@@ -64,3 +64,14 @@ def test_host_side_validation_without_gpu(lib):
     assert lib.iht_adjoint(ctypes.byref(q), c(16), c(16), 0, c(0), 0, c(0)) == _lib.IHT_EINVAL
     assert lib.iht_threshold(c(0), c(0), c(0), c(0), 1.0, -1, 10, c(0), c(0), c(0), c(0), 0, c(0)) == _lib.IHT_EINVAL
     assert lib.iht_solver_create(None, 0, None, None) == _lib.IHT_EINVAL
+    # batched entry points (config 5) validate on the host too
+    assert lib.iht_absmax_batched(c(16), 4, 0, c(16), c(0)) == _lib.IHT_EINVAL
+    assert lib.iht_forward_batched(None, c(0), c(0), c(0), 0, 0, 1, c(0), c(0), c(0)) == _lib.IHT_EINVAL
+    assert lib.iht_threshold_batched(c(0), c(0), c(16), 4, c(16), 1.0, 8, 100, 0, 2, c(16), c(16), 4, c(16),
+                                     c(16), 1 << 20, c(0)) == _lib.IHT_EINVAL          # ldo < s
+    assert lib.iht_threshold_batched_ws_bytes(1000, 4, 3) == 3 * lib.iht_threshold_batched_ws_bytes(1000, 4, 1)
+    assert lib.iht_merge_candidates(c(16), c(16), c(16), 20000, 2, 5000, 1, c(16), c(16), c(16), c(0)) == \
+        _lib.IHT_EUNSUPPORTED                                                          # P s > 8192
+    q = _lib.IhtQmat(rows=256, cols=64, planes=1, bits=2, strip_bytes=64, codes=16)
+    assert lib.iht_adjoint_batched(ctypes.byref(q), c(16), 3, c(16), c(16), 1 << 20, c(0)) == \
+        _lib.IHT_EUNSUPPORTED                                                          # 2B not a multiple of 16
