@@ -73,5 +73,9 @@ def test_host_side_validation_without_gpu(lib):
     assert lib.iht_merge_candidates(c(16), c(16), c(16), 20000, 2, 5000, 1, c(16), c(16), c(16), c(0)) == \
         _lib.IHT_EUNSUPPORTED                                                          # P s > 8192
     q = _lib.IhtQmat(rows=256, cols=64, planes=1, bits=2, strip_bytes=64, codes=16)
-    assert lib.iht_adjoint_batched(ctypes.byref(q), c(16), 3, c(16), c(16), 1 << 20, c(0)) == \
-        _lib.IHT_EUNSUPPORTED                                                          # 2B not a multiple of 16
+    assert lib.iht_adjoint_batched(ctypes.byref(q), c(16), 3, c(16), c(16), 0, c(0)) == \
+        _lib.IHT_EINVAL                                                                # workspace too small
+    assert lib.iht_adjoint_batched_ws_bytes(ctypes.byref(q), 3) == lib.iht_adjoint_batched_ws_bytes(ctypes.byref(q), 8)
+    big = _lib.IhtQmat(rows=1 << 20, cols=64, planes=2, bits=8, strip_bytes=2 * (1 << 20), codes=16)
+    assert lib.iht_adjoint_batched(ctypes.byref(big), c(16), 8, c(16), c(16), 1 << 40, c(0)) == \
+        _lib.IHT_EUNSUPPORTED                                                          # int32 accumulator bound
