@@ -30,7 +30,8 @@ namespace iht {
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
 constexpr int kAStages = 3;            // A (expanded codes) stages in TMEM
 constexpr int kBStages = 4;            // B (r limbs) stages in shared memory
-constexpr int kPkSlots = 8;            // packed-code staging slots
+constexpr int kPkSlots = 4;            // packed-code staging slots
+constexpr int kKG = 2;                 // K-blocks per packed-code slot (one 2*TS KiB copy per column tile)
 constexpr int kBThreads = 352;         // 11 warps (roles above)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -98,7 +99,8 @@ struct BatchArgs {
   int ntiles;              // ceil(N / 128)
   int B;                   // MMA snapshots (padded to a multiple of 8; 2B <= 128)
   int Breal;               // snapshots actually written (<= B)
-  int probe;               // 0; profiling probes (IHT_BATCHED_PROBE): 1 no B copies, 2 no MMAs, 4 no TMEM stores
+  int probe;               // 0; profiling probes (IHT_BATCHED_PROBE): 1 no B copies, 2 no MMAs, 4 no TMEM
+                           // stores, 8 no packed codes (converters only hand A stages over)
   int L;
   float sigma;
   const uint8_t* bimg;     // [nkb][KBB*2B] pre-swizzled limb image
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   constexpr int KBB = KBR;               // u8 bytes per row per K-block
   constexpr int CH = KBB / 16;           // 16-byte chunks per row
   constexpr int NKS = KBB / 32;          // MMAs (K = 32) per K-block
-  constexpr int PK = 8 * TS * 1024;      // packed bytes per K-block (8 column tiles x TS KiB)
+  constexpr int PK = 8 * kKG * TS * 1024;  // packed bytes per slot (8 column tiles x kKG K-blocks x TS KiB)
   constexpr int ACOLS = KBB / 4;         // TMEM columns of one A stage (4 u8 per column)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -183,11 +185,21 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     bool a_wrapped = false;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
-        mbar_wait2(smem_u32(&pk_full[ps]), pph);
+        const int kg = kb % kKG;                  // K-block inside the current slot
+        const bool slot_end = kg == kKG - 1 || kb == a.nkb - 1;
+        if (a.probe & 8) {                        // probe: hand the A stage over untouched
+          if (a_wrapped) mbar_wait2(smem_u32(&a_free[ss]), sph ^ 1u);
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive2(smem_u32(&a_full[ss]));
+          if (++ss == kAStages) { ss = 0; sph ^= 1u; a_wrapped = true; }
+          continue;
+        }
+        if (kg == 0) mbar_wait2(smem_u32(&pk_full[ps]), pph);
         uint32_t out[ACOLS];              // this pixel row's KBB u8 bytes, 4 per TMEM column
 #pragma unroll
         for (int ts = 0; ts < TS; ++ts) {
-          const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;   // 64 packed bytes
+          const uint8_t* src = sP + ps * PK + ct * (kKG * TS * 1024) + (kg * TS + ts) * 1024 + cc * 64;
           const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
                                reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
           const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
@@ -217,7 +229,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));   // packed slot consumed (registers hold it)
+        if (slot_end && lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));   // slot consumed (registers hold it)
         if (a_wrapped) mbar_wait2(smem_u32(&a_free[ss]), sph ^ 1u);
         // A stage ss lives in TMEM columns a_col0 + ss * ACOLS .. ; lane = pixel row n
         const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive2(smem_u32(&a_full[ss]));
-        if (++ps == kPkSlots) { ps = 0; pph ^= 1u; }
+        if (slot_end && ++ps == kPkSlots) { ps = 0; pph ^= 1u; }
         if (++ss == kAStages) { ss = 0; sph ^= 1u; a_wrapped = true; }
       }
     }
@@ -288,24 +300,27 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- packed-code producer
-    if (lane == 0) {
-      int ps = 0;
-      uint32_t ph = 0;
-      bool wrapped = false;
-      const int64_t last_tile = (a.N + 15) / 16 - 1;
-      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-        for (int kb = 0; kb < a.nkb; ++kb) {
-          if (wrapped) mbar_wait2(smem_u32(&pk_free[ps]), ph ^ 1u);
-          mbar_expect_tx2(smem_u32(&pk_full[ps]), PK);
-          for (int ct = 0; ct < 8; ++ct) {
-            int64_t col_tile = (int64_t)tile * 8 + ct;                // 16-column tile index
-            if (col_tile > last_tile) col_tile = last_tile;            // past N: any valid data
-            bulk_g2s2(smem_u32(sP + ps * PK + ct * (TS * 1024)),
-                      a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb * TS * 1024, TS * 1024,
-                      smem_u32(&pk_full[ps]));
-          }
-          if (++ps == kPkSlots) { ps = 0; ph ^= 1u; wrapped = true; }
+    // lanes 0-7 each copy one column tile's kKG consecutive K-blocks (contiguous in the
+    // tiled layout) so the 8 requests of a slot are issued in parallel
+    int ps = 0;
+    uint32_t ph = 0;
+    bool wrapped = false;
+    const int64_t last_tile = (a.N + 15) / 16 - 1;
+    for (int tile = (a.probe & 8) ? a.ntiles : blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      for (int kb0 = 0; kb0 < a.nkb; kb0 += kKG) {
+        const int kgn = a.nkb - kb0 < kKG ? a.nkb - kb0 : kKG;
+        const uint32_t bytes = (uint32_t)(kgn * TS * 1024);
+        if (wrapped) mbar_wait2(smem_u32(&pk_free[ps]), ph ^ 1u);
+        if (lane == 0) mbar_expect_tx2(smem_u32(&pk_full[ps]), 8 * bytes);
+        __syncwarp();
+        if (lane < 8) {
+          int64_t col_tile = (int64_t)tile * 8 + lane;                // 16-column tile index
+          if (col_tile > last_tile) col_tile = last_tile;              // past N: any valid data
+          bulk_g2s2(smem_u32(sP + ps * PK + lane * (kKG * TS * 1024)),
+                    a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb0 * TS * 1024, bytes,
+                    smem_u32(&pk_full[ps]));
         }
+        if (++ps == kPkSlots) { ps = 0; ph ^= 1u; wrapped = true; }
       }
     }
   } else if (warp == 6) {
@@ -368,19 +383,26 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
 }
 
 // Per-snapshot block fixed point of R (one CTA per snapshot): F_b from max |r|, two
-// balanced signed limbs written into the pre-swizzled image, exact limb sums S_b.
+// balanced signed limbs written into the pre-swizzled image, exact limb sums S_b.  A
+// thread owns 16 consecutive rows (one 16-byte K chunk of the image): it reads them as
+// four float4, permutes them into MMA K order in registers and writes two 16-byte stores.
 template <int BITS>
-__global__ void batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nreal, int nkb,
-                                     uint8_t* __restrict__ bimg, int* __restrict__ Fb, int* __restrict__ Sb) {
+__global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nreal,
+                                                            int nkb, uint8_t* __restrict__ bimg, int* __restrict__ Fb,
+                                                            int* __restrict__ Sb) {
   constexpr int KBR = (BITS == 8 ? 2 : 1) * 512 / BITS;
   const int b = blockIdx.x;                 // b >= nreal: zero padding snapshot (MMA N granularity)
-  const float* r = R + (int64_t)(b < nreal ? b : 0) * Rpad;
-  __shared__ float red[32];
-  __shared__ int ired[2][32];
+  const bool live = b < nreal;
+  const float* r = R + (int64_t)(live ? b : 0) * Rpad;
+  __shared__ float red[8];
+  __shared__ int ired[2][8];
   __shared__ int Fs;
   float m = 0.0f;
-  if (b < nreal)
-    for (int i = threadIdx.x; i < Rpad; i += blockDim.x) m = fmaxf(m, fabsf(r[i]));
+  if (live)
+    for (int i = threadIdx.x * 4; i < Rpad; i += blockDim.x * 4) {
+      const float4 v = *reinterpret_cast<const float4*>(r + i);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -396,22 +418,32 @@ __global__ void batched_limbs_kernel(const float* __restrict__ R, int Rpad, int 
   const float scale = ldexpf(1.0f, Fs);
   const int NB = 2 * B;
   int s0 = 0, s1 = 0;
-  for (int row = threadIdx.x; row < nkb * KBR; row += blockDim.x) {
-    const float rv = (row < Rpad && b < nreal) ? r[row] : 0.0f;
-    const int ri = __float2int_rn(rv * scale);
-    const int l0 = ((ri + 128) & 255) - 128;
-    const int l1 = (ri - l0) >> 8;
-    s0 += l0;
-    s1 += l1;
-    // K position of this row inside its K-block (inverse of perm_row per 16-row chunk)
-    const int kb = row / KBR, rr = row % KBR;
-    const int q = rr >> 4;
-    int p = 0;
-    for (int pp = 0; pp < 16; ++pp)
-      if (perm_row(pp, BITS) == (rr & 15)) p = pp;
+  for (int ch = threadIdx.x; ch < Rpad / 16; ch += blockDim.x) {
+    const int row0 = ch * 16;
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 f = live ? *reinterpret_cast<const float4*>(r + row0 + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * k] = f.x;
+      v[4 * k + 1] = f.y;
+      v[4 * k + 2] = f.z;
+      v[4 * k + 3] = f.w;
+    }
+    uint32_t w0[4] = {0u, 0u, 0u, 0u}, w1[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {          // byte p of the chunk <- row row0 + perm_row(p)
+      const int ri = __float2int_rn(v[perm_row(p, BITS)] * scale);
+      const int l0 = ((ri + 128) & 255) - 128;
+      const int l1 = (ri - l0) >> 8;
+      s0 += l0;
+      s1 += l1;
+      w0[p >> 2] |= (uint32_t)(l0 & 255) << (8 * (p & 3));
+      w1[p >> 2] |= (uint32_t)(l1 & 255) << (8 * (p & 3));
+    }
+    const int kb = row0 / KBR, q = (row0 % KBR) >> 4;
     uint8_t* blk = bimg + (int64_t)kb * NB * KBR;
-    blk[sw128_off(2 * b, q, NB) + p] = (uint8_t)(l0 & 255);
-    blk[sw128_off(2 * b + 1, q, NB) + p] = (uint8_t)(l1 & 255);
+    *reinterpret_cast<uint4*>(blk + sw128_off(2 * b, q, NB)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    *reinterpret_cast<uint4*>(blk + sw128_off(2 * b + 1, q, NB)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
   }
   for (int o = 16; o > 0; o >>= 1) {
     s0 += __shfl_xor_sync(0xffffffffu, s0, o);
@@ -437,7 +469,7 @@ static int kb_rows(int bits) { return (bits == 8 ? 2 : 1) * 512 / bits; }
 
 static size_t batched_smem(int bits, int B) {
   const int KBB = kb_rows(bits), TS = bits == 8 ? 2 : 1;
-  return 1024 + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * TS * 1024 +
+  return 1024 + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * kKG * TS * 1024 +
          (size_t)(2 * kPkSlots + 2 * kAStages + 2 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
 }
 
