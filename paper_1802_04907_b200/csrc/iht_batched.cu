@@ -28,7 +28,8 @@
 namespace iht {
 
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
-constexpr int kAStages = 3;            // A (expanded codes) stages in TMEM
+constexpr int kAStagesMax = 8;         // A (expanded codes) stages in TMEM: all 256 columns left by
+                                       // the two accumulators (4 at 2 bits, 8 at 4/8 bits)
 constexpr int kBStages = 4;            // B (r limbs) stages in shared memory
 constexpr int kPkSlots = 4;            // packed-code staging slots
 constexpr int kKG = 2;                 // K-blocks per packed-code slot (one 2*TS KiB copy per column tile)
@@ -100,7 +101,8 @@ struct BatchArgs {
   int B;                   // MMA snapshots (padded to a multiple of 8; 2B <= 128)
   int Breal;               // snapshots actually written (<= B)
   int probe;               // 0; profiling probes (IHT_BATCHED_PROBE): 1 no B copies, 2 no MMAs, 4 no TMEM
-                           // stores, 8 no packed codes (converters only hand A stages over)
+                           // stores, 8 no packed codes (converters only hand A stages over), 16 no
+                           // epilogue loads/stores
   int L;
   float sigma;
   const uint8_t* bimg;     // [nkb][KBB*2B] pre-swizzled limb image
@@ -118,6 +120,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   constexpr int NKS = KBB / 32;          // MMAs (K = 32) per K-block
   constexpr int PK = 8 * kKG * TS * 1024;  // packed bytes per slot (8 column tiles x kKG K-blocks x TS KiB)
   constexpr int ACOLS = KBB / 4;         // TMEM columns of one A stage (4 u8 per column)
+  constexpr int kAStages = 256 / ACOLS;  // A stages in the 256 TMEM columns after the accumulators
+  static_assert(kAStages <= kAStagesMax, "A stages");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NB = 2 * a.B;                 // MMA N (snapshot-limb columns), multiple of 16
@@ -128,8 +132,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   uint64_t* pk_full = bar;                        // [kPkSlots]  tx
   uint64_t* pk_free = pk_full + kPkSlots;         // [kPkSlots]  4 converter warps
   uint64_t* a_full = pk_free + kPkSlots;          // [kAStages]  4 converter warps
-  uint64_t* a_free = a_full + kAStages;           // [kAStages]  tcgen05.commit
-  uint64_t* b_full = a_free + kAStages;           // [kBStages]  tx
+  uint64_t* a_free = a_full + kAStagesMax;        // [kAStages]  tcgen05.commit
+  uint64_t* b_full = a_free + kAStagesMax;        // [kBStages]  tx
   uint64_t* b_free = b_full + kBStages;           // [kBStages]  tcgen05.commit
   uint64_t* acc_full = b_free + kBStages;         // [2]         tcgen05.commit
   uint64_t* acc_free = acc_full + 2;        // [2]         4 epilogue warps
@@ -325,21 +329,23 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     }
   } else if (warp == 6) {
     // ---------------------------------------------------------------- r-limb (B) producer
-    if (lane == 0) {
-      int bs = 0;
-      uint32_t ph = 0;
-      bool wrapped = false;
-      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-        for (int kb = 0; kb < a.nkb; ++kb) {
-          if (wrapped) mbar_wait2(smem_u32(&b_free[bs]), ph ^ 1u);
+    // the whole warp waits (no divergent spin), lane 0 issues
+    int bs = 0;
+    uint32_t ph = 0;
+    bool wrapped = false;
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        if (wrapped) mbar_wait2(smem_u32(&b_free[bs]), ph ^ 1u);
+        if (lane == 0) {
           if ((a.probe & 1) && wrapped) {
             mbar_arrive2(smem_u32(&b_full[bs]));                 // probe: reuse the stale stage
           } else {
             mbar_expect_tx2(smem_u32(&b_full[bs]), (uint32_t)BSZ);
             bulk_g2s2(smem_u32(sB + bs * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&b_full[bs]));
           }
-          if (++bs == kBStages) { bs = 0; ph ^= 1u; wrapped = true; }
         }
+        __syncwarp();
+        if (++bs == kBStages) { bs = 0; ph ^= 1u; wrapped = true; }
       }
     }
   } else {
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t n = (int64_t)tile * kBT + quarter * 32 + lane;
       const uint32_t taddr = tmem + ab * acc_stride + ((uint32_t)(quarter * 32) << 16);
-      for (int c0 = 0; c0 < NB; c0 += 16) {
+      for (int c0 = 0; c0 < ((a.probe & 16) ? 0 : NB); c0 += 16) {   // probe 16: no epilogue work
         uint32_t v[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -470,7 +476,7 @@ static int kb_rows(int bits) { return (bits == 8 ? 2 : 1) * 512 / bits; }
 static size_t batched_smem(int bits, int B) {
   const int KBB = kb_rows(bits), TS = bits == 8 ? 2 : 1;
   return 1024 + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * kKG * TS * 1024 +
-         (size_t)(2 * kPkSlots + 2 * kAStages + 2 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
+         (size_t)(2 * kPkSlots + 2 * kAStagesMax + 2 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
 }
 
 }  // namespace iht

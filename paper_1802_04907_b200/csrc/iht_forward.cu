@@ -6,63 +6,75 @@
 // strips each support column is a contiguous run of R codes, so the scale-and-add
 // streams s * R * b / 8 bytes (0.4% of the adjoint's bytes at config 4).
 //
-// Mapping: a CTA owns a window of 32 consecutive 32-bit code words of every strip
-// (32 * 32/b stacked rows); its 16 warps split the support in rounds of 16 columns
-// (loads issued before use), each lane accumulates the 32/b rows of its word, and the 8
-// partial sums are added in a fixed order through shared memory (deterministic).
+// Mapping: a CTA owns a window of 8 consecutive 32-bit code words of every strip
+// (8 * 32/b stacked rows); each warp load instruction covers 4 support columns x 8 words
+// (one 32-byte sector per column), 8 such loads in flight per lane; partial sums are
+// combined in a fixed order (shuffles, then shared memory), so r is deterministic.
 // Batched (config 5): grid row blockIdx.y = snapshot b, with its own x_b, y-hat_b, r_b.
 // Column shards: x holds GLOBAL indices; only [col_offset, col_offset + cols) are local.
 #include "iht_internal.cuh"
 
 namespace iht {
 
-constexpr int kFwdWarps = 16;
-constexpr int kFwdUnroll = 16;
+constexpr int kFwdThreads = 256;       // 8 warps
+constexpr int kFwdWords = 8;           // 32-bit code words (8 * 32/b rows) per CTA and plane chunk
+constexpr int kFwdUnroll = 8;          // support columns in flight per lane
+constexpr int kFwdStage = 1536;        // support entries staged in shared memory per round (18 KiB)
 
+// CTA = (chunk of 8 words of every strip, snapshot b).  Lane = (column slot c in 0..3,
+// word wl in 0..7): one load instruction of a warp reads 4 columns x one 32-byte sector.
+// The snapshot's support (idx, val) is staged in shared memory first, so the code loads
+// depend on a shared-memory read only.  Partial sums: shuffle over the 4 column slots,
+// then over the 8 warps through shared memory, both in a fixed order (deterministic).
 template <int B>
-__global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(
-    const uint8_t* __restrict__ codes, int64_t strip_bytes, int64_t words_total, int64_t rows,
-    int64_t rpad, int L, float sigma,
-    const int32_t* __restrict__ x_idx, const float* __restrict__ x_val,
+__global__ void __launch_bounds__(kFwdThreads) forward_kernel(
+    const uint8_t* __restrict__ codes, int64_t strip_bytes, int64_t words_total, int rows, int rpad, int L,
+    float sigma, const int32_t* __restrict__ x_idx, const float* __restrict__ x_val,
     const int32_t* __restrict__ x_nnz, int32_t max_nnz, int32_t ldx, int64_t col_offset, int64_t ncols,
     const float* __restrict__ yhat, float* __restrict__ r, int64_t vlen) {
   constexpr int CPW = 32 / B;
   constexpr uint32_t MASK = (1u << B) - 1u;
-  __shared__ float part[kFwdWarps][32][CPW + 1];
+  __shared__ float part[kFwdThreads / 32][kFwdWords][CPW];
+  __shared__ int64_t sidx[kFwdStage];   // tiled byte offset of each staged support column
+  __shared__ float sval[kFwdStage];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t word = (int64_t)blockIdx.x * 32 + lane;
-  const bool live = word < words_total;
-  {
-    const int b = blockIdx.y;
-    x_idx += (int64_t)b * ldx;
-    x_val += (int64_t)b * ldx;
-    x_nnz += b;
-    if (yhat) yhat += (int64_t)b * vlen;
-    r += (int64_t)b * vlen;
-  }
-  int nnz = *x_nnz;
+  const int c = lane >> 3, wl = lane & 7;
+  const int b = blockIdx.y;
+  x_idx += (int64_t)b * ldx;
+  x_val += (int64_t)b * ldx;
+  if (yhat) yhat += (int64_t)b * vlen;
+  r += (int64_t)b * vlen;
+  int nnz = x_nnz[b];
   nnz = nnz < 0 ? 0 : (nnz > max_nnz ? max_nnz : nnz);
-  const float negLm1 = -(float)(L - 1);
-
+  const int64_t word = (int64_t)blockIdx.x * kFwdWords + wl;
+  const bool live = word < words_total;
+  const int64_t kofs = (word >> 4) * 1024 + (word & 15) * 4;   // tiled offset of this word, sans column
   float acc[CPW];
 #pragma unroll
   for (int i = 0; i < CPW; ++i) acc[i] = 0.0f;
-
-  // kFwdUnroll support columns per round, their code words loaded before use
-  const int64_t kofs = (word >> 4) * 1024 + (word & 15) * 4;   // tiled offset of this word, sans column
-  for (int j0 = warp * kFwdUnroll; j0 < nnz; j0 += kFwdWarps * kFwdUnroll) {
+  const float negLm1 = -(float)(L - 1);
+  for (int st0 = 0; st0 < nnz; st0 += kFwdStage) {
+  const int nst = nnz - st0 < kFwdStage ? nnz - st0 : kFwdStage;
+  __syncthreads();
+  // stage the support: byte offset of each column's tile + slot (columns outside this
+  // shard get value 0 and column 0, adding +0 exactly)
+  for (int j = threadIdx.x; j < nst; j += kFwdThreads) {
+    int64_t col = (int64_t)x_idx[st0 + j] - col_offset;
+    const bool ok = col >= 0 && col < ncols;
+    col = ok ? col : 0;
+    sidx[j] = (col >> 4) * (16 * strip_bytes) + (col & 15) * 64;
+    sval[j] = ok ? x_val[st0 + j] : 0.0f;
+  }
+  __syncthreads();
+  for (int j0 = warp * 4 + c; j0 < nst; j0 += 32 * kFwdUnroll) {
     uint32_t w[kFwdUnroll];
     float xv[kFwdUnroll];
 #pragma unroll
     for (int u = 0; u < kFwdUnroll; ++u) {
-      const int j = j0 + u;
-      int64_t col = j < nnz ? (int64_t)__ldg(x_idx + j) - col_offset : 0;
-      const bool ok = j < nnz && col >= 0 && col < ncols;   // outside this column shard: skip
-      col = ok ? col : 0;
-      xv[u] = ok ? __ldg(x_val + j) : 0.0f;
-      w[u] = (ok && live) ? __ldg(reinterpret_cast<const uint32_t*>(
-                                codes + (col >> 4) * (16 * strip_bytes) + (col & 15) * 64 + kofs))
-                          : 0u;
+      const int j = j0 + 32 * u;
+      const bool ok = j < nst && live;
+      xv[u] = j < nst ? sval[j] : 0.0f;
+      w[u] = ok ? __ldg(reinterpret_cast<const uint32_t*>(codes + sidx[j] + kofs)) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < kFwdUnroll; ++u) {
@@ -71,24 +83,32 @@ __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(
         // code -> float exactly: 2^23 + code, minus 2^23; q = 2 code - (L-1) exactly
         const float cf = __int_as_float(0x4B000000u | ((w[u] >> (i * B)) & MASK)) - 8388608.0f;
         const float q = __fmaf_rn(2.0f, cf, negLm1);
-        acc[i] = __fmaf_rn(xv[u], q, acc[i]);   // xv = 0 for j >= nnz: adds +0, exact
+        acc[i] = __fmaf_rn(xv[u], q, acc[i]);   // xv = 0 past the support: adds +0, exact
       }
     }
   }
+  }
+  // fixed-order reduction over the 4 column slots (lanes wl, wl+8, wl+16, wl+24)
 #pragma unroll
-  for (int i = 0; i < CPW; ++i) part[warp][lane][i] = acc[i];
+  for (int i = 0; i < CPW; ++i) {
+    acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], 8));
+    acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], 16));
+  }
+  if (c == 0) {
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) part[warp][wl][i] = acc[i];
+  }
   __syncthreads();
-  // warp 0 combines the kFwdWarps partials in fixed order
-  if (warp == 0 && live) {
+  // one output row per thread, over the 8 warps in a fixed order; coalesced r writes
+  for (int t = threadIdx.x; t < kFwdWords * CPW; t += kFwdThreads) {
+    const int ww = t / CPW, i = t % CPW;
+    const int64_t m = ((int64_t)blockIdx.x * kFwdWords + ww) * CPW + i;   // stacked row p * rpad + local row
+    if (m >= (int64_t)words_total * CPW) continue;
+    float s = part[0][ww][i];
 #pragma unroll
-    for (int i = 0; i < CPW; ++i) {
-      float s = part[0][lane][i];
-#pragma unroll
-      for (int w2 = 1; w2 < kFwdWarps; ++w2) s = __fadd_rn(s, part[w2][lane][i]);
-      const int64_t m = word * CPW + i;   // stacked row p * rpad + local row
-      const float yv = yhat ? yhat[m] : 0.0f;      // NULL y-hat: partial product (column shards)
-      r[m] = (m % rpad) < rows ? __fsub_rn(yv, __fmul_rn(sigma, s)) : 0.0f;  // pad rows: 0
-    }
+    for (int w2 = 1; w2 < kFwdThreads / 32; ++w2) s = __fadd_rn(s, part[w2][ww][i]);
+    const float yv = yhat ? yhat[m] : 0.0f;      // NULL y-hat: partial product (column shards)
+    r[m] = (int)(m % rpad) < rows ? __fsub_rn(yv, __fmul_rn(sigma, s)) : 0.0f;  // pad rows: 0
   }
 }
 
@@ -125,14 +145,15 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
   const int L = num_levels(F->bits, F->level_mode);
   const float sigma = F->scale_c / (float)(L - 1);
   const int64_t words_total = F->strip_bytes / 4;
-  const unsigned blocks = (unsigned)ceil_div<int64_t>(words_total, 32);
+  const unsigned blocks = (unsigned)ceil_div<int64_t>(words_total, kFwdWords);
   const int64_t vlen = iht_vec_len(F->rows, F->planes);
+  if (F->rows > 0x7FFFFFFF) return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* codes = static_cast<const uint8_t*>(F->codes);
 #define IHT_FWD(BB)                                                                             \
-  forward_kernel<BB><<<dim3(blocks, nrhs), kFwdWarps * 32, 0, st>>>(                           \
-      codes, F->strip_bytes, words_total, F->rows, iht_rows_pad(F->rows), L, sigma, x_idx, x_val, x_nnz, \
-      max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen)
+  forward_kernel<BB><<<dim3(blocks, nrhs), kFwdThreads, 0, st>>>(                            \
+      codes, F->strip_bytes, words_total, (int)F->rows, (int)iht_rows_pad(F->rows), L, sigma, x_idx, x_val, \
+      x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen)
   if (F->bits == 2) IHT_FWD(2);
   else if (F->bits == 4) IHT_FWD(4);
   else IHT_FWD(8);

@@ -22,7 +22,19 @@
 // Batched (config 5): grid row blockIdx.y (T3: blockIdx.x) = snapshot b, each with its own
 // x_b, g_b, workspace slice and output; a column shard adds col_offset to every index.
 // iht_merge_candidates (T4, 1 CTA per snapshot) merges the shards' local top-s lists.
+//
+// Fused path (default when N <= kClusterMaxN): ONE launch, a thread-block cluster of CL
+// CTAs per snapshot.  Each CTA holds its slice of a = x + mu g in shared memory; the three
+// radix passes build local histograms that every CTA sums over the cluster through
+// distributed shared memory (DSMEM), so all CTAs agree on the threshold key T; the ordered
+// compaction takes per-CTA (greater, equal) counts, an exclusive scan over the cluster
+// gives each CTA its output offset and its share of the lowest-index ties.  No global
+// atomics, no workspace memset, no candidate-capacity limit.
+#include <cooperative_groups.h>
+
 #include "iht_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace iht {
 
@@ -31,15 +43,16 @@ constexpr int kThrWarps = kThrThreads / 32;
 
 // Block-wide: given hist[0..nbins), find the largest bin d with sum_{b>=d} hist[b] >= target.
 // Writes d, and the count strictly above d, into *d_out, *above_out.  target >= 1.
+template <int NT = kThrThreads>
 __device__ void find_bin(const int* hist, int nbins, int target, int* d_out, int* above_out,
-                         int* scratch /* kThrWarps ints */) {
+                         int* scratch /* NT / 32 ints */) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bpt = (nbins + kThrThreads - 1) / kThrThreads;
+  const int bpt = (nbins + NT - 1) / NT;
   // thread rt = kThrThreads-1-tid owns bins [tid*bpt, ...): scan order = descending bins
   int local = 0;
   for (int b = tid * bpt; b < min(nbins, (tid + 1) * bpt); ++b) local += hist[b];
   // inclusive suffix scan over tid (higher tid = higher bins first): reverse-index prefix
-  const int rt = kThrThreads - 1 - tid;
+  const int rt = NT - 1 - tid;
   const int rlane = rt & 31, rwarp = rt >> 5;
   // warp-level inclusive scan along rlane: lanes of warp `warp` map to rwarp = 31 - warp
   int v = local;
@@ -383,6 +396,279 @@ __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
   }
 }
 
+// ---------------------------------------------------------------------------- fused (cluster)
+constexpr int kClThreads = 512;               // threads per CTA of the fused kernel
+constexpr int kClWarps = kClThreads / 32;
+constexpr int kClusterSlice = 32768;          // a-values per CTA held in shared memory (128 KiB)
+constexpr int kClusterMax = 8;                // portable cluster size
+constexpr int64_t kClusterMaxN = (int64_t)kClusterSlice * kClusterMax;
+constexpr int kWarpCand = 256;                // candidate slots per warp (per CTA: 4096)
+
+// Passes `pass0`.. of the radix select over the cluster-wide list (n local entries val(i),
+// global index gidx(i), in increasing index order within and across CTAs), then the
+// ordered compaction into out_*.  `prefix`/`target`: state after the passes before pass0.
+template <class Val, class Gidx>
+__device__ void cluster_select(cg::cluster_group& cluster, int n, Val val, Gidx gidx, int pass0, unsigned int prefix,
+                               int target, bool all, int* hist, int* tot, int* scratch, int* wgt, int* weq,
+                               int* wtake, int* wbase, int* sh, int* cnt, int32_t* __restrict__ out_idx,
+                               float* __restrict__ out_val, int32_t* __restrict__ out_nnz) {
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned int T = 0;
+  int need = 0;
+  if (!all) {
+    const int shifts[3] = {20, 9, 0};
+    const int widths[3] = {11, 11, 9};
+    for (int pass = pass0; pass < 3; ++pass) {
+      const int nb = 1 << widths[pass];
+      for (int q = tid; q < nb; q += kClThreads) hist[q] = 0;
+      __syncthreads();
+      const int sh_ = shifts[pass];
+      const unsigned int hi_shift = sh_ + widths[pass];
+      for (int i = tid; i < n; i += kClThreads) {
+        const unsigned int key = __float_as_uint(val(i)) & 0x7FFFFFFFu;
+        if (hi_shift >= 31 || (key >> hi_shift) == (prefix >> hi_shift)) atomicAdd(&hist[(key >> sh_) & (nb - 1)], 1);
+      }
+      cluster.sync();                               // every CTA's histogram complete
+      for (int q = tid; q < nb; q += kClThreads) {
+        int acc = 0;
+        for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(hist, p)[q];
+        tot[q] = acc;
+      }
+      cluster.sync();                               // remote reads done before hist is reused
+      find_bin<kClThreads>(tot, nb, target, &sh[0], &sh[1], scratch);
+      prefix |= (unsigned int)sh[0] << sh_;
+      target -= sh[1];
+      __syncthreads();
+    }
+    T = prefix;
+    need = target;
+  }
+  // ordered compaction: per-warp contiguous ranges, per-CTA counts, exclusive scan over the cluster
+  const int span = ((n + kClWarps - 1) / kClWarps + 31) / 32 * 32;
+  const int wlo = warp * span, whi = min(n, wlo + span);
+  int gt = 0, eq = 0;
+  for (int i0 = wlo; i0 < whi; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned int key = i < whi ? (__float_as_uint(val(i)) & 0x7FFFFFFFu) : 0u;
+    const bool live = i < whi && key > 0u;
+    gt += __popc(__ballot_sync(0xffffffffu, live && (all || key > T)));
+    eq += __popc(__ballot_sync(0xffffffffu, live && !all && key == T));
+  }
+  if (lane == 0) {
+    wgt[warp] = gt;
+    weq[warp] = eq;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int g_ = 0, e_ = 0;
+    for (int w = 0; w < kClWarps; ++w) {
+      g_ += wgt[w];
+      e_ += weq[w];
+    }
+    cnt[0] = g_;
+    cnt[1] = e_;
+  }
+  cluster.sync();
+  if (tid == 0) {
+    int eq_before = 0, base = 0, total = 0, mytake = 0;
+    for (int p = 0; p < CL; ++p) {                  // CTAs hold increasing index ranges
+      const int* rc = cluster.map_shared_rank(cnt, p);
+      const int tk = (all || T == 0u) ? 0 : max(0, min(rc[1], need - eq_before));
+      eq_before += rc[1];
+      if (p < rank) base += rc[0] + tk;
+      if (p == rank) mytake = tk;
+      total += rc[0] + tk;
+    }
+    if (rank == 0) *out_nnz = total;
+    int take_left = mytake, wb = base;              // lowest-index ties first: warps in order
+    for (int w = 0; w < kClWarps; ++w) {
+      const int tk = min(weq[w], take_left);
+      take_left -= tk;
+      wtake[w] = tk;
+      wbase[w] = wb;
+      wb += wgt[w] + tk;
+    }
+  }
+  __syncthreads();
+  int run_sel = 0, run_eq = 0;
+  const unsigned int lt = (1u << lane) - 1u;
+  const int take = wtake[warp], base = wbase[warp];
+  for (int i0 = wlo; i0 < whi; i0 += 32) {
+    const int i = i0 + lane;
+    const float av = i < whi ? val(i) : 0.0f;
+    const unsigned int key = __float_as_uint(av) & 0x7FFFFFFFu;
+    const bool live = i < whi && key > 0u;
+    const bool is_gt = live && (all || key > T);
+    const bool is_eq = live && !all && key == T;
+    const unsigned int beq = __ballot_sync(0xffffffffu, is_eq);
+    const bool tk = is_eq && (run_eq + __popc(beq & lt)) < take;
+    const bool sel = is_gt || tk;
+    const unsigned int bsel = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
+      const int pos = base + run_sel + __popc(bsel & lt);
+      out_idx[pos] = (int32_t)gidx(i);
+      out_val[pos] = av;
+    }
+    run_sel += __popc(bsel);
+    run_eq += __popc(beq);
+  }
+}
+
+// One launch per selection: cluster of CL CTAs per snapshot (blockIdx.y), CTA rank r owns
+// a-values [r slice, (r+1) slice) in shared memory.  Full passes over the slice: (1) a =
+// mu g, (2) + x, NaN check and the 11-bit histogram, (3) extraction of the candidates
+// (digit >= the bin of the s-th largest key) into per-warp lists; the last two radix
+// passes and the ordered compaction then run on the candidates only.  If a warp's list
+// overflows (ties, mostly-zero a) the cluster falls back to the passes over the slice.
+__global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
+    const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, int s, int64_t N, int64_t col_offset,
+    int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo,
+    int32_t* __restrict__ out_nnz) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float* as = reinterpret_cast<float*>(dsm);                                  // [slice]
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm + (size_t)slice * 4);        // [kClWarps][kWarpCand]
+  float* cval = reinterpret_cast<float*>(cidx + kClWarps * kWarpCand);        // [kClWarps][kWarpCand]
+  __shared__ int hist[2048];
+  __shared__ int tot[2048];
+  __shared__ int scratch[kClWarps];
+  __shared__ int wgt[kClWarps], weq[kClWarps], wtake[kClWarps], wbase[kClWarps];
+  __shared__ int sh[4];
+  __shared__ int cnt[4];          // [0] gt, [1] eq, [2] nan | poisoned, [3] list overflow  (read by the cluster)
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.y;
+  x_idx += (int64_t)b * ldx;
+  x_val += (int64_t)b * ldx;
+  g += (int64_t)b * N;
+  out_idx += (int64_t)b * ldo;
+  out_val += (int64_t)b * ldo;
+  const int64_t lo = (int64_t)rank * slice;
+  const int n = (int)min64(max64(N - lo, 0), slice);           // this CTA's slice [lo, lo + n)
+  // ---- (1) a = mu g on the slice; float4 loads when aligned
+  for (int q = tid; q < 2048; q += kClThreads) hist[q] = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 15) == 0);
+  if (vec) {
+    const int n4 = n >> 2;
+    for (int i = tid; i < n4; i += kClThreads) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(g + lo) + i);
+      reinterpret_cast<float4*>(as)[i] = make_float4(__fmul_rn(mu, v.x), __fmul_rn(mu, v.y), __fmul_rn(mu, v.z),
+                                                     __fmul_rn(mu, v.w));
+    }
+    for (int i = (n4 << 2) + tid; i < n; i += kClThreads) as[i] = __fmul_rn(mu, g[lo + i]);
+  } else {
+    for (int i = tid; i < n; i += kClThreads) as[i] = __fmul_rn(mu, g[lo + i]);
+  }
+  int nnz = x_nnz[b];
+  const int poisoned = nnz < 0;
+  nnz = nnz < 0 ? 0 : min(nnz, max_nnz);
+  __syncthreads();
+  for (int j = tid; j < nnz; j += kClThreads) {
+    const int64_t c = (int64_t)x_idx[j] - col_offset - lo;
+    if (c >= 0 && c < n) as[c] = __fadd_rn(x_val[j], as[c]);
+  }
+  __syncthreads();
+  // ---- (2) NaN check + histogram of the top 11 key bits
+  int nan = 0;
+  for (int i = tid; i < n; i += kClThreads) {
+    const unsigned int key = __float_as_uint(as[i]) & 0x7FFFFFFFu;
+    nan |= key > 0x7F800000u;
+    atomicAdd(&hist[key >> 20], 1);
+  }
+  nan = __syncthreads_or(nan);
+  if (tid == 0) cnt[2] = nan | poisoned;
+  cluster.sync();
+  int bad = 0;
+  for (int p = 0; p < CL; ++p) bad |= cluster.map_shared_rank(cnt, p)[2];
+  for (int q = tid; q < 2048; q += kClThreads) {
+    int acc = 0;
+    for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(hist, p)[q];
+    tot[q] = acc;
+  }
+  cluster.sync();                                   // remote reads of hist / cnt done
+  if (bad || s == 0) {
+    if (rank == 0 && tid == 0) out_nnz[b] = bad ? -1 : 0;
+    cluster.sync();
+    return;
+  }
+  const bool all = (int64_t)s >= N;
+  unsigned int d1 = 0;
+  int target = s;
+  if (!all) {
+    find_bin<kClThreads>(tot, 2048, s, &sh[0], &sh[1], scratch);
+    d1 = (unsigned int)sh[0];
+    target = s - sh[1];
+  }
+  // ---- (3) candidates: key > 0 and digit >= d1, per-warp ordered lists (contiguous ranges)
+  const int span = ((n + kClWarps - 1) / kClWarps + 31) / 32 * 32;
+  const int wlo = warp * span, whi = min(n, wlo + span);
+  int wc = 0;
+  const unsigned int lt = (1u << lane) - 1u;
+  int32_t* my_idx = cidx + warp * kWarpCand;
+  float* my_val = cval + warp * kWarpCand;
+  for (int i0 = wlo; i0 < whi; i0 += 32) {
+    const int i = i0 + lane;
+    const float av = i < whi ? as[i] : 0.0f;
+    const unsigned int key = __float_as_uint(av) & 0x7FFFFFFFu;
+    const bool sel = i < whi && key > 0u && (key >> 20) >= d1;
+    const unsigned int bs = __ballot_sync(0xffffffffu, sel);
+    const int pos = wc + __popc(bs & lt);
+    if (sel && pos < kWarpCand) {
+      my_idx[pos] = (int32_t)(col_offset + lo + i);
+      my_val[pos] = av;
+    }
+    wc += __popc(bs);
+  }
+  if (lane == 0) wgt[warp] = wc;
+  const int ovf = __syncthreads_or(wc > kWarpCand);
+  if (tid == 0) {
+    cnt[3] = ovf;
+    int acc = 0;
+    for (int w = 0; w < kClWarps; ++w) {                 // pack the warp lists (in order) in place
+      wbase[w] = acc;
+      acc += min(wgt[w], kWarpCand);
+    }
+    sh[2] = acc;
+  }
+  cluster.sync();
+  int any_ovf = 0;
+  for (int p = 0; p < CL; ++p) any_ovf |= cluster.map_shared_rank(cnt, p)[3];
+  cluster.sync();                                   // cnt may be rewritten below
+  if (!any_ovf) {
+    // compact the lists: warp w moves its entries to wbase[w] (<= its own slot start)
+    const int nc = sh[2];
+    static_assert(kWarpCand <= kClThreads, "one entry per thread per warp list");
+    for (int w = 1; w < kClWarps; ++w) {             // warp 0's list is already in place
+      const int c0 = min(wgt[w], kWarpCand), dst = wbase[w];
+      int32_t ii = 0;
+      float vv = 0.0f;
+      if (tid < c0) {
+        ii = cidx[w * kWarpCand + tid];
+        vv = cval[w * kWarpCand + tid];
+      }
+      __syncthreads();                                // reads before the (lower, overlapping) writes
+      if (tid < c0) {
+        cidx[dst + tid] = ii;
+        cval[dst + tid] = vv;
+      }
+      __syncthreads();
+    }
+    cluster_select(cluster, nc, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, 1,
+                   all ? 0u : (d1 << 20), target, all, hist, tot, scratch, wgt, weq, wtake, wbase, sh, cnt, out_idx,
+                   out_val, out_nnz + b);
+  } else {
+    const int64_t base_idx = col_offset + lo;
+    cluster_select(cluster, n, [&](int i) { return as[i]; }, [&](int i) { return base_idx + i; }, 1,
+                   all ? 0u : (d1 << 20), target, all, hist, tot, scratch, wgt, weq, wtake, wbase, sh, cnt, out_idx,
+                   out_val, out_nnz + b);
+  }
+  cluster.sync();                                   // keep shared memory alive for remote readers
+}
+
 // T4: merge of the shards' local top-s lists (column-sharded batched path): the global
 // top-s is contained in the union of the local top-s (same tie rule), and the shards'
 // lists concatenated in shard order are in increasing global index order.
@@ -448,6 +734,8 @@ static int thr_attrs() {
   if (!g_thr_attr) {
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
+    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kClusterSlice * 4 + kClWarps * kWarpCand * 8));
     g_thr_attr = true;
   }
   return IHT_OK;
@@ -467,12 +755,34 @@ extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, c
   int rc;
   if ((rc = thr_attrs()) != IHT_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  // max_nnz: the caller's x arrays hold at most min(ldx, s) entries (x is an H_s output)
+  const int32_t max_nnz = ldx < s ? ldx : s;
+  if (N <= kClusterMaxN && nrhs <= 65535) {
+    int CL = 1;
+    while ((int64_t)CL * kClusterSlice < N) CL *= 2;
+    // spread small problems too: up to ~2 CTAs per SM while slices stay >= 4096 a-values
+    while (CL < kClusterMax && (int64_t)CL * 2 * nrhs <= 148 && N / (2 * CL) >= 4096) CL *= 2;
+    const int slice = (int)((N + CL - 1) / CL);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(CL, nrhs);
+    lc.blockDim = dim3(kClThreads);
+    lc.dynamicSmemBytes = (size_t)slice * 4 + (size_t)kClWarps * kWarpCand * 8;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, s, N,
+                                      col_offset, slice, out_idx, out_val, ldo, out_nnz));
+    return IHT_OK;
+  }
   ThrWs w{};
   thr_ws_layout(N, nrhs, static_cast<char*>(ws), &w);
   IHT_CUDA_CHECK(cudaMemsetAsync(ws, 0, nrhs * thr_hdr_bytes(), st));
   const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
-  // max_nnz: the caller's x arrays hold at most min(ldx, s) entries (x is an H_s output)
-  const int32_t max_nnz = ldx < s ? ldx : s;
   thr_update_hist<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, N,
                                                               col_offset, w);
   IHT_LAUNCH_CHECK();

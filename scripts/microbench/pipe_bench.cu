@@ -1,0 +1,116 @@
+// Which part of the batched adjoint's warp-specialised pipeline costs MMA throughput?
+// MODE 1: one thread issues 8 MMAs per "K-block" and commits to a_free[stage] (4 stages),
+//         nobody waits (pure issue rate).
+// MODE 2: + 4 "converter" warps: wait a_free[stage] (K-block i-4), arrive a_full[stage];
+//         the MMA warp waits a_full before each K-block (the kernel's A handoff).
+// MODE 3: MODE 2 + 6 extra warps spinning on an mbarrier that completes at the end.
+// MODE 4: MODE 2 but the MMA warp's 32 lanes all wait (kernel style) vs lane 0 only.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void mbar_init(uint32_t m, uint32_t c) { asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(m), "r"(c)); }
+__device__ __forceinline__ void mbar_arrive(uint32_t m) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(m) : "memory"); }
+__device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t ph) {
+  asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(m), "r"(ph) : "memory");
+}
+constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr int ST = 4;
+
+template <int MODE>
+__global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t a_full[ST], a_free[ST], done;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ST; ++i) { mbar_init(su32(&a_full[i]), 4); mbar_init(su32(&a_free[i]), 1); }
+    mbar_init(su32(&done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  if (warp < 4 && MODE >= 2) {
+    int s = 0; uint32_t ph = 0; bool wr = false;
+    for (int kb = 0; kb < nkb; ++kb) {
+      if (wr) mbar_wait(su32(&a_free[s]), ph ^ 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(su32(&a_full[s]));
+      if (++s == ST) { s = 0; ph ^= 1u; wr = true; }
+    }
+  } else if (warp == 4) {
+    const long long t0 = clock64();
+    int s = 0; uint32_t ph = 0;
+    const uint32_t bbase = su32(smem);
+    for (int kb = 0; kb < nkb; ++kb) {
+      if (MODE >= 2) {
+        if (MODE == 4 || lane == 0) mbar_wait(su32(&a_full[s]), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
+          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                       "r"(tmem + 256 + (uint32_t)(s * 64 + kk * 8)), "l"(bd), "r"(IDESC), "r"(acc) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&a_free[s])) : "memory");
+      }
+      __syncwarp();
+      if (++s == ST) { s = 0; ph ^= 1u; }
+    }
+    if (lane == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&done)) : "memory");
+      mbar_wait(su32(&done), 0);
+      cyc[blockIdx.x] = clock64() - t0;
+    }
+    __syncwarp();
+  } else if (MODE == 3 && warp >= 5) {
+    mbar_wait(su32(&done), 0);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+template <int MODE>
+void run(const char* name, int sms) {
+  const int nkb = 2048;
+  long long* d;
+  cudaMalloc(&d, sms * sizeof(long long));
+  auto k = pipe<MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  k<<<sms, 352, 80 * 1024>>>(nkb, d);
+  cudaError_t err = cudaDeviceSynchronize();
+  long long h[256];
+  cudaMemcpy(h, d, sms * sizeof(long long), cudaMemcpyDeviceToHost);
+  double mean = 0;
+  for (int i = 0; i < sms; ++i) mean += h[i];
+  mean /= sms;
+  printf("%-60s %s  %.1f clk/MMA\n", name, cudaGetErrorString(err), mean / (nkb * 8.0));
+  cudaFree(d);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<1>("1: issue + commit per K-block, no waits", sms);
+  run<2>("2: + converter handoff (a_full/a_free, 4 stages), lane-0 wait", sms);
+  run<3>("3: + 6 spinning warps", sms);
+  run<4>("4: handoff, all 32 MMA-warp lanes wait", sms);
+  return 0;
+}

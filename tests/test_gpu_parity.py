@@ -180,7 +180,8 @@ def _a32(x_idx, x_val, g, mu):
 
 
 @pytest.mark.parametrize("N,s", [(1024, 16), (16384, 128), (262144, 1024), (1001, 37), (5, 3), (1, 1),
-                                 (100, 100), (100, 150), (3000, 0)])
+                                 (100, 100), (100, 150), (3000, 0), (131073, 64), (262145, 1024),   # fused cluster
+                                 (300000, 100), (300000, 7000)])                                   # multi-kernel
 def test_threshold_exact_selection(N, s):
     """Selection on identical fp32 a is exact: GPU H_s = oracle H_s of the same a."""
     rng = np.random.default_rng(N + s)
