@@ -281,6 +281,17 @@ typedef struct {
                            batched path is COLUMN-sharded (pool[k].col_offset = rank N/P):
                            forward partials all-reduced (sum), local H_s candidates
                            all-gathered and merged                         */
+  int32_t step_mode;    /* 0: fixed step mu (reading c9, the north star's hot path);
+                           1: Algorithm 1's adaptive step:
+                           Gamma^[1] = supp(H_s(Phi-hat_1^H y-hat)); per iteration
+                           mu = |g_G|^2 / |Phi-hat_A[:, G] g_G|^2 (reading c10), proposal
+                           H_s(x + mu g); if its support differs from G, accept only when
+                           mu <= (1 - c) |dx|^2 / |Phi-hat_A dx|^2, else mu /= k (1 - c)
+                           and propose again (reading c11).  `mu` is the fallback step for
+                           a vanishing denominator.  Not with a column-sharded batch.   */
+  float step_c;         /* c of the acceptance test (0 < c < 1; SPEC default 1e-3)       */
+  float step_k;         /* k of the shrink mu / (k (1 - c)), k > 1 / (1 - c) (default 2) */
+  int32_t max_shrink;   /* bound on proposals per iteration; the last is kept    */
 } iht_config;
 
 /* Stateful solver over a pool of K quantised copies pool[0..K) (all with the
@@ -322,7 +333,11 @@ IHT_API int iht_solver_buffers(iht_solver* solver, const float** yhat_dev, const
  * run, from the CUDA event pairs recorded on the run's stream around each adjoint
  * (inside the graph).  Synchronises on the last event. */
 IHT_API int iht_solver_adjoint_times(iht_solver* solver, float* ms_host);
-/* Number of kernel launches one iht_solver_run enqueues (for gpu_launches). */
+/* Adaptive step (cfg.step_mode = 1): the accepted mu and the number of shrinks of every
+ * iteration of the LAST run, [n_iter][B] each (host arrays).  Synchronises the stream. */
+IHT_API int iht_solver_steps(iht_solver* solver, float* mu_host, int32_t* shrinks_host, void* stream);
+/* Number of kernel launches one iht_solver_run enqueues (for gpu_launches); with the
+ * adaptive step it counts one pass of the shrink loop per iteration. */
 IHT_API int64_t iht_solver_launches_per_run(const iht_solver* solver);
 
 /* One-shot convenience: create, run, destroy. */

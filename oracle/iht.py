@@ -169,6 +169,112 @@ def qniht_batched(phi, Y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, reco
                   pool=pool, snapshot=b) for b in range(Y.shape[1])]
 
 
+def adaptive_step(g, A, gamma):
+    """Eq. step_size / Algorithm 1 line 4: mu = (g_G^T g_G) /
+    (g_G^T A_G^H A_G g_G) on the support G, with A the quantised copy that produced g
+    (reading c10).  Returns None for a zero denominator (degenerate step)."""
+    gamma = np.asarray(gamma, dtype=np.int64)
+    gg = np.asarray(g, dtype=np.float64)[gamma]
+    num = float(gg @ gg)
+    Ag = A[:, gamma] @ gg
+    den = float(np.real(np.vdot(Ag, Ag)))
+    if den == 0.0:
+        return None
+    return num / den
+
+
+@dataclass
+class AdaptiveRecord:
+    n: int
+    mu: float
+    shrinks: int
+    support_changed: bool
+    x_idx: np.ndarray
+    x_val: np.ndarray
+    accept_margin: float = np.inf   # min |mu - (1-c) b| / mu over the acceptance tests (parity rule)
+    select_margin: float = np.inf   # |a|_(s) - |a|_(s+1) of the accepted proposal, relative to |a|_(s)
+
+
+def qniht_adaptive(phi, y, s, n_iter, b_phi, b_y, seed, K, c=1e-3, k=2.0, level_mode=0, max_shrink=60,
+                   mu_fallback=1.0, pool=None, snapshot=0, quantized=True):
+    """Algorithm 1 "QNIHT" with the adaptive step and the acceptance / shrink
+    loop, in the paper's order:
+
+      Gamma^[1] = supp(H_s(Phi-hat_1^H y-hat))
+      for n = 1..n*:
+        g   = Re(Phi-hat_{2n-1}^H (y-hat - Phi-hat_{2n} x))               (P:349)
+        mu  = |g_G|^2 / |Phi-hat_{2n-1}[:, G] g_G|^2, G = Gamma^[n]      (reading c10)
+        x'  = H_s(x + mu g), Gamma' = supp(x')                            (P:351-352)
+        if Gamma' != Gamma^[n]:                                           (reading c11)
+          b = |x' - x|^2 / |Phi-hat_{2n-1}(x' - x)|^2
+          while mu > (1 - c) b:  mu <- mu / (k (1 - c));  x' = H_s(x + mu g);  b from the new x'
+        x^[n+1] = x', Gamma^[n+1] = supp(x')
+    Reading c11: the garbled "x^[n+1] = x^[n]" branches are read as ACCEPT (support unchanged,
+    or mu <= (1-c) b), REJECT-and-shrink otherwise.  A zero step denominator falls back to
+    mu_fallback.  quantized=False runs the same loop on Phi and y themselves (NIHT).
+    Returns (x_idx, x_val, records)."""
+    if quantized:
+        c_phi = Q.scale_c(phi)
+        c_y = Q.scale_c(y)
+        y_codes, _ = Q.quantize_vector(y, b_y, level_mode, seed, c=c_y, snapshot=snapshot)
+        y_hat = Q.dequantize(y_codes, c_y, b_y, level_mode)
+        if pool is None:
+            pool = CopyPool(phi, b_phi, level_mode, seed, c_phi, cache=max(2, min(K, 4)))
+        mat = pool.dequantized
+    else:
+        cplx = np.iscomplexobj(phi)
+        full = np.asarray(phi, dtype=np.complex128 if cplx else np.float64)
+        y_hat = np.asarray(y, dtype=full.dtype)
+        mat = lambda _k: full   # noqa: E731
+    N = phi.shape[1]
+    x_idx, x_val = np.zeros(0, dtype=np.int64), np.zeros(0)
+    A1 = mat(0)
+    gamma, _ = hard_threshold(adjoint(A1, y_hat), s)                  # Gamma^[1] (P:347)
+    recs = []
+    for n in range(1, n_iter + 1):
+        A = mat((2 * n - 2) % K)
+        F = mat((2 * n - 1) % K)
+        g = adjoint(A, forward(F, x_idx, x_val, y_hat))
+        mu = adaptive_step(g, A, gamma) if len(gamma) else None
+        if mu is None:
+            mu = mu_fallback
+        xd = np.zeros(N)
+        xd[x_idx] = x_val
+
+        def propose(m):
+            return hard_threshold(xd + m * g, s)
+
+        ni, nv = propose(mu)
+        shrinks = 0
+        acc_margin = np.inf
+        changed = ni.tolist() != list(gamma)
+        if changed:
+            while True:
+                dx = np.zeros(N)
+                dx[ni] = nv
+                dx = dx - xd
+                sup = np.flatnonzero(dx)
+                num = float(dx[sup] @ dx[sup])
+                Adx = A[:, sup] @ dx[sup]
+                den = float(np.real(np.vdot(Adx, Adx)))
+                if num > 0.0 and den > 0.0:
+                    acc_margin = min(acc_margin, abs(mu - (1.0 - c) * (num / den)) / mu)
+                if num == 0.0 or den == 0.0 or mu <= (1.0 - c) * (num / den):
+                    break
+                if shrinks >= max_shrink:
+                    raise RuntimeError("shrink loop did not terminate")
+                mu = mu / (k * (1.0 - c))
+                shrinks += 1
+                ni, nv = propose(mu)
+        x_idx, x_val = ni, nv
+        gamma = x_idx
+        a = xd + mu * g
+        mag = np.sort(np.abs(a))[::-1]
+        sel = (mag[s - 1] - mag[s]) / max(mag[s - 1], 1e-300) if 0 < s < N else np.inf
+        recs.append(AdaptiveRecord(n, mu, shrinks, changed, x_idx, x_val, acc_margin, sel))
+    return x_idx, x_val, recs
+
+
 def niht_fixed_full_precision(phi, y, s, n_iter, mu):
     """Full-precision IHT with fixed step (Eq. iht_update_rule); exists
     only for the oracle's own pins (b = infinity, no Q)."""

@@ -49,10 +49,12 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   const int64_t word = (int64_t)blockIdx.x * kFwdWords + wl;
   const bool live = word < words_total;
   const int64_t kofs = (word >> 4) * 1024 + (word & 15) * 4;   // tiled offset of this word, sans column
+  // acc_i = sum_j x_j code_ij and xs = sum_j x_j; the affine map q = 2 code - (L-1) is
+  // applied once at the end: sum_j x_j q_ij = 2 acc_i - (L-1) xs
   float acc[CPW];
 #pragma unroll
   for (int i = 0; i < CPW; ++i) acc[i] = 0.0f;
-  const float negLm1 = -(float)(L - 1);
+  float xs = 0.0f;
   for (int st0 = 0; st0 < nnz; st0 += kFwdStage) {
   const int nst = nnz - st0 < kFwdStage ? nnz - st0 : kFwdStage;
   __syncthreads();
@@ -66,7 +68,8 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     sval[j] = ok ? x_val[st0 + j] : 0.0f;
   }
   __syncthreads();
-  for (int j0 = warp * 4 + c; j0 < nst; j0 += 32 * kFwdUnroll) {
+  for (int jb = warp * 4; jb < nst; jb += 32 * kFwdUnroll) {   // warp-uniform trip count
+    const int j0 = jb + c;
     uint32_t w[kFwdUnroll];
     float xv[kFwdUnroll];
 #pragma unroll
@@ -78,19 +81,22 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     }
 #pragma unroll
     for (int u = 0; u < kFwdUnroll; ++u) {
+      if (!__any_sync(0xffffffffu, j0 + 32 * u < nst)) break;     // warp-uniform: skip empty slots
+      xs = __fadd_rn(xs, xv[u]);
 #pragma unroll
       for (int i = 0; i < CPW; ++i) {
-        // code -> float exactly: 2^23 + code, minus 2^23; q = 2 code - (L-1) exactly
+        // code -> float exactly: 2^23 + code, minus 2^23
         const float cf = __int_as_float(0x4B000000u | ((w[u] >> (i * B)) & MASK)) - 8388608.0f;
-        const float q = __fmaf_rn(2.0f, cf, negLm1);
-        acc[i] = __fmaf_rn(xv[u], q, acc[i]);   // xv = 0 past the support: adds +0, exact
+        acc[i] = __fmaf_rn(xv[u], cf, acc[i]);   // xv = 0 past the support: adds +0, exact
       }
     }
   }
   }
-  // fixed-order reduction over the 4 column slots (lanes wl, wl+8, wl+16, wl+24)
+  // q-sum of each row (affine map), then the fixed-order reduction over the 4 column slots
+  const float xl = __fmul_rn((float)(L - 1), xs);
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
+    acc[i] = __fsub_rn(__fmul_rn(2.0f, acc[i]), xl);
     acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], 8));
     acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], 16));
   }

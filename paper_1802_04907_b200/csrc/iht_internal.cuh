@@ -18,6 +18,15 @@
 
 void iht_set_last_cuda_error(cudaError_t e, const char* expr, const char* file, int line);
 
+// iht_threshold_batched with the step read per snapshot from device memory (mu_dev[b]) when
+// mu_dev is not NULL (adaptive step, Algorithm 1); internal to the library.
+int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                             const float* g, float mu, const float* mu_dev, int32_t s, int64_t N, int64_t col_offset,
+                             int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws,
+                             int64_t ws_bytes, void* stream);
+// Kernel launches one iht_threshold_batched call makes for N columns (fused cluster path: 1).
+int iht_threshold_launches(int64_t N);
+
 namespace iht {
 
 constexpr int kNumSMs = 148;  // B200; launch code queries the device, this is a default

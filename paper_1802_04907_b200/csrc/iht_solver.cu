@@ -12,6 +12,7 @@
 #include <mutex>
 #include <vector>
 
+#include "iht_adaptive.cuh"
 #include "iht_internal.cuh"
 
 // ------------------------------------------------------------------ errors
@@ -159,6 +160,15 @@ struct iht_solver {
   int32_t* xs_idx = nullptr;   // [nslots][B][s]
   float* xs_val = nullptr;     // [nslots][B][s]
   int32_t* xs_nnz = nullptr;   // [nslots][B]
+  // adaptive step (step_mode 1): per snapshot mu, loop state (accepted, shrinks), norms,
+  // Gamma^[1], the support-restricted gradient, the difference x' - x and a scratch vector
+  float *ad_mu = nullptr, *ad_num = nullptr, *ad_den = nullptr, *ad_dnum = nullptr, *ad_dden = nullptr;
+  int32_t *ad_state = nullptr, *ad_pending = nullptr;
+  int32_t *ad_gi = nullptr, *ad_gn = nullptr, *ad_xgi = nullptr, *ad_xgn = nullptr, *ad_di = nullptr, *ad_dn = nullptr;
+  float *ad_gv = nullptr, *ad_xgv = nullptr, *ad_dv = nullptr, *ad_tmp = nullptr;
+  float* ad_mu_rec = nullptr;      // [n_iter][B]
+  int32_t* ad_shr_rec = nullptr;   // [n_iter][B]
+  cudaStream_t body_stream = nullptr;
   int32_t* cand_send = nullptr;   // column shards: idx [B][s] | val [B][s] | nnz [B]
   int32_t* cand_recv = nullptr;   // [P][same]
   int64_t cand_words = 0;
@@ -178,6 +188,100 @@ static cudaError_t record_event(cudaEvent_t e, cudaStream_t st) {
   if (err != cudaSuccess) return err;
   return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
                                              : cudaEventRecord(e, st);
+}
+
+static int64_t& pass_dummy() {
+  static thread_local int64_t d = 0;
+  return d;
+}
+
+// One pass of the shrink loop (propose, compare supports, |Phi-hat_A dx|^2, decide).
+static int enqueue_shrink_body(iht_solver* S, cudaStream_t st, int n, const iht_qmat& A, const int32_t* gi,
+                               const int32_t* gn, const int32_t* xi, const float* xv, const int32_t* xn, int32_t* oi,
+                               float* ov, int32_t* on, cudaGraphConditionalHandle h, int use_h, int64_t* L) {
+  int rc;
+  const int B = S->B, s = S->cfg.s;
+  if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g, S->cfg.mu, S->ad_mu, s, S->N, 0, B, oi, ov, s, on,
+                                     S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+    return rc;
+  if ((rc = ad_delta(oi, ov, on, gi, gn, s, xi, xv, xn, s, S->ad_state, S->ad_di, S->ad_dv, S->ad_dn, S->ad_dnum, B,
+                     st)) != IHT_OK)
+    return rc;
+  if ((rc = iht_forward_batched(&A, S->ad_di, S->ad_dv, S->ad_dn, 2 * s, 2 * s, B, nullptr, S->ad_tmp, st)) !=
+      IHT_OK)
+    return rc;
+  if ((rc = ad_norm(S->ad_tmp, S->vlen, S->ad_dden, B, st)) != IHT_OK) return rc;
+  if (S->rowshard) {
+    if ((rc = iht_comm_allreduce(S->cfg.comm, S->ad_dden, B, 0, st)) != IHT_OK) return rc;
+  }
+  if ((rc = ad_decide(S->ad_dnum, S->ad_dden, S->cfg.step_c, S->cfg.step_k, S->cfg.max_shrink, B, S->ad_mu,
+                      S->ad_state, S->ad_mu_rec + (int64_t)(n - 1) * B, S->ad_shr_rec + (int64_t)(n - 1) * B, h, use_h,
+                      S->ad_pending, st)) != IHT_OK)
+    return rc;
+  *L += iht_threshold_launches(S->N) + 4;   // threshold + delta + forward + norm + decide
+  return IHT_OK;
+}
+
+// Algorithm 1's step for iteration n: Gamma, mu, then the proposal / shrink
+// loop (a conditional WHILE node when captured into the graph, else a host loop).
+static int enqueue_adaptive(iht_solver* S, cudaStream_t st, int n, const iht_qmat& A, const int32_t* xi,
+                            const float* xv, const int32_t* xn, int32_t* oi, float* ov, int32_t* on, int64_t* L) {
+  int rc;
+  const int B = S->B, s = S->cfg.s;
+  const int32_t *gi = xi, *gn = xn;
+  if (n == 1) {   // Gamma^[1] = supp(H_s(Phi-hat_1^H y-hat)): x^[1] = 0, so H_s(g^[1])
+    if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, 1.0f, s, S->N, 0, B, S->ad_gi, S->ad_gv, s, S->ad_gn,
+                                    S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+      return rc;
+    gi = S->ad_gi;
+    gn = S->ad_gn;
+    *L += iht_threshold_launches(S->N);
+  }
+  if ((rc = ad_gather(S->g, S->N, 0, gi, gn, s, S->ad_xgi, S->ad_xgv, S->ad_xgn, S->ad_num, B, st)) != IHT_OK) return rc;
+  if ((rc = iht_forward_batched(&A, S->ad_xgi, S->ad_xgv, S->ad_xgn, s, s, B, nullptr, S->ad_tmp, st)) != IHT_OK)
+    return rc;
+  if ((rc = ad_norm(S->ad_tmp, S->vlen, S->ad_den, B, st)) != IHT_OK) return rc;
+  if (S->rowshard) {
+    if ((rc = iht_comm_allreduce(S->cfg.comm, S->ad_den, B, 0, st)) != IHT_OK) return rc;
+  }
+  if ((rc = ad_step(S->ad_num, S->ad_den, S->cfg.mu, B, S->ad_mu, S->ad_state, st)) != IHT_OK) return rc;
+  *L += 4;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  IHT_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive) {
+    cudaGraph_t graph;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    IHT_CUDA_CHECK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &graph, &deps, &ndeps));
+    cudaGraphConditionalHandle h;
+    IHT_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    IHT_CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, ndeps, &p));
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    IHT_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    IHT_CUDA_CHECK(cudaStreamBeginCaptureToGraph(S->body_stream, body, nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeRelaxed));
+    rc = enqueue_shrink_body(S, S->body_stream, n, A, gi, gn, xi, xv, xn, oi, ov, on, h, 1, L);
+    cudaGraph_t tmp;
+    const cudaError_t e = cudaStreamEndCapture(S->body_stream, &tmp);
+    if (rc != IHT_OK) return rc;
+    IHT_CUDA_CHECK(e);
+  } else {
+    int32_t pending = 1;
+    for (int pass = 0; pending; ++pass) {
+      if ((rc = enqueue_shrink_body(S, st, n, A, gi, gn, xi, xv, xn, oi, ov, on, 0, 0, pass == 0 ? L : &pass_dummy()))
+          != IHT_OK)
+        return rc;
+      IHT_CUDA_CHECK(cudaMemcpyAsync(&pending, S->ad_pending, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      IHT_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+  }
+  return IHT_OK;
 }
 
 // Enqueue one complete run (absmax .. last threshold) on stream st; counts launches.
@@ -233,11 +337,13 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       if ((rc = iht_comm_allreduce(S->cfg.comm, S->g, S->N, 0, st)) != IHT_OK) return rc;
     }
     // (a6) update + H_s
-    if (!S->colshard) {
+    if (S->cfg.step_mode == 1) {
+      if ((rc = enqueue_adaptive(S, st, n, A, xi, xv, xn, oi, ov, on, &L)) != IHT_OK) return rc;
+    } else if (!S->colshard) {
       if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
-      L += 3;
+      L += iht_threshold_launches(S->N);
     } else {
       int32_t* ci = S->cand_send;
       float* cv = reinterpret_cast<float*>(S->cand_send + xslot);
@@ -245,7 +351,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, q0.col_offset, B, ci, cv, s, cn,
                                       S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
-      L += 3;
+      L += iht_threshold_launches(S->N);
       if ((rc = iht_comm_allgather(S->cfg.comm, S->cand_send, S->cand_recv, S->cand_words * 4, st)) != IHT_OK)
         return rc;
       if ((rc = iht_merge_candidates(S->cand_recv, reinterpret_cast<const float*>(S->cand_recv + xslot),
@@ -285,6 +391,13 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
   const int64_t Ng = batched ? q0.cols * world : q0.cols;          // global columns
   if (cfg->s > Mg * q0.planes || cfg->s > Ng) return IHT_EINVAL;   // s <= M
   if (batched && cfg->comm && (int64_t)world * cfg->s > 8192) return IHT_EUNSUPPORTED;
+  if (cfg->step_mode != 0 && cfg->step_mode != 1) return IHT_EINVAL;
+  if (cfg->step_mode == 1) {
+    if (batched && cfg->comm) return IHT_EUNSUPPORTED;            // column-sharded adaptive: not built
+    if (!(cfg->step_c > 0.0f && cfg->step_c < 1.0f) || !(cfg->step_k * (1.0f - cfg->step_c) > 1.0f) ||
+        cfg->max_shrink < 0 || !(cfg->mu > 0.0f))
+      return IHT_EINVAL;                                             // k > 1/(1-c)
+  }
   iht_solver* S = new iht_solver();
   S->pool.assign(pool, pool + K);
   S->cfg = *cfg;
@@ -298,6 +411,9 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
   S->rank = cfg->comm ? cfg->comm->rank : 0;
   S->rowshard = !batched && world > 1;
   S->colshard = batched && cfg->comm != nullptr;   // any world size (world 1 exercises the same path)
+  // NCCL kernels may not sit inside a conditional body graph: the adaptive row-sharded
+  // run drives its shrink loop from the host
+  if (cfg->step_mode == 1 && S->rowshard) S->cfg.use_graph = 0;
   S->ws_adj_bytes = batched ? iht_adjoint_batched_ws_bytes(&q0, B) : iht_adjoint_ws_bytes(&q0);
   S->ws_thr_bytes = iht_threshold_batched_ws_bytes(S->N, cfg->s, B);
   S->nslots = cfg->trace ? cfg->n_iter + 1 : 2;
@@ -311,8 +427,14 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
                 sz_xi = al((int64_t)S->nslots * B * s * 4), sz_xv = al((int64_t)S->nslots * B * s * 4),
                 sz_xn = al((int64_t)S->nslots * B * 4), sz_cs = al(S->cand_words * 4),
                 sz_cr = al(S->cand_words * 4 * world);
+  const bool ad = cfg->step_mode == 1;
+  const int64_t sz_b4 = al((int64_t)B * 4), sz_bs = al((int64_t)B * s * 4), sz_b2s = al((int64_t)B * 2 * s * 4),
+                sz_rec = al((int64_t)(cfg->n_iter > 0 ? cfg->n_iter : 1) * B * 4);
+  const int64_t sz_ad = ad ? (6 * sz_b4 + al((int64_t)B * 8) + 2 * sz_bs + sz_b4 + 2 * sz_bs + sz_b4 + 2 * sz_b2s +
+                              sz_b4 + sz_v + 2 * sz_rec)
+                           : 0;
   const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_xi + sz_xv + sz_xn +
-                        (S->colshard ? sz_cs + sz_cr : 0);
+                        (S->colshard ? sz_cs + sz_cr : 0) + sz_ad;
   if (cudaMalloc(&S->block, total) != cudaSuccess) {
     delete S;
     return IHT_ENOMEM;
@@ -332,9 +454,31 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
     S->cand_send = reinterpret_cast<int32_t*>(p); p += sz_cs;
     S->cand_recv = reinterpret_cast<int32_t*>(p); p += sz_cr;
   }
+  if (ad) {
+    S->ad_mu = reinterpret_cast<float*>(p); p += sz_b4;
+    S->ad_num = reinterpret_cast<float*>(p); p += sz_b4;
+    S->ad_den = reinterpret_cast<float*>(p); p += sz_b4;
+    S->ad_dnum = reinterpret_cast<float*>(p); p += sz_b4;
+    S->ad_dden = reinterpret_cast<float*>(p); p += sz_b4;
+    S->ad_pending = reinterpret_cast<int32_t*>(p); p += sz_b4;
+    S->ad_state = reinterpret_cast<int32_t*>(p); p += al((int64_t)B * 8);
+    S->ad_gi = reinterpret_cast<int32_t*>(p); p += sz_bs;
+    S->ad_gv = reinterpret_cast<float*>(p); p += sz_bs;
+    S->ad_gn = reinterpret_cast<int32_t*>(p); p += sz_b4;
+    S->ad_xgi = reinterpret_cast<int32_t*>(p); p += sz_bs;
+    S->ad_xgv = reinterpret_cast<float*>(p); p += sz_bs;
+    S->ad_xgn = reinterpret_cast<int32_t*>(p); p += sz_b4;
+    S->ad_di = reinterpret_cast<int32_t*>(p); p += sz_b2s;
+    S->ad_dv = reinterpret_cast<float*>(p); p += sz_b2s;
+    S->ad_dn = reinterpret_cast<int32_t*>(p); p += sz_b4;
+    S->ad_tmp = reinterpret_cast<float*>(p); p += sz_v;
+    S->ad_mu_rec = reinterpret_cast<float*>(p); p += sz_rec;
+    S->ad_shr_rec = reinterpret_cast<int32_t*>(p); p += sz_rec;
+  }
   // zero everything once (pad rows of the stacked vectors stay 0)
   if (cudaMemset(S->block, 0, total) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&S->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&S->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&S->body_stream, cudaStreamNonBlocking) != cudaSuccess) {
     cudaFree(S->block);
     delete S;
     return IHT_ECUDA;
@@ -365,6 +509,7 @@ extern "C" int iht_solver_destroy(iht_solver* S) {
     if (e) cudaEventDestroy(e);
   if (S->exec) cudaGraphExecDestroy(S->exec);
   if (S->cap_stream) cudaStreamDestroy(S->cap_stream);
+  if (S->body_stream) cudaStreamDestroy(S->body_stream);
   if (S->block) cudaFree(S->block);
   delete S;
   return IHT_OK;
@@ -451,6 +596,17 @@ extern "C" int iht_solver_buffers(iht_solver* S, const float** yhat, const float
 }
 
 extern "C" int64_t iht_solver_launches_per_run(const iht_solver* S) { return S ? S->launches : -1; }
+
+extern "C" int iht_solver_steps(iht_solver* S, float* mu_host, int32_t* shrinks_host, void* stream) {
+  if (S == nullptr || mu_host == nullptr || shrinks_host == nullptr || S->cfg.step_mode != 1) return IHT_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t n = (size_t)S->cfg.n_iter * S->B;
+  if (n == 0) return IHT_OK;
+  IHT_CUDA_CHECK(cudaMemcpyAsync(mu_host, S->ad_mu_rec, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  IHT_CUDA_CHECK(cudaMemcpyAsync(shrinks_host, S->ad_shr_rec, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  IHT_CUDA_CHECK(cudaStreamSynchronize(st));
+  return IHT_OK;
+}
 
 extern "C" int iht_solve(const iht_qmat* pool, int K, const iht_config* cfg, const float* y, int flags,
                          int32_t* out_idx, float* out_val, int32_t* out_nnz, void* stream) {

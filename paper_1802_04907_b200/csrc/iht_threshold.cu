@@ -228,10 +228,11 @@ __device__ __forceinline__ ThrWs thr_at(const ThrWs& w, int b) {
 // T1: a = x + mu g, global histogram of key >> 20
 __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
-    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, int64_t N, int64_t col_offset,
-    ThrWs w0) {
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev,
+    int64_t N, int64_t col_offset, ThrWs w0) {
   __shared__ float as[kTile];
   const int bq = blockIdx.y;
+  if (mu_dev) mu = mu_dev[bq];
   const ThrWs w = thr_at(w0, bq);
   x_idx += (int64_t)bq * ldx;
   x_val += (int64_t)bq * ldx;
@@ -404,13 +405,53 @@ constexpr int kClusterMax = 8;                // portable cluster size
 constexpr int64_t kClusterMaxN = (int64_t)kClusterSlice * kClusterMax;
 constexpr int kWarpCand = 256;                // candidate slots per warp (per CTA: 4096)
 
-// Passes `pass0`.. of the radix select over the cluster-wide list (n local entries val(i),
+// Cluster-shared state of one CTA (read by the other CTAs through DSMEM).  Every slot is
+// written once per launch, except the two histogram buffers, which alternate between
+// passes: a CTA rewrites buffer k only after the next cluster barrier, which every CTA
+// reaches after its remote reads of buffer k.  One barrier per histogram pass.
+struct ClShared {
+  int hist[2][2048];
+  int flags[2];        // [0] NaN or poisoned input, [1] a warp's candidate list overflowed
+  int counts[2];       // [0] keys > T, [1] keys == T (ordered compaction)
+};
+
+// Histogram pass over the local list (pass index `pass`, 11/11/9 bits) summed over the
+// cluster; find the bin of the target-th largest key.  Returns through sh[0], sh[1].
+template <class Val>
+__device__ void cluster_hist_pass(cg::cluster_group& cluster, ClShared& cs, int& buf, int n, Val val, int pass,
+                                  unsigned int prefix, int target, int* tot, int* scratch, int* sh) {
+  const int CL = (int)cluster.num_blocks();
+  const int tid = threadIdx.x;
+  const int shifts[3] = {20, 9, 0};
+  const int widths[3] = {11, 11, 9};
+  const int nb = 1 << widths[pass];
+  const int sh_ = shifts[pass];
+  const unsigned int hi_shift = sh_ + widths[pass];
+  int* hist = cs.hist[buf];
+  for (int q = tid; q < nb; q += kClThreads) hist[q] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += kClThreads) {
+    const unsigned int key = __float_as_uint(val(i)) & 0x7FFFFFFFu;
+    if ((key >> hi_shift) == (prefix >> hi_shift)) atomicAdd(&hist[(key >> sh_) & (nb - 1)], 1);
+  }
+  cluster.sync();
+  for (int q = tid; q < nb; q += kClThreads) {
+    int acc = 0;
+    for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(cs.hist[buf], p)[q];
+    tot[q] = acc;
+  }
+  __syncthreads();
+  find_bin<kClThreads>(tot, nb, target, &sh[0], &sh[1], scratch);
+  buf ^= 1;
+}
+
+// Passes 1, 2 of the radix select over the cluster-wide list (n local entries val(i),
 // global index gidx(i), in increasing index order within and across CTAs), then the
-// ordered compaction into out_*.  `prefix`/`target`: state after the passes before pass0.
+// ordered compaction into out_*.  `prefix`/`target`: state after pass 0.
 template <class Val, class Gidx>
-__device__ void cluster_select(cg::cluster_group& cluster, int n, Val val, Gidx gidx, int pass0, unsigned int prefix,
-                               int target, bool all, int* hist, int* tot, int* scratch, int* wgt, int* weq,
-                               int* wtake, int* wbase, int* sh, int* cnt, int32_t* __restrict__ out_idx,
+__device__ void cluster_select(cg::cluster_group& cluster, ClShared& cs, int& buf, int n, Val val, Gidx gidx,
+                               unsigned int prefix, int target, bool all, int* tot, int* scratch, int* wgt, int* weq,
+                               int* wtake, int* wbase, int* sh, int32_t* __restrict__ out_idx,
                                float* __restrict__ out_val, int32_t* __restrict__ out_nnz) {
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -418,27 +459,9 @@ __device__ void cluster_select(cg::cluster_group& cluster, int n, Val val, Gidx 
   unsigned int T = 0;
   int need = 0;
   if (!all) {
-    const int shifts[3] = {20, 9, 0};
-    const int widths[3] = {11, 11, 9};
-    for (int pass = pass0; pass < 3; ++pass) {
-      const int nb = 1 << widths[pass];
-      for (int q = tid; q < nb; q += kClThreads) hist[q] = 0;
-      __syncthreads();
-      const int sh_ = shifts[pass];
-      const unsigned int hi_shift = sh_ + widths[pass];
-      for (int i = tid; i < n; i += kClThreads) {
-        const unsigned int key = __float_as_uint(val(i)) & 0x7FFFFFFFu;
-        if (hi_shift >= 31 || (key >> hi_shift) == (prefix >> hi_shift)) atomicAdd(&hist[(key >> sh_) & (nb - 1)], 1);
-      }
-      cluster.sync();                               // every CTA's histogram complete
-      for (int q = tid; q < nb; q += kClThreads) {
-        int acc = 0;
-        for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(hist, p)[q];
-        tot[q] = acc;
-      }
-      cluster.sync();                               // remote reads done before hist is reused
-      find_bin<kClThreads>(tot, nb, target, &sh[0], &sh[1], scratch);
-      prefix |= (unsigned int)sh[0] << sh_;
+    for (int pass = 1; pass < 3; ++pass) {
+      cluster_hist_pass(cluster, cs, buf, n, val, pass, prefix, target, tot, scratch, sh);
+      prefix |= (unsigned int)sh[0] << (pass == 1 ? 9 : 0);
       target -= sh[1];
       __syncthreads();
     }
@@ -467,14 +490,14 @@ __device__ void cluster_select(cg::cluster_group& cluster, int n, Val val, Gidx 
       g_ += wgt[w];
       e_ += weq[w];
     }
-    cnt[0] = g_;
-    cnt[1] = e_;
+    cs.counts[0] = g_;
+    cs.counts[1] = e_;
   }
   cluster.sync();
   if (tid == 0) {
     int eq_before = 0, base = 0, total = 0, mytake = 0;
     for (int p = 0; p < CL; ++p) {                  // CTAs hold increasing index ranges
-      const int* rc = cluster.map_shared_rank(cnt, p);
+      const int* rc = cluster.map_shared_rank(cs.counts, p);
       const int tk = (all || T == 0u) ? 0 : max(0, min(rc[1], need - eq_before));
       eq_before += rc[1];
       if (p < rank) base += rc[0] + tk;
@@ -518,25 +541,26 @@ __device__ void cluster_select(cg::cluster_group& cluster, int n, Val val, Gidx 
 
 // One launch per selection: cluster of CL CTAs per snapshot (blockIdx.y), CTA rank r owns
 // a-values [r slice, (r+1) slice) in shared memory.  Full passes over the slice: (1) a =
-// mu g, (2) + x, NaN check and the 11-bit histogram, (3) extraction of the candidates
-// (digit >= the bin of the s-th largest key) into per-warp lists; the last two radix
-// passes and the ordered compaction then run on the candidates only.  If a warp's list
-// overflows (ties, mostly-zero a) the cluster falls back to the passes over the slice.
+// mu g with the 11-bit histogram of its keys (x's few entries are then added and their
+// histogram bins moved), (2) extraction of the candidates (digit >= the bin of the s-th
+// largest key) into per-warp ordered lists; the last two radix passes and the ordered
+// compaction run on the candidates only.  If a warp's list overflows (massive ties,
+// mostly-zero a) the cluster falls back to the passes over the whole slice.
 __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
-    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, int s, int64_t N, int64_t col_offset,
-    int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo,
-    int32_t* __restrict__ out_nnz) {
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
+    int64_t N, int64_t col_offset, int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
+    int32_t ldo, int32_t* __restrict__ out_nnz) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  float* as = reinterpret_cast<float*>(dsm);                                  // [slice]
+  float* as = reinterpret_cast<float*>(dsm);                                  // [slice] (multiple of 4)
+  if (mu_dev) mu = mu_dev[blockIdx.y];
   int32_t* cidx = reinterpret_cast<int32_t*>(dsm + (size_t)slice * 4);        // [kClWarps][kWarpCand]
   float* cval = reinterpret_cast<float*>(cidx + kClWarps * kWarpCand);        // [kClWarps][kWarpCand]
-  __shared__ int hist[2048];
+  __shared__ ClShared cs;
   __shared__ int tot[2048];
   __shared__ int scratch[kClWarps];
   __shared__ int wgt[kClWarps], weq[kClWarps], wtake[kClWarps], wbase[kClWarps];
   __shared__ int sh[4];
-  __shared__ int cnt[4];          // [0] gt, [1] eq, [2] nan | poisoned, [3] list overflow  (read by the cluster)
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -549,47 +573,74 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   out_val += (int64_t)b * ldo;
   const int64_t lo = (int64_t)rank * slice;
   const int n = (int)min64(max64(N - lo, 0), slice);           // this CTA's slice [lo, lo + n)
-  // ---- (1) a = mu g on the slice; float4 loads when aligned
+  int buf = 0;
+  int* hist = cs.hist[0];
   for (int q = tid; q < 2048; q += kClThreads) hist[q] = 0;
+  __syncthreads();
+  // ---- (1) a = mu g and the histogram of the top 11 key bits; float4 when aligned
+  int nan = 0;
   const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 15) == 0);
-  if (vec) {
-    const int n4 = n >> 2;
-    for (int i = tid; i < n4; i += kClThreads) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(g + lo) + i);
-      reinterpret_cast<float4*>(as)[i] = make_float4(__fmul_rn(mu, v.x), __fmul_rn(mu, v.y), __fmul_rn(mu, v.z),
-                                                     __fmul_rn(mu, v.w));
+  const int n4 = vec ? (n >> 2) : 0;
+  constexpr int kLd = 8;                 // float4 loads in flight per thread (g is read once)
+  for (int i0 = 0; i0 < n4; i0 += kClThreads * kLd) {
+    float4 v[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int i = i0 + u * kClThreads + tid;
+      v[u] = i < n4 ? __ldg(reinterpret_cast<const float4*>(g + lo) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int i = (n4 << 2) + tid; i < n; i += kClThreads) as[i] = __fmul_rn(mu, g[lo + i]);
-  } else {
-    for (int i = tid; i < n; i += kClThreads) as[i] = __fmul_rn(mu, g[lo + i]);
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int i = i0 + u * kClThreads + tid;
+      if (i >= n4) break;
+      const float4 a4 =
+          make_float4(__fmul_rn(mu, v[u].x), __fmul_rn(mu, v[u].y), __fmul_rn(mu, v[u].z), __fmul_rn(mu, v[u].w));
+      reinterpret_cast<float4*>(as)[i] = a4;
+      const unsigned int k0 = __float_as_uint(a4.x) & 0x7FFFFFFFu, k1 = __float_as_uint(a4.y) & 0x7FFFFFFFu,
+                         k2 = __float_as_uint(a4.z) & 0x7FFFFFFFu, k3 = __float_as_uint(a4.w) & 0x7FFFFFFFu;
+      nan |= (k0 > 0x7F800000u) | (k1 > 0x7F800000u) | (k2 > 0x7F800000u) | (k3 > 0x7F800000u);
+      atomicAdd(&hist[k0 >> 20], 1);
+      atomicAdd(&hist[k1 >> 20], 1);
+      atomicAdd(&hist[k2 >> 20], 1);
+      atomicAdd(&hist[k3 >> 20], 1);
+    }
+  }
+  for (int i = (n4 << 2) + tid; i < n; i += kClThreads) {
+    const float a1 = __fmul_rn(mu, g[lo + i]);
+    as[i] = a1;
+    const unsigned int k = __float_as_uint(a1) & 0x7FFFFFFFu;
+    nan |= k > 0x7F800000u;
+    atomicAdd(&hist[k >> 20], 1);
   }
   int nnz = x_nnz[b];
   const int poisoned = nnz < 0;
   nnz = nnz < 0 ? 0 : min(nnz, max_nnz);
   __syncthreads();
+  // x's entries (distinct indices, an H_s output): a_n = x_n + mu g_n, moving the bin
   for (int j = tid; j < nnz; j += kClThreads) {
     const int64_t c = (int64_t)x_idx[j] - col_offset - lo;
-    if (c >= 0 && c < n) as[c] = __fadd_rn(x_val[j], as[c]);
-  }
-  __syncthreads();
-  // ---- (2) NaN check + histogram of the top 11 key bits
-  int nan = 0;
-  for (int i = tid; i < n; i += kClThreads) {
-    const unsigned int key = __float_as_uint(as[i]) & 0x7FFFFFFFu;
-    nan |= key > 0x7F800000u;
-    atomicAdd(&hist[key >> 20], 1);
+    if (c >= 0 && c < n) {
+      const float old = as[c];
+      const float nw = __fadd_rn(x_val[j], old);
+      as[c] = nw;
+      const unsigned int ko = __float_as_uint(old) & 0x7FFFFFFFu, kn = __float_as_uint(nw) & 0x7FFFFFFFu;
+      nan |= kn > 0x7F800000u;
+      atomicSub(&hist[ko >> 20], 1);
+      atomicAdd(&hist[kn >> 20], 1);
+    }
   }
   nan = __syncthreads_or(nan);
-  if (tid == 0) cnt[2] = nan | poisoned;
+  if (tid == 0) cs.flags[0] = nan | poisoned;
   cluster.sync();
   int bad = 0;
-  for (int p = 0; p < CL; ++p) bad |= cluster.map_shared_rank(cnt, p)[2];
+  for (int p = 0; p < CL; ++p) bad |= cluster.map_shared_rank(cs.flags, p)[0];
   for (int q = tid; q < 2048; q += kClThreads) {
     int acc = 0;
-    for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(hist, p)[q];
+    for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(cs.hist[0], p)[q];
     tot[q] = acc;
   }
-  cluster.sync();                                   // remote reads of hist / cnt done
+  buf = 1;
+  __syncthreads();
   if (bad || s == 0) {
     if (rank == 0 && tid == 0) out_nnz[b] = bad ? -1 : 0;
     cluster.sync();
@@ -603,7 +654,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     d1 = (unsigned int)sh[0];
     target = s - sh[1];
   }
-  // ---- (3) candidates: key > 0 and digit >= d1, per-warp ordered lists (contiguous ranges)
+  // ---- (2) candidates: key > 0 and digit >= d1, per-warp ordered lists (contiguous ranges)
   const int span = ((n + kClWarps - 1) / kClWarps + 31) / 32 * 32;
   const int wlo = warp * span, whi = min(n, wlo + span);
   int wc = 0;
@@ -625,25 +676,16 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   }
   if (lane == 0) wgt[warp] = wc;
   const int ovf = __syncthreads_or(wc > kWarpCand);
-  if (tid == 0) {
-    cnt[3] = ovf;
-    int acc = 0;
-    for (int w = 0; w < kClWarps; ++w) {                 // pack the warp lists (in order) in place
-      wbase[w] = acc;
-      acc += min(wgt[w], kWarpCand);
-    }
-    sh[2] = acc;
-  }
+  if (tid == 0) cs.flags[1] = ovf;
   cluster.sync();
   int any_ovf = 0;
-  for (int p = 0; p < CL; ++p) any_ovf |= cluster.map_shared_rank(cnt, p)[3];
-  cluster.sync();                                   // cnt may be rewritten below
+  for (int p = 0; p < CL; ++p) any_ovf |= cluster.map_shared_rank(cs.flags, p)[1];
   if (!any_ovf) {
-    // compact the lists: warp w moves its entries to wbase[w] (<= its own slot start)
-    const int nc = sh[2];
+    // pack the warp lists in order: warp w's entries move down to the running offset
     static_assert(kWarpCand <= kClThreads, "one entry per thread per warp list");
-    for (int w = 1; w < kClWarps; ++w) {             // warp 0's list is already in place
-      const int c0 = min(wgt[w], kWarpCand), dst = wbase[w];
+    int nc = min(wgt[0], kWarpCand);
+    for (int w = 1; w < kClWarps; ++w) {
+      const int c0 = min(wgt[w], kWarpCand);
       int32_t ii = 0;
       float vv = 0.0f;
       if (tid < c0) {
@@ -652,19 +694,20 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
       }
       __syncthreads();                                // reads before the (lower, overlapping) writes
       if (tid < c0) {
-        cidx[dst + tid] = ii;
-        cval[dst + tid] = vv;
+        cidx[nc + tid] = ii;
+        cval[nc + tid] = vv;
       }
+      nc += c0;
       __syncthreads();
     }
-    cluster_select(cluster, nc, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, 1,
-                   all ? 0u : (d1 << 20), target, all, hist, tot, scratch, wgt, weq, wtake, wbase, sh, cnt, out_idx,
-                   out_val, out_nnz + b);
+    cluster_select(cluster, cs, buf, nc, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; },
+                   all ? 0u : (d1 << 20), target, all, tot, scratch, wgt, weq, wtake, wbase, sh, out_idx, out_val,
+                   out_nnz + b);
   } else {
     const int64_t base_idx = col_offset + lo;
-    cluster_select(cluster, n, [&](int i) { return as[i]; }, [&](int i) { return base_idx + i; }, 1,
-                   all ? 0u : (d1 << 20), target, all, hist, tot, scratch, wgt, weq, wtake, wbase, sh, cnt, out_idx,
-                   out_val, out_nnz + b);
+    cluster_select(cluster, cs, buf, n, [&](int i) { return as[i]; }, [&](int i) { return base_idx + i; },
+                   all ? 0u : (d1 << 20), target, all, tot, scratch, wgt, weq, wtake, wbase, sh, out_idx, out_val,
+                   out_nnz + b);
   }
   cluster.sync();                                   // keep shared memory alive for remote readers
 }
@@ -741,10 +784,10 @@ static int thr_attrs() {
   return IHT_OK;
 }
 
-extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
-                                     const float* g, float mu, int32_t s, int64_t N, int64_t col_offset,
-                                     int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo,
-                                     int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream) {
+int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                             const float* g, float mu, const float* mu_dev, int32_t s, int64_t N, int64_t col_offset,
+                             int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws,
+                             int64_t ws_bytes, void* stream) {
   if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr ||
       s < 0 || N <= 0 || N > 0x7FFFFFFFll || nrhs <= 0 || nrhs > 65535 || ldo < s || ldx < 0 ||
       col_offset < 0 || col_offset + N > 0x7FFFFFFFll)
@@ -762,7 +805,7 @@ extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, c
     while ((int64_t)CL * kClusterSlice < N) CL *= 2;
     // spread small problems too: up to ~2 CTAs per SM while slices stay >= 4096 a-values
     while (CL < kClusterMax && (int64_t)CL * 2 * nrhs <= 148 && N / (2 * CL) >= 4096) CL *= 2;
-    const int slice = (int)((N + CL - 1) / CL);
+    const int slice = (int)(((N + CL - 1) / CL + 31) / 32 * 32);   // 16-byte aligned slices
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(CL, nrhs);
     lc.blockDim = dim3(kClThreads);
@@ -775,16 +818,16 @@ extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, c
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, s, N,
-                                      col_offset, slice, out_idx, out_val, ldo, out_nnz));
+    IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
+                                      N, col_offset, slice, out_idx, out_val, ldo, out_nnz));
     return IHT_OK;
   }
   ThrWs w{};
   thr_ws_layout(N, nrhs, static_cast<char*>(ws), &w);
   IHT_CUDA_CHECK(cudaMemsetAsync(ws, 0, nrhs * thr_hdr_bytes(), st));
   const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
-  thr_update_hist<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, N,
-                                                              col_offset, w);
+  thr_update_hist<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev,
+                                                              N, col_offset, w);
   IHT_LAUNCH_CHECK();
   thr_candidates<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(s, N, col_offset, w);
   IHT_LAUNCH_CHECK();
@@ -792,6 +835,16 @@ extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, c
   IHT_LAUNCH_CHECK();
   return IHT_OK;
 }
+
+extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                                     const float* g, float mu, int32_t s, int64_t N, int64_t col_offset,
+                                     int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo,
+                                     int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream) {
+  return iht_threshold_batched_mu(x_idx, x_val, x_nnz, ldx, g, mu, nullptr, s, N, col_offset, nrhs, out_idx, out_val,
+                                  ldo, out_nnz, ws, ws_bytes, stream);
+}
+
+int iht_threshold_launches(int64_t N) { return N <= kClusterMaxN ? 1 : 3; }
 
 extern "C" int iht_threshold(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz,
                              const float* g, float mu, int32_t s, int64_t N, int32_t* out_idx,

@@ -316,7 +316,7 @@ class Solver:
     and the outputs are (B, s) / (B,)."""
 
     def __init__(self, pool, s, n_iter, mu, b_y, seed, level_mode=0, adjoint_variant=0, trace=False,
-                 use_graph=True, comm=None, profile=False, nrhs=1):
+                 use_graph=True, comm=None, profile=False, nrhs=1, adaptive=False, c=1e-3, k=2.0, max_shrink=60):
         lib = load()
         self.pool = pool                     # keep the code tensors alive
         self.s, self.n_iter = s, n_iter
@@ -325,7 +325,8 @@ class Solver:
         arr = (IhtQmat * len(pool))(*[c.desc for c in pool])
         cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
                         adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
-                        comm=comm.handle if comm is not None else None, profile=int(profile), nrhs=self.nrhs)
+                        comm=comm.handle if comm is not None else None, profile=int(profile), nrhs=self.nrhs,
+                        step_mode=int(adaptive), step_c=float(c), step_k=float(k), max_shrink=int(max_shrink))
         h = ctypes.c_void_p()
         check(lib.iht_solver_create(arr, len(pool), ctypes.byref(cfg), ctypes.byref(h)), "iht_solver_create")
         self.handle = h
@@ -375,6 +376,15 @@ class Solver:
         check(load().iht_solver_adjoint_times(self.handle, ctypes.cast(buf, ctypes.c_void_p)),
               "iht_solver_adjoint_times")
         return list(buf)
+
+    def steps(self, stream=None):
+        """Adaptive step: accepted mu and shrink count per iteration of the last run, CPU tensors
+        [n_iter] (batched: [n_iter, B])."""
+        shape = (self.n_iter, self.nrhs) if self.nrhs > 1 else (self.n_iter,)
+        mu = torch.empty(shape, dtype=torch.float32)
+        sh = torch.empty(shape, dtype=torch.int32)
+        check(load().iht_solver_steps(self.handle, _ptr(mu), _ptr(sh), _stream(stream)), "iht_solver_steps")
+        return mu, sh
 
     def launches_per_run(self):
         return int(load().iht_solver_launches_per_run(self.handle))
