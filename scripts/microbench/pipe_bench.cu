@@ -5,6 +5,10 @@
 //         the MMA warp waits a_full before each K-block (the kernel's A handoff).
 // MODE 3: MODE 2 + 6 extra warps spinning on an mbarrier that completes at the end.
 // MODE 4: MODE 2 but the MMA warp's 32 lanes all wait (kernel style) vs lane 0 only.
+// MODE 5: MODE 4 + a B ring (warp 6 waits b_free, arrives b_full; MMA warp waits b_full,
+//         commits to b_free as well): the kernel's two handoffs per K-block.
+// MODE 6: MODE 5 + tiles of 18 K-blocks with double-buffered accumulators handed to 4
+//         epilogue warps (acc_full commit / acc_free arrive), like adjoint_batched_kernel.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -25,12 +29,16 @@ template <int MODE>
 __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t a_full[ST], a_free[ST], done;
+  __shared__ uint64_t a_full[ST], a_free[ST], b_full[ST], b_free[ST], acc_full[2], acc_free[2], done;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < ST; ++i) { mbar_init(su32(&a_full[i]), 4); mbar_init(su32(&a_free[i]), 1); }
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(su32(&a_full[i]), 4); mbar_init(su32(&a_free[i]), 1);
+      mbar_init(su32(&b_full[i]), 1); mbar_init(su32(&b_free[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) { mbar_init(su32(&acc_full[i]), 1); mbar_init(su32(&acc_free[i]), 4); }
     mbar_init(su32(&done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -54,24 +62,37 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
     const long long t0 = clock64();
     int s = 0; uint32_t ph = 0;
     const uint32_t bbase = su32(smem);
-    for (int kb = 0; kb < nkb; ++kb) {
-      if (MODE >= 2) {
-        if (MODE == 4 || lane == 0) mbar_wait(su32(&a_full[s]), ph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
-          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
-                       "r"(tmem + 256 + (uint32_t)(s * 64 + kk * 8)), "l"(bd), "r"(IDESC), "r"(acc) : "memory");
+    const int tiles = MODE >= 6 ? nkb / 18 : 1;
+    const int per = MODE >= 6 ? 18 : nkb;
+    int kbg = 0;
+    for (int t = 0; t < tiles; ++t) {
+      const int ab = t & 1;
+      if (MODE >= 6 && t >= 2) mbar_wait(su32(&acc_free[ab]), ((t - 2) >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kb = 0; kb < per; ++kb, ++kbg) {
+        if (MODE >= 2) {
+          if (MODE >= 4 || lane == 0) mbar_wait(su32(&a_full[s]), ph);
+          if (MODE >= 5) mbar_wait(su32(&b_full[s]), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&a_free[s])) : "memory");
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t bd = sw128_desc(bbase + (MODE >= 5 ? s * 32768 : 0) + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + (MODE >= 6 ? ab * 128 : 0)),
+                         "r"(tmem + 256 + (uint32_t)(s * 64 + kk * 8)), "l"(bd), "r"(IDESC), "r"(acc) : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&a_free[s])) : "memory");
+          if (MODE >= 5)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&b_free[s])) : "memory");
+          if (MODE >= 6 && kb == per - 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&acc_full[ab])) : "memory");
+        }
+        __syncwarp();
+        if (++s == ST) { s = 0; ph ^= 1u; }
       }
-      __syncwarp();
-      if (++s == ST) { s = 0; ph ^= 1u; }
     }
     if (lane == 0) {
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&done)) : "memory");
@@ -79,6 +100,23 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
       cyc[blockIdx.x] = clock64() - t0;
     }
     __syncwarp();
+  } else if (warp == 6 && MODE >= 5) {
+    int s = 0; uint32_t ph = 0; bool wr = false;
+    for (int kb = 0; kb < nkb; ++kb) {
+      if (wr) mbar_wait(su32(&b_free[s]), ph ^ 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(su32(&b_full[s]));
+      if (++s == ST) { s = 0; ph ^= 1u; wr = true; }
+    }
+  } else if (warp >= 7 && MODE >= 6) {
+    for (int t = 0; t < nkb / 18; ++t) {
+      const int ab = t & 1;
+      mbar_wait(su32(&acc_full[ab]), (t >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(su32(&acc_free[ab]));
+    }
   } else if (MODE == 3 && warp >= 5) {
     mbar_wait(su32(&done), 0);
   }
@@ -89,12 +127,12 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
 
 template <int MODE>
 void run(const char* name, int sms) {
-  const int nkb = 2048;
+  const int nkb = 18 * 114;
   long long* d;
   cudaMalloc(&d, sms * sizeof(long long));
   auto k = pipe<MODE>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  k<<<sms, 352, 80 * 1024>>>(nkb, d);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+  k<<<sms, 352, 140 * 1024>>>(nkb, d);
   cudaError_t err = cudaDeviceSynchronize();
   long long h[256];
   cudaMemcpy(h, d, sms * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -112,5 +150,7 @@ int main() {
   run<2>("2: + converter handoff (a_full/a_free, 4 stages), lane-0 wait", sms);
   run<3>("3: + 6 spinning warps", sms);
   run<4>("4: handoff, all 32 MMA-warp lanes wait", sms);
+  run<5>("5: + B ring (second handoff + commit)", sms);
+  run<6>("6: + tiles with double-buffered accumulators / epilogue warps", sms);
   return 0;
 }
