@@ -16,11 +16,15 @@
 //
 // K order inside a 16-byte u8 chunk is permuted (row(p) below) identically on A and B.
 //
-// Roles per CTA (352 threads): warps 0-3 expand packed codes -> u8 A stages in TMEM
+// Roles per CTA (320 threads): warps 0-3 expand packed codes -> u8 A stages in TMEM
 // (tcgen05.st); warp 4 issues the MMAs (one thread); warp 5 bulk-copies the packed codes
-// (8 slots), warp 6 the r-limb image (4 stages), each on its own ring so neither waits for
-// the other; warps 7-10 run the epilogue (TMEM -> registers -> g).  The accumulators are
-// double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
+// (own ring of slots), warp 6 the r-limb image; warps 7-10 run the epilogue.
+// A (TMEM) and B (shared memory) share ONE stage ring: a stage is full when the 4 converter
+// warps and the limb producer (with its bulk-copy bytes) have arrived, and free after ONE
+// tcgen05.commit per K-block; a K-block is 16 MMAs (2/4-bit).  Each handoff costs MMA-pipe
+// time (scripts/microbench/pipe_bench.cu: 8-MMA K-blocks with split A/B rings ran at
+// 105 clk per MMA, one ring with 16-MMA K-blocks at 74, back-to-back issue 64-68).  The
+// accumulators are double-buffered so the epilogue of tile t overlaps the MMAs of t+1.
 #include <stdlib.h>
 
 #include "iht_internal.cuh"
@@ -28,12 +32,21 @@
 namespace iht {
 
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
-constexpr int kAStagesMax = 8;         // A (expanded codes) stages in TMEM: all 256 columns left by
-                                       // the two accumulators (4 at 2 bits, 8 at 4/8 bits)
-constexpr int kBStages = 4;            // B (r limbs) stages in shared memory
-constexpr int kPkSlots = 4;            // packed-code staging slots
-constexpr int kKG = 2;                 // K-blocks per packed-code slot (one 2*TS KiB copy per column tile)
 constexpr int kBThreads = 352;         // 11 warps (roles above)
+
+// Per bit width: tile-steps (512/b rows, 1 KiB of a 16-column tile) per K-block, so that a
+// K-block is 16 MMAs (K = 32 each) at 2 and 4 bits and 8 at 8 bits; A stages fill the 256
+// TMEM columns left by the two accumulators; B stages take 128 KiB of shared memory.
+template <int BITS> struct BCfg {
+  static constexpr int TS = BITS == 8 ? 4 : BITS;       // tile-steps per K-block
+  static constexpr int KBR = TS * 512 / BITS;           // rows (= u8 bytes per pixel row) per K-block
+  static constexpr int NKS = KBR / 32;                  // MMAs per K-block
+  static constexpr int ACOLS = KBR / 4;                 // TMEM columns of one A stage
+  static constexpr int STAGES = 256 / ACOLS;            // 2 (2/4-bit) or 4 (8-bit)
+  static constexpr int PK = 8 * TS * 1024;              // packed bytes per K-block (8 column tiles)
+  static constexpr int PKSLOTS = PK <= 16384 ? 4 : 2;   // packed-code slots
+};
+constexpr int kStagesMax = 4, kPkSlotsMax = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -96,7 +109,8 @@ struct BatchArgs {
   int64_t strip_bytes;
   int64_t N;
   int Rpad;
-  int nkb;                 // K-blocks (tile-steps) = Rpad / (512/b)
+  int nkb;                 // K-blocks = ceil(Rpad / KBR); the last may be ragged (fewer tile-steps)
+  int ksteps;              // tile-steps of a strip = Rpad / (512 / b)
   int ntiles;              // ceil(N / 128)
   int B;                   // MMA snapshots (padded to a multiple of 8; 2B <= 128)
   int Breal;               // snapshots actually written (<= B)
@@ -105,7 +119,7 @@ struct BatchArgs {
                            // epilogue loads/stores
   int L;
   float sigma;
-  const uint8_t* bimg;     // [nkb][KBB*2B] pre-swizzled limb image
+  const uint8_t* bimg;     // [nkb][KBR*2B] pre-swizzled limb image (rows past Rpad: zero limbs)
   const int* Fb;           // [B] exponents
   const int* Sb;           // [B][2] limb sums
   float* g;                // [B][N]
@@ -113,47 +127,36 @@ struct BatchArgs {
 
 template <int BITS>
 __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs a) {
-  constexpr int TS = BITS == 8 ? 2 : 1;  // tile-steps per K-block (>= 128 u8 bytes per row)
-  constexpr int KBR = TS * 512 / BITS;   // rows per K-block
-  constexpr int KBB = KBR;               // u8 bytes per row per K-block
-  constexpr int CH = KBB / 16;           // 16-byte chunks per row
-  constexpr int NKS = KBB / 32;          // MMAs (K = 32) per K-block
-  constexpr int PK = 8 * kKG * TS * 1024;  // packed bytes per slot (8 column tiles x kKG K-blocks x TS KiB)
-  constexpr int ACOLS = KBB / 4;         // TMEM columns of one A stage (4 u8 per column)
-  constexpr int kAStages = 256 / ACOLS;  // A stages in the 256 TMEM columns after the accumulators
-  static_assert(kAStages <= kAStagesMax, "A stages");
+  using C = BCfg<BITS>;
+  constexpr int TS = C::TS, KBB = C::KBR, NKS = C::NKS, PK = C::PK, ACOLS = C::ACOLS;
+  constexpr int ST = C::STAGES, PKS = C::PKSLOTS;
+  constexpr int CH = KBB / 16;           // 16-byte chunks per pixel row per K-block
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NB = 2 * a.B;                 // MMA N (snapshot-limb columns), multiple of 16
   const int BSZ = NB * KBB;               // B stage bytes
-  uint8_t* sB = smem;                                   // [kBStages][BSZ]  (BSZ multiple of 1024)
-  uint8_t* sP = sB + kBStages * BSZ;                    // [kPkSlots][PK]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kPkSlots * PK);
-  uint64_t* pk_full = bar;                        // [kPkSlots]  tx
-  uint64_t* pk_free = pk_full + kPkSlots;         // [kPkSlots]  4 converter warps
-  uint64_t* a_full = pk_free + kPkSlots;          // [kAStages]  4 converter warps
-  uint64_t* a_free = a_full + kAStagesMax;        // [kAStages]  tcgen05.commit
-  uint64_t* b_full = a_free + kAStagesMax;        // [kBStages]  tx
-  uint64_t* b_free = b_full + kBStages;           // [kBStages]  tcgen05.commit
-  uint64_t* acc_full = b_free + kBStages;         // [2]         tcgen05.commit
-  uint64_t* acc_free = acc_full + 2;        // [2]         4 epilogue warps
+  uint8_t* sB = smem;                                   // [ST][BSZ]  (BSZ multiple of 1024)
+  uint8_t* sP = sB + ST * BSZ;                          // [PKS][PK]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + PKS * PK);
+  uint64_t* pk_full = bar;                        // [PKS]  tx
+  uint64_t* pk_free = pk_full + kPkSlotsMax;      // [PKS]  4 converter warps
+  uint64_t* st_full = pk_free + kPkSlotsMax;      // [ST]   4 converter warps + B producer (+ tx)
+  uint64_t* st_free = st_full + kStagesMax;       // [ST]   one tcgen05.commit per K-block
+  uint64_t* acc_full = st_free + kStagesMax;      // [2]    tcgen05.commit
+  uint64_t* acc_free = acc_full + 2;              // [2]    4 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   float* ep_scale = reinterpret_cast<float*>(tmem_slot + 4);            // [B] sigma 2^-F_b
   long long* ep_off = reinterpret_cast<long long*>(ep_scale + 256);    // [B] (L-1) S_b
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPkSlots; ++i) {
+    for (int i = 0; i < PKS; ++i) {
       mbar_init2(smem_u32(&pk_full[i]), 1);
       mbar_init2(smem_u32(&pk_free[i]), 4);
     }
-    for (int i = 0; i < kAStages; ++i) {
-      mbar_init2(smem_u32(&a_full[i]), 4);
-      mbar_init2(smem_u32(&a_free[i]), 1);
-    }
-    for (int i = 0; i < kBStages; ++i) {
-      mbar_init2(smem_u32(&b_full[i]), 1);
-      mbar_init2(smem_u32(&b_free[i]), 1);
+    for (int i = 0; i < ST; ++i) {
+      mbar_init2(smem_u32(&st_full[i]), 5);
+      mbar_init2(smem_u32(&st_free[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init2(smem_u32(&acc_full[i]), 1);
@@ -161,10 +164,9 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {   // TMEM: 2 accumulator buffers (NB <= 128 columns each) + kAStages A stages
-    const uint32_t cols = 512;
+  if (warp == 4) {   // TMEM: 2 accumulator buffers (NB <= 128 columns each) + ST A stages
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(cols)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -185,81 +187,83 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     const int n = warp * 32 + lane;              // pixel row inside the tile (0..127)
     const int ct = n >> 4, cc = n & 15;           // column tile / column inside the tile
     int ps = 0, ss = 0;
-    uint32_t pph = 0, sph = 0;                    // phase bits of pk_full / a_free
-    bool a_wrapped = false;
+    uint32_t pph = 0, sph = 0;
+    bool s_wrapped = false;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
-        const int kg = kb % kKG;                  // K-block inside the current slot
-        const bool slot_end = kg == kKG - 1 || kb == a.nkb - 1;
         if (a.probe & 8) {                        // probe: hand the A stage over untouched
-          if (a_wrapped) mbar_wait2(smem_u32(&a_free[ss]), sph ^ 1u);
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
           __syncwarp();
-          if (lane == 0) mbar_arrive2(smem_u32(&a_full[ss]));
-          if (++ss == kAStages) { ss = 0; sph ^= 1u; a_wrapped = true; }
+          if (lane == 0) mbar_arrive2(smem_u32(&st_full[ss]));
+          if (++ss == ST) { ss = 0; sph ^= 1u; s_wrapped = true; }
           continue;
         }
-        if (kg == 0) mbar_wait2(smem_u32(&pk_full[ps]), pph);
-        uint32_t out[ACOLS];              // this pixel row's KBB u8 bytes, 4 per TMEM column
-#pragma unroll
+        const int tsn = min(TS, a.ksteps - kb * TS);   // tile-steps present (ragged last K-block)
+        mbar_wait2(smem_u32(&pk_full[ps]), pph);
+        if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
+        const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
+        // one tile-step at a time: 64 packed bytes of this pixel -> 512/b u8 codes -> TMEM
+#pragma unroll 1
         for (int ts = 0; ts < TS; ++ts) {
-          const uint8_t* src = sP + ps * PK + ct * (kKG * TS * 1024) + (kg * TS + ts) * 1024 + cc * 64;
-          const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
-                               reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
-          const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
-                                  w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
-          constexpr int CHT = CH / TS;       // 16-byte chunks per tile-step
+          constexpr int OW = 512 / BITS / 4;        // u32 outputs per tile-step (64, 32 or 16)
+          uint32_t out[OW];
+          if (ts < tsn) {
+            const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;
+            const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
+                                 reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
+            const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
+                                    w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
 #pragma unroll
-          for (int qq = 0; qq < CHT; ++qq) {
-            const int q = ts * CHT + qq;
-            if (BITS == 2) {            // chunk = packed word qq (16 codes)
-              const uint32_t x = w[qq];
-              out[4 * q + 0] = x & 0x03030303u;
-              out[4 * q + 1] = (x >> 2) & 0x03030303u;
-              out[4 * q + 2] = (x >> 4) & 0x03030303u;
-              out[4 * q + 3] = (x >> 6) & 0x03030303u;
-            } else if (BITS == 4) {     // chunk = packed words 2qq, 2qq+1
-              const uint32_t x0 = w[2 * qq], x1 = w[2 * qq + 1];
-              out[4 * q + 0] = x0 & 0x0F0F0F0Fu;
-              out[4 * q + 1] = (x0 >> 4) & 0x0F0F0F0Fu;
-              out[4 * q + 2] = x1 & 0x0F0F0F0Fu;
-              out[4 * q + 3] = (x1 >> 4) & 0x0F0F0F0Fu;
-            } else {                    // chunk = packed words 4qq..4qq+3 (bytes)
-              out[4 * q + 0] = w[4 * qq];
-              out[4 * q + 1] = w[4 * qq + 1];
-              out[4 * q + 2] = w[4 * qq + 2];
-              out[4 * q + 3] = w[4 * qq + 3];
+            for (int q = 0; q < OW / 4; ++q) {       // 16-byte chunk q of this tile-step
+              if (BITS == 2) {            // chunk = packed word q (16 codes)
+                const uint32_t x = w[q];
+                out[4 * q + 0] = x & 0x03030303u;
+                out[4 * q + 1] = (x >> 2) & 0x03030303u;
+                out[4 * q + 2] = (x >> 4) & 0x03030303u;
+                out[4 * q + 3] = (x >> 6) & 0x03030303u;
+              } else if (BITS == 4) {     // chunk = packed words 2q, 2q+1
+                const uint32_t x0 = w[2 * q], x1 = w[2 * q + 1];
+                out[4 * q + 0] = x0 & 0x0F0F0F0Fu;
+                out[4 * q + 1] = (x0 >> 4) & 0x0F0F0F0Fu;
+                out[4 * q + 2] = x1 & 0x0F0F0F0Fu;
+                out[4 * q + 3] = (x1 >> 4) & 0x0F0F0F0Fu;
+              } else {                    // chunk = packed words 4q..4q+3 (bytes)
+                out[4 * q + 0] = w[4 * q];
+                out[4 * q + 1] = w[4 * q + 1];
+                out[4 * q + 2] = w[4 * q + 2];
+                out[4 * q + 3] = w[4 * q + 3];
+              }
             }
+          } else {
+#pragma unroll
+            for (int q = 0; q < OW; ++q) out[q] = 0u;   // past the strip: code 0 (zero limbs anyway)
+          }
+          if (!(a.probe & 4)) {
+#pragma unroll
+            for (int c0 = 0; c0 < OW; c0 += 8)
+              asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                               ta + (uint32_t)(ts * OW + c0)),
+                           "r"(out[c0]), "r"(out[c0 + 1]), "r"(out[c0 + 2]), "r"(out[c0 + 3]), "r"(out[c0 + 4]),
+                           "r"(out[c0 + 5]), "r"(out[c0 + 6]), "r"(out[c0 + 7])
+                           : "memory");
           }
         }
         __syncwarp();
-        if (slot_end && lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));   // slot consumed (registers hold it)
-        if (a_wrapped) mbar_wait2(smem_u32(&a_free[ss]), sph ^ 1u);
-        // A stage ss lives in TMEM columns a_col0 + ss * ACOLS .. ; lane = pixel row n
-        const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
-#pragma unroll
-        for (int c0 = 0; c0 < ACOLS; c0 += 16)
-          if (!(a.probe & 4))
-          asm volatile(
-              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-                  ta + (uint32_t)c0),
-              "r"(out[c0]), "r"(out[c0 + 1]), "r"(out[c0 + 2]), "r"(out[c0 + 3]), "r"(out[c0 + 4]), "r"(out[c0 + 5]),
-              "r"(out[c0 + 6]), "r"(out[c0 + 7]), "r"(out[c0 + 8]), "r"(out[c0 + 9]), "r"(out[c0 + 10]),
-              "r"(out[c0 + 11]), "r"(out[c0 + 12]), "r"(out[c0 + 13]), "r"(out[c0 + 14]), "r"(out[c0 + 15])
-              : "memory");
+        if (lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));     // packed slot consumed
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive2(smem_u32(&a_full[ss]));
-        if (slot_end && ++ps == kPkSlots) { ps = 0; pph ^= 1u; }
-        if (++ss == kAStages) { ss = 0; sph ^= 1u; a_wrapped = true; }
+        if (lane == 0) mbar_arrive2(smem_u32(&st_full[ss]));
+        if (++ps == PKS) { ps = 0; pph ^= 1u; }
+        if (++ss == ST) { ss = 0; sph ^= 1u; s_wrapped = true; }
       }
     }
+    (void)CH;
   } else if (warp == 4) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = idesc_i8(kBT, NB);
-    int as = 0, bs = 0;
-    uint32_t aph = 0, bph = 0;
+    int ss = 0;
+    uint32_t sph = 0;
     int t = 0;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
       const int ab = t & 1;
@@ -267,85 +271,80 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dtm = tmem + ab * acc_stride;
       for (int kb = 0; kb < a.nkb; ++kb) {
-        mbar_wait2(smem_u32(&a_full[as]), aph);
-        mbar_wait2(smem_u32(&b_full[bs]), bph);
+        mbar_wait2(smem_u32(&st_full[ss]), sph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0 && (a.probe & 2)) {          // probe: no tensor work, release the stages at once
-          mbar_arrive2(smem_u32(&a_free[as]));
-          mbar_arrive2(smem_u32(&b_free[bs]));
-          if (kb == a.nkb - 1) mbar_arrive2(smem_u32(&acc_full[ab]));
-        } else if (lane == 0) {
-          const uint32_t atm = tmem + a_col0 + (uint32_t)(as * ACOLS), bbase = smem_u32(sB + bs * BSZ);
+        if (lane == 0) {
+          if (a.probe & 2) {                        // probe: no tensor work
+            mbar_arrive2(smem_u32(&st_free[ss]));
+            if (kb == a.nkb - 1) mbar_arrive2(smem_u32(&acc_full[ab]));
+          } else {
+            const uint32_t atm = tmem + a_col0 + (uint32_t)(ss * ACOLS), bbase = smem_u32(sB + ss * BSZ);
 #pragma unroll
-          for (int kk = 0; kk < NKS; ++kk) {
-            const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (NB * 128) + (kk & 3) * 32);
-            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtm),
-                "r"(atm + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc), "r"(acc)
-                : "memory");
-          }
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(&a_free[as]))
-                       : "memory");
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(&b_free[bs]))
-                       : "memory");
-          if (kb == a.nkb - 1)
+            for (int kk = 0; kk < NKS; ++kk) {
+              const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (NB * 128) + (kk & 3) * 32);
+              const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtm),
+                  "r"(atm + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc), "r"(acc)
+                  : "memory");
+            }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(&acc_full[ab]))
+                             smem_u32(&st_free[ss]))
                          : "memory");
+            if (kb == a.nkb - 1)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                               smem_u32(&acc_full[ab]))
+                           : "memory");
+          }
         }
         __syncwarp();
-        if (++as == kAStages) { as = 0; aph ^= 1u; }
-        if (++bs == kBStages) { bs = 0; bph ^= 1u; }
+        if (++ss == ST) { ss = 0; sph ^= 1u; }
       }
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- packed-code producer
-    // lanes 0-7 each copy one column tile's kKG consecutive K-blocks (contiguous in the
-    // tiled layout) so the 8 requests of a slot are issued in parallel
+    // lanes 0-7 each copy one column tile's tile-steps of the K-block (contiguous in the
+    // tiled layout), so the 8 requests of a slot are issued in parallel
     int ps = 0;
     uint32_t ph = 0;
     bool wrapped = false;
     const int64_t last_tile = (a.N + 15) / 16 - 1;
     for (int tile = (a.probe & 8) ? a.ntiles : blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-      for (int kb0 = 0; kb0 < a.nkb; kb0 += kKG) {
-        const int kgn = a.nkb - kb0 < kKG ? a.nkb - kb0 : kKG;
-        const uint32_t bytes = (uint32_t)(kgn * TS * 1024);
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        const int tsn = min(TS, a.ksteps - kb * TS);
+        const uint32_t bytes = (uint32_t)(tsn * 1024);
         if (wrapped) mbar_wait2(smem_u32(&pk_free[ps]), ph ^ 1u);
         if (lane == 0) mbar_expect_tx2(smem_u32(&pk_full[ps]), 8 * bytes);
         __syncwarp();
         if (lane < 8) {
           int64_t col_tile = (int64_t)tile * 8 + lane;                // 16-column tile index
           if (col_tile > last_tile) col_tile = last_tile;              // past N: any valid data
-          bulk_g2s2(smem_u32(sP + ps * PK + lane * (kKG * TS * 1024)),
-                    a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb0 * TS * 1024, bytes,
+          bulk_g2s2(smem_u32(sP + ps * PK + lane * (TS * 1024)),
+                    a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb * TS * 1024, bytes,
                     smem_u32(&pk_full[ps]));
         }
-        if (++ps == kPkSlots) { ps = 0; ph ^= 1u; wrapped = true; }
+        if (++ps == PKS) { ps = 0; ph ^= 1u; wrapped = true; }
       }
     }
   } else if (warp == 6) {
     // ---------------------------------------------------------------- r-limb (B) producer
-    // the whole warp waits (no divergent spin), lane 0 issues
-    int bs = 0;
-    uint32_t ph = 0;
+    int ss = 0;
+    uint32_t sph = 0;
     bool wrapped = false;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
-        if (wrapped) mbar_wait2(smem_u32(&b_free[bs]), ph ^ 1u);
+        if (wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
         if (lane == 0) {
           if ((a.probe & 1) && wrapped) {
-            mbar_arrive2(smem_u32(&b_full[bs]));                 // probe: reuse the stale stage
+            mbar_arrive2(smem_u32(&st_full[ss]));                 // probe: reuse the stale stage
           } else {
-            mbar_expect_tx2(smem_u32(&b_full[bs]), (uint32_t)BSZ);
-            bulk_g2s2(smem_u32(sB + bs * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&b_full[bs]));
+            mbar_expect_tx2(smem_u32(&st_full[ss]), (uint32_t)BSZ);
+            bulk_g2s2(smem_u32(sB + ss * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&st_full[ss]));
           }
         }
         __syncwarp();
-        if (++bs == kBStages) { bs = 0; ph ^= 1u; wrapped = true; }
+        if (++ss == ST) { ss = 0; sph ^= 1u; wrapped = true; }
       }
     }
   } else {
@@ -396,7 +395,7 @@ template <int BITS>
 __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nreal,
                                                             int nkb, uint8_t* __restrict__ bimg, int* __restrict__ Fb,
                                                             int* __restrict__ Sb) {
-  constexpr int KBR = (BITS == 8 ? 2 : 1) * 512 / BITS;
+  constexpr int KBR = BCfg<BITS>::KBR;
   const int b = blockIdx.x;                 // b >= nreal: zero padding snapshot (MMA N granularity)
   const bool live = b < nreal;
   const float* r = R + (int64_t)(live ? b : 0) * Rpad;
@@ -424,12 +423,13 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
   const float scale = ldexpf(1.0f, Fs);
   const int NB = 2 * B;
   int s0 = 0, s1 = 0;
-  for (int ch = threadIdx.x; ch < Rpad / 16; ch += blockDim.x) {
+  for (int ch = threadIdx.x; ch < nkb * KBR / 16; ch += blockDim.x) {   // rows past Rpad: zero limbs
     const int row0 = ch * 16;
+    const bool in = live && row0 < Rpad;      // Rpad is a multiple of 256: chunks are all-in or all-out
     float v[16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float4 f = live ? *reinterpret_cast<const float4*>(r + row0 + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 f = in ? *reinterpret_cast<const float4*>(r + row0 + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
       v[4 * k] = f.x;
       v[4 * k + 1] = f.y;
       v[4 * k + 2] = f.z;
@@ -471,12 +471,17 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
   }
 }
 
-static int kb_rows(int bits) { return (bits == 8 ? 2 : 1) * 512 / bits; }
+static int kb_rows(int bits) {
+  return bits == 2 ? BCfg<2>::KBR : bits == 4 ? BCfg<4>::KBR : BCfg<8>::KBR;
+}
 
 static size_t batched_smem(int bits, int B) {
-  const int KBB = kb_rows(bits), TS = bits == 8 ? 2 : 1;
-  return 1024 + (size_t)kBStages * 2 * B * KBB + (size_t)kPkSlots * 8 * kKG * TS * 1024 +
-         (size_t)(2 * kPkSlots + 2 * kAStagesMax + 2 * kBStages + 4) * 8 + 16 + 256 * 4 + 256 * 8;
+  const int KBB = kb_rows(bits);
+  const int ST = bits == 2 ? BCfg<2>::STAGES : bits == 4 ? BCfg<4>::STAGES : BCfg<8>::STAGES;
+  const size_t pk = bits == 2 ? (size_t)BCfg<2>::PK * BCfg<2>::PKSLOTS
+                  : bits == 4 ? (size_t)BCfg<4>::PK * BCfg<4>::PKSLOTS : (size_t)BCfg<8>::PK * BCfg<8>::PKSLOTS;
+  return 1024 + (size_t)ST * 2 * B * KBB + pk + (size_t)(2 * kPkSlotsMax + 2 * kStagesMax + 4) * 8 + 16 +
+         256 * 4 + 256 * 8;
 }
 
 }  // namespace iht
@@ -519,8 +524,8 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
   const int64_t need = iht_adjoint_batched_ws_bytes(A, nrhs);
   if (ws == nullptr || ws_bytes < need) return IHT_EINVAL;
   const int KBR = kb_rows(A->bits);
-  const int nkb = (int)(Rpad / KBR);        // Rpad is a multiple of 256 rows per plane
-  if (nkb * KBR != Rpad) return IHT_EINVAL;
+  const int nkb = (int)((Rpad + KBR - 1) / KBR);   // the last K-block may hold fewer tile-steps
+  const int ksteps = (int)(Rpad / (512 / A->bits));
   cudaStream_t st = (cudaStream_t)stream;
   const int bp_max = chunk_pad(nrhs);
   uint8_t* bimg = static_cast<uint8_t*>(ws);
@@ -541,6 +546,7 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     b.N = A->cols;
     b.Rpad = (int)Rpad;
     b.nkb = nkb;
+    b.ksteps = ksteps;
     b.ntiles = (int)((A->cols + kBT - 1) / kBT);
     b.B = bp;
     b.Breal = nb;

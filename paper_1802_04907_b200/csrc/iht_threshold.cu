@@ -30,6 +30,8 @@
 // compaction takes per-CTA (greater, equal) counts, an exclusive scan over the cluster
 // gives each CTA its output offset and its share of the lowest-index ties.  No global
 // atomics, no workspace memset, no candidate-capacity limit.
+#include <stdlib.h>
+
 #include <cooperative_groups.h>
 
 #include "iht_internal.cuh"
@@ -550,7 +552,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
     int64_t N, int64_t col_offset, int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
-    int32_t ldo, int32_t* __restrict__ out_nnz) {
+    int32_t ldo, int32_t* __restrict__ out_nnz, int probe) {
   extern __shared__ __align__(16) unsigned char dsm[];
   float* as = reinterpret_cast<float*>(dsm);                                  // [slice] (multiple of 4)
   if (mu_dev) mu = mu_dev[blockIdx.y];
@@ -631,6 +633,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   }
   nan = __syncthreads_or(nan);
   if (tid == 0) cs.flags[0] = nan | poisoned;
+  if (probe == 1) return;                           // profiling probe (IHT_THR_PROBE): phases' cost
   cluster.sync();
   int bad = 0;
   for (int p = 0; p < CL; ++p) bad |= cluster.map_shared_rank(cs.flags, p)[0];
@@ -646,6 +649,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     cluster.sync();
     return;
   }
+  if (probe == 2) { cluster.sync(); return; }
   const bool all = (int64_t)s >= N;
   unsigned int d1 = 0;
   int target = s;
@@ -675,6 +679,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     wc += __popc(bs);
   }
   if (lane == 0) wgt[warp] = wc;
+  if (probe == 3) { cluster.sync(); return; }
   const int ovf = __syncthreads_or(wc > kWarpCand);
   if (tid == 0) cs.flags[1] = ovf;
   cluster.sync();
@@ -763,6 +768,15 @@ __global__ void __launch_bounds__(kThrThreads, 1) thr_merge(
 
 using namespace iht;
 
+static int thr_probe() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IHT_THR_PROBE");     // profiling only: stop the fused kernel after a phase
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 extern "C" int64_t iht_threshold_batched_ws_bytes(int64_t N, int32_t s, int32_t nrhs) {
   (void)s;
   if (N <= 0 || nrhs <= 0) return -1;
@@ -819,7 +833,7 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
     lc.attrs = at;
     lc.numAttrs = 1;
     IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
-                                      N, col_offset, slice, out_idx, out_val, ldo, out_nnz));
+                                      N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe()));
     return IHT_OK;
   }
   ThrWs w{};

@@ -9,6 +9,17 @@
 //         commits to b_free as well): the kernel's two handoffs per K-block.
 // MODE 6: MODE 5 + tiles of 18 K-blocks with double-buffered accumulators handed to 4
 //         epilogue warps (acc_full commit / acc_free arrive), like adjoint_batched_kernel.
+// MODE 7: MODE 6 with ONE commit per K-block to a shared stage-free barrier (converters and
+//         B producer both wait on it).
+// MODE 8: MODE 7 with ONE stage-full barrier (4 converter arrivals + 1 producer arrival).
+// MODE 9: MODE 8, the MMA warp polls with mbarrier.test_wait (no suspend) instead of try_wait.
+// MODE 10: MODE 8 with 8 stages (A stages of 32 TMEM columns, 4 MMAs per K-block... kept 8).
+// MODE 11: MODE 8 with 16 MMAs per K-block and 2 stages.
+// MODE 12: MODE 8 without the MMA warp's tcgen05.fence::after_thread_sync per K-block.
+// MODE 14: MODE 8, but converters and producer never wait for a free stage (timing only).
+// MODE 15: MODE 8 with 16 stages (aliased TMEM/smem addresses; timing only).
+// MODE 13: MODE 8, converters skip tcgen05.fence::before_thread_sync... (they issue no tcgen05 ops here)
+//          and the MMA warp fences only every 2nd K-block (timing probe only).
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -23,19 +34,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t ph) {
   asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(m), "r"(ph) : "memory");
 }
 constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-constexpr int ST = 4;
+template <int MODE> struct Cfg { static constexpr int ST = MODE == 10 ? 8 : (MODE == 11 ? 2 : (MODE == 15 ? 16 : 4));
+                                  static constexpr bool FENCE = MODE != 12;
+                                  static constexpr int KPB = MODE == 11 ? 16 : 8; };
+__device__ __forceinline__ void mbar_spin(uint32_t m, uint32_t ph) {
+  asm volatile("{\n\t.reg .pred p;\n\tS_%=:\n\tmbarrier.test_wait.parity.shared.b64 p, [%0], %1;\n\t@!p bra S_%=;\n\t}" ::"r"(m), "r"(ph) : "memory");
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
+  constexpr int ST = Cfg<MODE>::ST, KPB = Cfg<MODE>::KPB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t a_full[ST], a_free[ST], b_full[ST], b_free[ST], acc_full[2], acc_free[2], done;
+  __shared__ uint64_t a_full[16], a_free[16], b_full[16], b_free[16], acc_full[2], acc_free[2], done;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < ST; ++i) {
-      mbar_init(su32(&a_full[i]), 4); mbar_init(su32(&a_free[i]), 1);
+      mbar_init(su32(&a_full[i]), MODE >= 8 ? 5 : 4); mbar_init(su32(&a_free[i]), 1);
       mbar_init(su32(&b_full[i]), 1); mbar_init(su32(&b_free[i]), 1);
     }
     for (int i = 0; i < 2; ++i) { mbar_init(su32(&acc_full[i]), 1); mbar_init(su32(&acc_free[i]), 4); }
@@ -53,7 +70,7 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
   if (warp < 4 && MODE >= 2) {
     int s = 0; uint32_t ph = 0; bool wr = false;
     for (int kb = 0; kb < nkb; ++kb) {
-      if (wr) mbar_wait(su32(&a_free[s]), ph ^ 1u);
+      if (wr && MODE != 14) mbar_wait(su32(&a_free[s]), ph ^ 1u);
       __syncwarp();
       if (lane == 0) mbar_arrive(su32(&a_full[s]));
       if (++s == ST) { s = 0; ph ^= 1u; wr = true; }
@@ -71,21 +88,22 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int kb = 0; kb < per; ++kb, ++kbg) {
         if (MODE >= 2) {
-          if (MODE >= 4 || lane == 0) mbar_wait(su32(&a_full[s]), ph);
-          if (MODE >= 5) mbar_wait(su32(&b_full[s]), ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (MODE == 9) mbar_spin(su32(&a_full[s]), ph);
+          else if (MODE >= 4 || lane == 0) mbar_wait(su32(&a_full[s]), ph);
+          if (MODE >= 5 && MODE < 8) mbar_wait(su32(&b_full[s]), ph);
+          if (Cfg<MODE>::FENCE && (MODE != 13 || (kb & 1) == 0)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
         if (lane == 0) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t bd = sw128_desc(bbase + (MODE >= 5 ? s * 32768 : 0) + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
+          for (int kk = 0; kk < KPB; ++kk) {
+            const uint64_t bd = sw128_desc(bbase + (MODE >= 5 ? (s & 3) * 32768 : 0) + ((kk >> 2) & 1) * (128 * 128) + (kk & 3) * 32);
             const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                          "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + (MODE >= 6 ? ab * 128 : 0)),
-                         "r"(tmem + 256 + (uint32_t)(s * 64 + kk * 8)), "l"(bd), "r"(IDESC), "r"(acc) : "memory");
+                         "r"(tmem + 256 + (uint32_t)((s * KPB * 8 + kk * 8) & 255)), "l"(bd), "r"(IDESC), "r"(acc) : "memory");
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&a_free[s])) : "memory");
-          if (MODE >= 5)
+          if (MODE >= 5 && MODE < 7)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&b_free[s])) : "memory");
           if (MODE >= 6 && kb == per - 1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&acc_full[ab])) : "memory");
@@ -103,9 +121,9 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
   } else if (warp == 6 && MODE >= 5) {
     int s = 0; uint32_t ph = 0; bool wr = false;
     for (int kb = 0; kb < nkb; ++kb) {
-      if (wr) mbar_wait(su32(&b_free[s]), ph ^ 1u);
+      if (wr && MODE != 14) mbar_wait(su32(MODE >= 7 ? &a_free[s] : &b_free[s]), ph ^ 1u);
       __syncwarp();
-      if (lane == 0) mbar_arrive(su32(&b_full[s]));
+      if (lane == 0) mbar_arrive(su32(MODE >= 8 ? &a_full[s] : &b_full[s]));
       if (++s == ST) { s = 0; ph ^= 1u; wr = true; }
     }
   } else if (warp >= 7 && MODE >= 6) {
@@ -139,7 +157,7 @@ void run(const char* name, int sms) {
   double mean = 0;
   for (int i = 0; i < sms; ++i) mean += h[i];
   mean /= sms;
-  printf("%-60s %s  %.1f clk/MMA\n", name, cudaGetErrorString(err), mean / (nkb * 8.0));
+  printf("%-60s %s  %.1f clk/MMA\n", name, cudaGetErrorString(err), mean / (nkb * (double)Cfg<MODE>::KPB));
   cudaFree(d);
 }
 
@@ -152,5 +170,14 @@ int main() {
   run<4>("4: handoff, all 32 MMA-warp lanes wait", sms);
   run<5>("5: + B ring (second handoff + commit)", sms);
   run<6>("6: + tiles with double-buffered accumulators / epilogue warps", sms);
+  run<7>("7: 6 with one commit per K-block (shared stage-free barrier)", sms);
+  run<8>("8: 7 with one stage-full barrier (5 arrivals)", sms);
+  run<9>("9: 8 with test_wait polling in the MMA warp", sms);
+  run<10>("10: 8 with 8 stages", sms);
+  run<11>("11: 8 with 16 MMAs per K-block, 2 stages", sms);
+  run<12>("12: 8 without tcgen05.fence::after_thread_sync", sms);
+  run<13>("13: 8 fencing every 2nd K-block", sms);
+  run<14>("14: 8 with no free-stage waits (unbounded run-ahead)", sms);
+  run<15>("15: 8 with 16 stages", sms);
   return 0;
 }
