@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--variant", type=int, default=0, help="adjoint: 0 int8 MMA, 1 FFMA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--adaptive", action="store_true", help="Algorithm 1's adaptive step (NEXT-1)")
     return ap.parse_args()
 
 
@@ -226,7 +227,7 @@ def main():
         y_shard = p.y[row0:row0 + rows]
     y_dev = torch.from_numpy(y_shard).to(dev)
     sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, adjoint_variant=args.variant, comm=comm,
-                     profile=True, nrhs=B)
+                     profile=True, nrhs=B, adaptive=args.adaptive)
     setup_s = time.perf_counter() - t_setup
 
     # ---- device-resident timed region -----------------------------------------------
@@ -342,6 +343,8 @@ def main():
             "l2": f"inputs > L2: pool {p.K * copy_bytes / 2**30:.2f} GiB per GPU streamed from HBM"
                   if p.K * copy_bytes > 126e6 else f"pool {p.K * copy_bytes / 2**20:.1f} MiB is L2-resident",
             "adjoint_variant": args.variant,
+            "step": "adaptive mu-hat with accept/shrink loop (Algorithm 1, P:350-363)" if args.adaptive
+                    else f"fixed mu = {p.mu:g}",
         },
         "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
                 "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},

@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
 constexpr int kClThreads = 512;               // threads per CTA of the fused kernel
 constexpr int kClWarps = kClThreads / 32;
 constexpr int kClusterSlice = 32768;          // a-values per CTA held in shared memory (128 KiB)
-constexpr int kClusterMax = 8;                // portable cluster size
+constexpr int kClusterMax = 8;                // portable cluster size (16 measured slower)
 constexpr int64_t kClusterMaxN = (int64_t)kClusterSlice * kClusterMax;
 constexpr int kWarpCand = 256;                // candidate slots per warp (per CTA: 4096)
 
@@ -791,6 +791,7 @@ static int thr_attrs() {
   if (!g_thr_attr) {
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
+    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kClusterSlice * 4 + kClWarps * kWarpCand * 8));
     g_thr_attr = true;
@@ -818,6 +819,8 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
     int CL = 1;
     while ((int64_t)CL * kClusterSlice < N) CL *= 2;
     // spread small problems too: up to ~2 CTAs per SM while slices stay >= 4096 a-values
+    // more, smaller slices while that keeps <= 1 CTA per SM and >= 4096 a-values per CTA
+    // (measured: 2 CTAs per SM or clusters of 16 are slower -- more cluster barriers)
     while (CL < kClusterMax && (int64_t)CL * 2 * nrhs <= 148 && N / (2 * CL) >= 4096) CL *= 2;
     const int slice = (int)(((N + CL - 1) / CL + 31) / 32 * 32);   // 16-byte aligned slices
     cudaLaunchConfig_t lc = {};
