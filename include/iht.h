@@ -209,6 +209,32 @@ IHT_API int64_t iht_adjoint_batched_ws_bytes(const iht_qmat* A, int32_t nrhs);
 IHT_API int iht_adjoint_batched(const iht_qmat* A, const float* R_dev, int32_t nrhs, float* G_dev,
                                 void* ws_dev, int64_t ws_bytes, void* stream);
 
+/* ------------------------------------- NEXT-2: fresh copies drawn on the fly */
+/* The fp32 Phi itself (this shard's rows), from which any copy Phi-hat_k is drawn on the
+ * fly: code(m, n) is the Q-contract rounding of phi with the Philox word of counter
+ * (n >> 2, row_offset + m, k, plane << 8), exactly what iht_quantize stores for copy k.
+ * Algorithm 1's 2 n* independent copies then need no storage. */
+typedef struct {
+  int64_t rows, cols, row_offset;
+  int64_t ld;           /* row stride in (complex) elements, >= cols                     */
+  int32_t planes, bits, level_mode, reserved;
+  uint64_t seed;
+  float scale_c;        /* global max |component| (a1)                                   */
+  int32_t reserved2;
+  const float* phi;     /* device, row-major, complex interleaved                        */
+} iht_fmat;
+
+/* g = Re(Phi-hat_k^H r) with Phi-hat_k drawn on the fly from F (copy_id = k).  r:
+ * stacked vector; g: cols floats.  Deterministic (row splits reduced in a fixed order).
+ * Workspace: iht_adjoint_fresh_ws_bytes. */
+IHT_API int64_t iht_adjoint_fresh_ws_bytes(const iht_fmat* F);
+IHT_API int iht_adjoint_fresh(const iht_fmat* F, int32_t copy_id, const float* r_dev, float* g_dev, void* ws_dev,
+                              int64_t ws_bytes, void* stream);
+/* r = y-hat - Phi-hat_k x over the support of x, Phi-hat_k drawn on the fly. */
+IHT_API int iht_forward_fresh(const iht_fmat* F, int32_t copy_id, const int32_t* x_idx_dev, const float* x_val_dev,
+                              const int32_t* x_nnz_dev, int32_t max_nnz, const float* yhat_dev, float* r_dev,
+                              void* stream);
+
 /* ---------------------------------------------------- (a6) update + H_s */
 /* a = x + mu g, then H_s: keep the s entries of largest |a|,
  * ties to the LOWEST index, zeros never kept (reading c15).  Output
@@ -302,6 +328,12 @@ typedef struct {
  * lazily, the CUDA graph); the pool's codes must outlive the solver. */
 typedef struct iht_solver iht_solver;
 IHT_API int iht_solver_create(const iht_qmat* pool, int K, const iht_config* cfg, iht_solver** out);
+/* Algorithm 1 with FRESH copies (NEXT-2): iteration n draws Phi-hat_{2n-1} (copy id 2n-2,
+ * adjoint) and Phi-hat_{2n} (copy id 2n-1, forward) on the fly from the fp32 Phi in F,
+ * i.e. K = 2 n* without storing any copy.  Single observation, fixed step; with a
+ * communicator the rows are sharded (F->row_offset) and g is all-reduced.  F->phi must
+ * outlive the solver. */
+IHT_API int iht_solver_create_fresh(const iht_fmat* F, const iht_config* cfg, iht_solver** out);
 IHT_API int iht_solver_destroy(iht_solver* solver);
 
 #define IHT_HOST_IO 1   /* y and the outputs are host pointers (pinned for async copies) */

@@ -33,6 +33,15 @@ class IhtQmat(ctypes.Structure):
     ]
 
 
+class IhtFmat(ctypes.Structure):
+    """Mirror of iht_fmat (include/iht.h): the fp32 Phi that fresh copies are drawn from."""
+    _fields_ = [
+        ("rows", c_i64), ("cols", c_i64), ("row_offset", c_i64), ("ld", c_i64),
+        ("planes", c_i32), ("bits", c_i32), ("level_mode", c_i32), ("reserved", c_i32),
+        ("seed", c_u64), ("scale_c", c_f32), ("reserved2", c_i32), ("phi", c_vp),
+    ]
+
+
 class IhtConfig(ctypes.Structure):
     """Mirror of iht_config (include/iht.h)."""
     _fields_ = [
@@ -69,6 +78,10 @@ SIGNATURES = {
     "iht_adjoint_batched": (c_int, [ctypes.POINTER(IhtQmat), c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
     "iht_threshold_ws_bytes": (c_i64, [c_i64, c_i32]),
     "iht_threshold": (c_int, [c_vp, c_vp, c_vp, c_vp, c_f32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "iht_adjoint_fresh_ws_bytes": (c_i64, [ctypes.POINTER(IhtFmat)]),
+    "iht_adjoint_fresh": (c_int, [ctypes.POINTER(IhtFmat), c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "iht_forward_fresh": (c_int, [ctypes.POINTER(IhtFmat), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "iht_solver_create_fresh": (c_int, [ctypes.POINTER(IhtFmat), ctypes.POINTER(IhtConfig), ctypes.POINTER(c_vp)]),
     "iht_threshold_batched_ws_bytes": (c_i64, [c_i64, c_i32, c_i32]),
     "iht_threshold_batched": (c_int, [c_vp, c_vp, c_vp, c_i32, c_vp, c_f32, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp,
                                       c_i32, c_vp, c_vp, c_i64, c_vp]),

@@ -145,7 +145,9 @@ extern "C" int iht_comm_allgather(iht_comm* comm, const void* send, void* recv, 
 //           all-reduced, local top-s candidates all-gathered and merged.
 
 struct iht_solver {
-  std::vector<iht_qmat> pool;
+  std::vector<iht_qmat> pool;          // fresh mode: one descriptor-only entry (codes NULL)
+  bool fresh = false;                  // NEXT-2: copies drawn on the fly from fm
+  iht_fmat fm{};
   iht_config cfg;
   int64_t rows, N, vlen;
   int planes;
@@ -317,14 +319,22 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
     int32_t* on = S->xs_nnz + (int64_t)out_slot * B;
     // (a4) forward: r_b = y-hat_b - Phi-hat_F x_b  (column shards: partial, then summed)
     const float* yh = (S->colshard && S->rank != 0) ? nullptr : S->yhat;
-    if ((rc = iht_forward_batched(&F, xi, xv, xn, s, s, B, yh, S->r, st)) != IHT_OK) return rc;
+    if (S->fresh) {
+      if ((rc = iht_forward_fresh(&S->fm, 2 * n - 1, xi, xv, xn, s, S->yhat, S->r, st)) != IHT_OK) return rc;
+    } else if ((rc = iht_forward_batched(&F, xi, xv, xn, s, s, B, yh, S->r, st)) != IHT_OK) {
+      return rc;
+    }
     L += 1;
     if (S->colshard) {
       if ((rc = iht_comm_allreduce(S->cfg.comm, S->r, (int64_t)B * S->vlen, 0, st)) != IHT_OK) return rc;
     }
     // (a5) adjoint
     if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[2 * (n - 1)], st));
-    if (!S->batched) {
+    if (S->fresh) {
+      if ((rc = iht_adjoint_fresh(&S->fm, 2 * n - 2, S->r, S->g, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
+        return rc;
+      L += 2;
+    } else if (!S->batched) {
       if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
         return rc;
       L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
@@ -367,13 +377,38 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
   return IHT_OK;
 }
 
+static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg, const iht_fmat* fm,
+                              iht_solver** out);
+
 extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* cfg, iht_solver** out) {
+  return solver_create_impl(pool, K, cfg, nullptr, out);
+}
+
+extern "C" int iht_solver_create_fresh(const iht_fmat* F, const iht_config* cfg, iht_solver** out) {
+  if (F == nullptr || cfg == nullptr || out == nullptr || F->phi == nullptr) return IHT_EINVAL;
+  if (cfg->nrhs > 1 || cfg->step_mode != 0) return IHT_EUNSUPPORTED;   // single observation, fixed step
+  if (iht_adjoint_fresh_ws_bytes(F) < 0) return IHT_EINVAL;
+  iht_qmat d{};                          // descriptor-only pool entry: shape of the copies
+  d.rows = F->rows;
+  d.cols = F->cols;
+  d.row_offset = F->row_offset;
+  d.planes = F->planes;
+  d.bits = F->bits;
+  d.level_mode = F->level_mode;
+  d.seed = F->seed;
+  d.scale_c = F->scale_c;
+  d.strip_bytes = iht_strip_bytes(F->rows, F->planes, F->bits);
+  return solver_create_impl(&d, 1, cfg, F, out);
+}
+
+static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg, const iht_fmat* fm,
+                              iht_solver** out) {
   if (pool == nullptr || K < 1 || cfg == nullptr || out == nullptr) return IHT_EINVAL;
   if (cfg->s < 0 || cfg->n_iter < 0 || !isfinite(cfg->mu) || cfg->nrhs < 0) return IHT_EINVAL;
   if (cfg->b_y < 2 || cfg->b_y > 8 || (cfg->level_mode != 0 && cfg->level_mode != 1)) return IHT_EINVAL;
   if (cfg->adjoint_variant != 0 && cfg->adjoint_variant != 1) return IHT_EINVAL;
   const iht_qmat& q0 = pool[0];
-  for (int k = 0; k < K; ++k) {
+  for (int k = 0; k < K && fm == nullptr; ++k) {
     const iht_qmat& q = pool[k];
     if (q.codes == nullptr || q.rows != q0.rows || q.cols != q0.cols || q.planes != q0.planes ||
         q.bits != q0.bits || q.row_offset != q0.row_offset || q.col_offset != q0.col_offset ||
@@ -400,6 +435,10 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
   }
   iht_solver* S = new iht_solver();
   S->pool.assign(pool, pool + K);
+  if (fm) {
+    S->fresh = true;
+    S->fm = *fm;
+  }
   S->cfg = *cfg;
   S->rows = q0.rows;
   S->N = q0.cols;
@@ -414,7 +453,8 @@ extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* 
   // NCCL kernels may not sit inside a conditional body graph: the adaptive row-sharded
   // run drives its shrink loop from the host
   if (cfg->step_mode == 1 && S->rowshard) S->cfg.use_graph = 0;
-  S->ws_adj_bytes = batched ? iht_adjoint_batched_ws_bytes(&q0, B) : iht_adjoint_ws_bytes(&q0);
+  S->ws_adj_bytes = fm ? iht_adjoint_fresh_ws_bytes(fm)
+                      : batched ? iht_adjoint_batched_ws_bytes(&q0, B) : iht_adjoint_ws_bytes(&q0);
   S->ws_thr_bytes = iht_threshold_batched_ws_bytes(S->N, cfg->s, B);
   S->nslots = cfg->trace ? cfg->n_iter + 1 : 2;
   const int s = cfg->s > 0 ? cfg->s : 1;

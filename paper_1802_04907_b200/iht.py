@@ -13,11 +13,12 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import IhtConfig, IhtQmat, check, load
+from ._lib import IhtConfig, IhtFmat, IhtQmat, check, load
 
 __all__ = ["absmax", "absmax_batched", "quantize", "quantize_rows", "quantize_vec", "quantize_vec_batched", "forward",
            "forward_batched", "adjoint", "adjoint_batched", "threshold", "threshold_batched", "merge_candidates",
-           "Solver", "solve", "Comm", "QCopy", "strip_bytes", "vec_len", "rows_pad"]
+           "Solver", "solve", "Comm", "QCopy", "FreshPhi", "adjoint_fresh", "forward_fresh", "strip_bytes", "vec_len",
+           "rows_pad"]
 
 
 def _stream(stream=None):
@@ -273,6 +274,48 @@ def merge_candidates(cand_idx, cand_val, cand_nnz, s, stream=None):
     return oi, ov, on
 
 
+@dataclass
+class FreshPhi:
+    """NEXT-2: the fp32 Phi (CUDA tensor kept alive here) from which copies are drawn on the fly."""
+    desc: IhtFmat
+    phi: torch.Tensor
+
+
+def fresh_phi(phi, bits, level_mode, seed, scale_c, row_offset=0):
+    """Describe a (rows x cols) float32 / complex64 row-major CUDA matrix for on-the-fly copies."""
+    _require_cuda(phi)
+    planes = 2 if phi.is_complex() else 1
+    if phi.stride(1) != 1:
+        raise ValueError("phi must be row-major (unit column stride)")
+    base = torch.view_as_real(phi) if planes == 2 else phi
+    rows, cols = phi.shape
+    d = IhtFmat(rows=rows, cols=cols, row_offset=row_offset, ld=phi.stride(0), planes=planes, bits=bits,
+                level_mode=level_mode, reserved=0, seed=seed, scale_c=float(scale_c), reserved2=0,
+                phi=base.data_ptr())
+    return FreshPhi(d, phi)
+
+
+def adjoint_fresh(F, copy_id, r, stream=None):
+    """g = Re(Phi-hat_k^H r) with copy k drawn on the fly (no stored codes)."""
+    _require_cuda(r)
+    lib = load()
+    wsb = lib.iht_adjoint_fresh_ws_bytes(ctypes.byref(F.desc))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=r.device)
+    g = torch.empty(F.desc.cols, dtype=torch.float32, device=r.device)
+    check(lib.iht_adjoint_fresh(ctypes.byref(F.desc), copy_id, _ptr(r), _ptr(g), _ptr(ws), wsb, _stream(stream)),
+          "iht_adjoint_fresh")
+    return g
+
+
+def forward_fresh(F, copy_id, x_idx, x_val, x_nnz, yhat, stream=None):
+    """r = y-hat - Phi-hat_k x over the support of x, copy k drawn on the fly."""
+    _require_cuda(x_idx, x_val, x_nnz, yhat)
+    r = torch.empty_like(yhat)
+    check(load().iht_forward_fresh(ctypes.byref(F.desc), copy_id, _ptr(x_idx), _ptr(x_val), _ptr(x_nnz),
+                                   x_idx.numel(), _ptr(yhat), _ptr(r), _stream(stream)), "iht_forward_fresh")
+    return r
+
+
 class Comm:
     """NCCL communicator of libiht (iht_comm_*); unique id broadcast via torch.distributed."""
 
@@ -317,20 +360,27 @@ class Solver:
 
     def __init__(self, pool, s, n_iter, mu, b_y, seed, level_mode=0, adjoint_variant=0, trace=False,
                  use_graph=True, comm=None, profile=False, nrhs=1, adaptive=False, c=1e-3, k=2.0, max_shrink=60):
+        """pool: list of QCopy (stored copies), or a FreshPhi (NEXT-2: copies drawn on the fly,
+        K = 2 n*)."""
         lib = load()
-        self.pool = pool                     # keep the code tensors alive
+        self.pool = pool                     # keep the code / Phi tensors alive
         self.s, self.n_iter = s, n_iter
         self.trace = trace
         self.nrhs = max(1, nrhs)
-        arr = (IhtQmat * len(pool))(*[c.desc for c in pool])
         cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
                         adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
                         comm=comm.handle if comm is not None else None, profile=int(profile), nrhs=self.nrhs,
                         step_mode=int(adaptive), step_c=float(c), step_k=float(k), max_shrink=int(max_shrink))
         h = ctypes.c_void_p()
-        check(lib.iht_solver_create(arr, len(pool), ctypes.byref(cfg), ctypes.byref(h)), "iht_solver_create")
+        if isinstance(pool, FreshPhi):
+            check(lib.iht_solver_create_fresh(ctypes.byref(pool.desc), ctypes.byref(cfg), ctypes.byref(h)),
+                  "iht_solver_create_fresh")
+            self.device = pool.phi.device
+        else:
+            arr = (IhtQmat * len(pool))(*[c.desc for c in pool])
+            check(lib.iht_solver_create(arr, len(pool), ctypes.byref(cfg), ctypes.byref(h)), "iht_solver_create")
+            self.device = pool[0].codes.device
         self.handle = h
-        self.device = pool[0].codes.device
         shape = (self.nrhs, max(s, 1)) if self.nrhs > 1 else (max(s, 1),)
         self.out_idx = torch.empty(shape, dtype=torch.int32, device=self.device)
         self.out_val = torch.empty(shape, dtype=torch.float32, device=self.device)
