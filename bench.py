@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--adaptive", action="store_true", help="Algorithm 1's adaptive step (NEXT-1)")
+    ap.add_argument("--fresh", action="store_true",
+                    help="NEXT-2: fresh copies drawn on the fly from the resident fp32 Phi (K = 2 n*, no codes)")
     return ap.parse_args()
 
 
@@ -219,8 +221,13 @@ def main():
     t_setup = time.perf_counter()
     p = make_problem(args)
     B = p.meta["batch_y"].shape[1] if "batch_y" in p.meta else 1
-    from paper_1802_04907_b200.problem import build_pool
-    pool, c_phi, prep, rows, row0 = build_pool(p, rank, world, dev, dist_on, shard="cols" if B > 1 else "rows")
+    from paper_1802_04907_b200.problem import build_fresh, build_pool
+    if args.fresh:
+        if B > 1:
+            raise SystemExit("--fresh is the single-observation path")
+        pool, c_phi, prep, rows, row0 = build_fresh(p, rank, world, dev, dist_on)
+    else:
+        pool, c_phi, prep, rows, row0 = build_pool(p, rank, world, dev, dist_on, shard="cols" if B > 1 else "rows")
     if B > 1:        # (B, M) observations, replicated on every column shard
         y_shard = np.ascontiguousarray(p.meta["batch_y"].T)
     else:
@@ -278,9 +285,12 @@ def main():
 
     # ---- bookkeeping --------------------------------------------------------------------
     peak, peak_kind = measured_peaks()
-    ncols = pool[0].cols                                       # this rank's columns
+    ncols = pool.desc.cols if args.fresh else pool[0].cols     # this rank's columns
     strip = iht.strip_bytes(rows, p.planes, p.b_phi)
     copy_bytes = iht._lib.load().iht_qmat_bytes(rows, ncols, p.planes, p.b_phi)
+    if args.fresh:          # the adjoint streams the fp32 Phi (4 bytes per component), the forward s columns
+        copy_bytes = 4 * rows * ncols * p.planes
+        strip = 4 * rows * p.planes
     R = iht.vec_len(rows, p.planes)
     adj_bytes = copy_bytes + B * (4 * R + 4 * ncols)          # codes + r read + g write
     fwd_bytes = B * (p.s * strip + 4 * R + 4 * R)              # support strips + yhat + r
@@ -340,16 +350,19 @@ def main():
             "parallelism": (f"column-sharded x{world}" + (", NCCL all-reduce of r + all-gather of top-s candidates"
                                                           if world > 1 else "") if B > 1 else
                             f"row-sharded x{world}" + (", NCCL all-reduce of g per iteration" if world > 1 else "")),
-            "l2": f"inputs > L2: pool {p.K * copy_bytes / 2**30:.2f} GiB per GPU streamed from HBM"
-                  if p.K * copy_bytes > 126e6 else f"pool {p.K * copy_bytes / 2**20:.1f} MiB is L2-resident",
+            "l2": (lambda res: f"inputs > L2: {res / 2**30:.2f} GiB per GPU streamed from HBM" if res > 126e6
+                   else f"{res / 2**20:.1f} MiB is L2-resident")(copy_bytes if args.fresh else p.K * copy_bytes),
             "adjoint_variant": args.variant,
             "step": "adaptive mu-hat with accept/shrink loop (Algorithm 1, P:350-363)" if args.adaptive
                     else f"fixed mu = {p.mu:g}",
+            "copies": "fresh: drawn on the fly from the resident fp32 Phi, K = 2 n* (NEXT-2)" if args.fresh
+                      else f"pool of K = {p.K} stored quantised copies",
         },
         "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
                 "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},
         "roofline": roof if B > 1 else
-                    {"bound": "hbm", "kernel": "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
+                    {"bound": "hbm", "kernel": "adjoint_fresh_kernel (fp32 Phi + Philox, NEXT-2)" if args.fresh else
+                               "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
                      "achieved": adj_gbs, "peak": peak, "unit": "GB/s", "frac": adj_gbs / peak,
                      "peak_kind": peak_kind, "traffic": traffic,
                      "algorithmic_bytes_per_launch": adj_bytes, "avg_launch_ms": adj_avg,

@@ -235,6 +235,28 @@ IHT_API int iht_forward_fresh(const iht_fmat* F, int32_t copy_id, const int32_t*
                               const int32_t* x_nnz_dev, int32_t max_nnz, const float* yhat_dev, float* r_dev,
                               void* stream);
 
+/* ------------------------------------------ NEXT-3: radio Phi computed on the fly */
+/* Phi_{k,p} = exp(-2 pi i (u_k l_p + v_k m_p)) (BASELINE config 3, reading c16; paper
+ * "Computing Phi on the fly"): u, v = baseline / lambda per visibility k
+ * (device fp64 arrays of nvis), pixel p = row * grid + col with l = -1 + (2 row + 1)/grid,
+ * m = -1 + (2 col + 1)/grid.  No Phi bytes are read.  bits = 0: full precision; bits in
+ * {2,4,8}: each component stochastically rounded in registers with the Q-contract and
+ * Philox counter (p >> 2, row_offset + k, copy_id, plane << 8) -- the codes iht_quantize
+ * stores for copy_id, up to components whose on-the-fly fp32 value differs by an ulp
+ * across a rounding decision. */
+typedef struct {
+  int64_t nvis, row_offset;
+  int32_t grid, bits, level_mode, copy_id;
+  uint64_t seed;
+  float scale_c;        /* c of the quantiser (unit-modulus entries: 1)                  */
+  int32_t reserved;
+  const double* u;      /* device [nvis] */
+  const double* v;      /* device [nvis] */
+} iht_radio;
+/* g = Re(Phi^H r) (full precision) or Re(Phi-hat^H r) (bits > 0) for all grid^2 pixels;
+ * r: stacked vector of iht_vec_len(nvis, 2); g: grid^2 floats. */
+IHT_API int iht_adjoint_radio(const iht_radio* R, const float* r_dev, float* g_dev, void* stream);
+
 /* ---------------------------------------------------- (a6) update + H_s */
 /* a = x + mu g, then H_s: keep the s entries of largest |a|,
  * ties to the LOWEST index, zeros never kept (reading c15).  Output

@@ -42,6 +42,14 @@ class IhtFmat(ctypes.Structure):
     ]
 
 
+class IhtRadio(ctypes.Structure):
+    """Mirror of iht_radio (include/iht.h): the on-the-fly radio Phi (NEXT-3)."""
+    _fields_ = [
+        ("nvis", c_i64), ("row_offset", c_i64), ("grid", c_i32), ("bits", c_i32), ("level_mode", c_i32),
+        ("copy_id", c_i32), ("seed", c_u64), ("scale_c", c_f32), ("reserved", c_i32), ("u", c_vp), ("v", c_vp),
+    ]
+
+
 class IhtConfig(ctypes.Structure):
     """Mirror of iht_config (include/iht.h)."""
     _fields_ = [
@@ -82,6 +90,7 @@ SIGNATURES = {
     "iht_adjoint_fresh": (c_int, [ctypes.POINTER(IhtFmat), c_i32, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "iht_forward_fresh": (c_int, [ctypes.POINTER(IhtFmat), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "iht_solver_create_fresh": (c_int, [ctypes.POINTER(IhtFmat), ctypes.POINTER(IhtConfig), ctypes.POINTER(c_vp)]),
+    "iht_adjoint_radio": (c_int, [ctypes.POINTER(IhtRadio), c_vp, c_vp, c_vp]),
     "iht_threshold_batched_ws_bytes": (c_i64, [c_i64, c_i32, c_i32]),
     "iht_threshold_batched": (c_int, [c_vp, c_vp, c_vp, c_i32, c_vp, c_f32, c_i32, c_i64, c_i64, c_i32, c_vp, c_vp,
                                       c_i32, c_vp, c_vp, c_i64, c_vp]),

@@ -25,6 +25,7 @@
 // time (scripts/microbench/pipe_bench.cu: 8-MMA K-blocks with split A/B rings ran at
 // 105 clk per MMA, one ring with 16-MMA K-blocks at 74, back-to-back issue 64-68).  The
 // accumulators are double-buffered so the epilogue of tile t overlaps the MMAs of t+1.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "iht_internal.cuh"
@@ -123,6 +124,7 @@ struct BatchArgs {
   const int* Fb;           // [B] exponents
   const int* Sb;           // [B][2] limb sums
   float* g;                // [B][N]
+  long long* tlog;         // probe 32: per-CTA clock64 stamps [cta][64] (profiling only)
 };
 
 template <int BITS>
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   }
   __syncthreads();
 
+  if (a.tlog && threadIdx.x == 0) a.tlog[blockIdx.x * 64 + 63] = clock64();
   if (warp < 4) {
     // ---------------------------------------------------------------- converters
     const int n = warp * 32 + lane;              // pixel row inside the tile (0..127)
@@ -269,9 +272,11 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       const int ab = t & 1;
       if (t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t] = clock64();
       const uint32_t dtm = tmem + ab * acc_stride;
       for (int kb = 0; kb < a.nkb; ++kb) {
         mbar_wait2(smem_u32(&st_full[ss]), sph);
+        if (a.tlog && lane == 0 && t == 0 && kb < 16) a.tlog[blockIdx.x * 64 + 40 + kb] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           if (a.probe & 2) {                        // probe: no tensor work
@@ -301,6 +306,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         __syncwarp();
         if (++ss == ST) { ss = 0; sph ^= 1u; }
       }
+      if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t + 1] = clock64();
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- packed-code producer
@@ -377,6 +383,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive2(smem_u32(&acc_free[ab]));
+      if (a.tlog && warp == 7 && lane == 0 && t < 8) a.tlog[blockIdx.x * 64 + 32 + t] = clock64();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -551,6 +558,9 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     b.B = bp;
     b.Breal = nb;
     b.probe = probe_flags();
+    static long long* tlog = nullptr;
+    if ((b.probe & 32) && tlog == nullptr) cudaMalloc(&tlog, 1024 * 64 * sizeof(long long));
+    b.tlog = (b.probe & 32) ? tlog : nullptr;
     b.L = L;
     b.sigma = A->scale_c / (float)(L - 1);
     b.bimg = bimg;
@@ -576,6 +586,22 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     else if (A->bits == 4) IHT_BATCH(4);
     else IHT_BATCH(8);
 #undef IHT_BATCH
+    if (b.tlog) {   // profiling probe 32: per-CTA timeline of CTA 0 and the slowest CTA (stderr)
+      static long long h[1024 * 64];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, b.tlog, sizeof(long long) * 64 * min(b.ntiles, sms), cudaMemcpyDeviceToHost);
+      for (int c : {0, 1, 100}) {
+        if (c >= min(b.ntiles, sms)) continue;
+        const long long* r = h + c * 64;
+        const long long t0 = r[63];
+        fprintf(stderr, "cta %d:", c);
+        for (int t = 0; t < 4; ++t) fprintf(stderr, " tile%d mma [%lld, %lld] epi %lld;", t, r[2 * t] - t0, r[2 * t + 1] - t0,
+                                            r[32 + t] - t0);
+        fprintf(stderr, " kb-full(t0):");
+        for (int k = 0; k < min(nkb, 16); ++k) fprintf(stderr, " %lld", r[40 + k] - t0);
+        fprintf(stderr, "\n");
+      }
+    }
   }
   return IHT_OK;
 }

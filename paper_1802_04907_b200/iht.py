@@ -17,7 +17,7 @@ from ._lib import IhtConfig, IhtFmat, IhtQmat, check, load
 
 __all__ = ["absmax", "absmax_batched", "quantize", "quantize_rows", "quantize_vec", "quantize_vec_batched", "forward",
            "forward_batched", "adjoint", "adjoint_batched", "threshold", "threshold_batched", "merge_candidates",
-           "Solver", "solve", "Comm", "QCopy", "FreshPhi", "adjoint_fresh", "forward_fresh", "strip_bytes", "vec_len",
+           "Solver", "solve", "Comm", "QCopy", "FreshPhi", "adjoint_fresh", "forward_fresh", "adjoint_radio", "strip_bytes", "vec_len",
            "rows_pad"]
 
 
@@ -314,6 +314,20 @@ def forward_fresh(F, copy_id, x_idx, x_val, x_nnz, yhat, stream=None):
     check(load().iht_forward_fresh(ctypes.byref(F.desc), copy_id, _ptr(x_idx), _ptr(x_val), _ptr(x_nnz),
                                    x_idx.numel(), _ptr(yhat), _ptr(r), _stream(stream)), "iht_forward_fresh")
     return r
+
+
+def adjoint_radio(u, v, grid, r, bits=0, level_mode=0, seed=0, copy_id=0, scale_c=1.0, row_offset=0, stream=None):
+    """NEXT-3: g = Re(Phi^H r) with the radio Phi computed on the fly from u, v (float64 CUDA
+    tensors, baseline / lambda per visibility); bits > 0 quantises each entry in registers."""
+    _require_cuda(u, v, r)
+    from ._lib import IhtRadio
+    if u.dtype != torch.float64 or v.dtype != torch.float64:
+        raise ValueError("u, v must be float64")
+    d = IhtRadio(nvis=u.numel(), row_offset=row_offset, grid=grid, bits=bits, level_mode=level_mode,
+                 copy_id=copy_id, seed=seed, scale_c=float(scale_c), reserved=0, u=u.data_ptr(), v=v.data_ptr())
+    g = torch.empty(grid * grid, dtype=torch.float32, device=r.device)
+    check(load().iht_adjoint_radio(ctypes.byref(d), _ptr(r), _ptr(g), _stream(stream)), "iht_adjoint_radio")
+    return g
 
 
 class Comm:

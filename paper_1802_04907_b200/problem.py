@@ -113,3 +113,32 @@ def _build_pool_cols(p, rank, world, dev, dist_on):
     del phi
     torch.cuda.empty_cache()
     return pool, c, t, p.M, 0
+
+
+def build_fresh(p, rank, world, dev, dist_on):
+    """NEXT-2: this rank's row shard of the fp32 Phi resident on the device (config 4: generated
+    block-wise on the device, 64 GiB at one GPU), described for on-the-fly copies.  Returns
+    (FreshPhi, c_phi, preprocess timings, rows, row0)."""
+    import torch
+    from . import iht
+    rows, row0 = shard_rows(p.M, world, rank)
+    t = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if p.phi is None:
+        from workloads.gpu import gauss_fill
+        phi = torch.empty((rows, p.N), dtype=torch.float32, device=dev)
+        blk = max(256, ((2 << 30) // (p.N * 4)) // 256 * 256)
+        for r in range(0, rows, blk):
+            n = min(blk, rows - r)
+            gauss_fill(phi[r:r + n], p.phi_key, p.N, row0 + r, 0, p.phi_sd)
+    else:
+        phi = torch.from_numpy(np.ascontiguousarray(p.phi[row0:row0 + rows])).to(dev)
+    cmax = iht.absmax(phi)
+    if dist_on:
+        import torch.distributed as dist
+        dist.all_reduce(cmax, op=dist.ReduceOp.MAX)
+    c = float(cmax.item())
+    torch.cuda.synchronize()
+    t["gen_absmax_ms"] = (time.perf_counter() - t0) * 1e3
+    return iht.fresh_phi(phi, p.b_phi, 0, p.seed, c, row_offset=row0), c, t, rows, row0
