@@ -307,7 +307,8 @@ def main():
         roof = {"bound": "tensor", "kernel": "adjoint_batched_kernel (+ batched_limbs_kernel)",
                 "achieved": adj_ops / (adj_avg / 1e3) / 1e12, "peak": tpeak, "unit": "TOP/s",
                 "frac": adj_ops / (adj_avg / 1e3) / 1e12 / tpeak, "peak_kind": tpeak_kind,
-                "traffic": None, "algorithmic_ops_per_launch": adj_ops,
+                "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+                "algorithmic_ops_per_launch": adj_ops,
                 "executed_int8_ops_per_launch": 2 * adj_ops, "avg_launch_ms": adj_avg,
                 "launches_timed": len(adj_ms), "code_bytes_per_launch": copy_bytes,
                 "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside the "

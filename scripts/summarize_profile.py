@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise a gpurun profiling session into profiles/<tag>/summary.md.
 
-    python scripts/summarize_profile.py <tag> [--bench gpurun_out/<tag>_bench.json]
+    python scripts/summarize_profile.py <tag> [<outdir> <label> <bench.json>]
 
 Reads gpurun_out/<tag>_launches.csv (ncu --metrics gpu__time_duration.sum launch list)
 and gpurun_out/<tag>_adjoint.ncu-rep (ncu --set full of the adjoint), writes the
@@ -43,11 +43,12 @@ def ncu_raw(path):
 
 def main():
     tag = sys.argv[1]
-    outdir = os.path.join(ROOT, "profiles", tag)
+    outdir = os.path.join(ROOT, "profiles", sys.argv[2] if len(sys.argv) > 2 else tag)
+    label = sys.argv[3] if len(sys.argv) > 3 else "summary"
     os.makedirs(outdir, exist_ok=True)
     g = os.path.join(ROOT, "gpurun_out")
     lines = [f"# Profile summary {tag}", ""]
-    bench = os.path.join(g, f"{tag}_bench.json")
+    bench = sys.argv[4] if len(sys.argv) > 4 else os.path.join(g, f"{tag}_bench.json")
     b = None
     if os.path.exists(bench):
         try:
@@ -101,7 +102,7 @@ def main():
             dd[key] = traffic
             json.dump(dd, open(tp, "w"), indent=1)
             lines.append(f"traffic per launch (dram read+write): {traffic:.4g} B -> profiles/adjoint_traffic.json[{key}]")
-    open(os.path.join(outdir, "summary.md"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(outdir, f"{label}.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
