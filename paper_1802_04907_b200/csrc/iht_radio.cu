@@ -5,14 +5,13 @@
 //   config 3, reading c16), pixel p = row * grid + col, l = centre(row), m = centre(col),
 //   centre(i) = -1 + (2 i + 1) / grid.
 //
-// The phase in turns tau = u l + v m is formed in fp64 (B200 keeps a full-rate-ish FP64
-// pipe) and reduced to its fractional part, then cos / sin come from sincospif in fp32: the
-// entries agree with the stored complex64 Phi (computed in fp64 and rounded) to ~1 ulp.
+// The phase in turns tau = u l + v m is formed in fp64 (B200 keeps a strong FP64 pipe) and
+// reduced to its fractional part; cos / sin come from fp64 sincospi rounded to fp32, i.e.
+// the entries of the stored complex64 Phi (computed in fp64 and rounded).
 // With bits > 0 every component is stochastically rounded in registers exactly as
 // iht_quantize would (Q-contract, Philox counter (p >> 2, row_offset + k, copy, plane << 8)),
-// so the on-the-fly quantised adjoint equals the stored-copy adjoint except for the (rare)
-// components whose fp32 value differs by an ulp across a rounding decision.  Zero bytes of
-// Phi are read: the kernel is ALU/SFU-bound.
+// so the on-the-fly quantised adjoint uses the stored copy's codes.  Zero bytes of Phi are
+// read: the kernel is FP64/ALU-bound.
 #include "iht_internal.cuh"
 
 namespace iht {
@@ -33,13 +32,15 @@ struct RadioArgs {
   float* g;
 };
 
-// e^{-2 pi i tau}: (cos, -sin) of the fractional turn, sincospif in fp32.
+// e^{-2 pi i tau}: (cos, -sin) of the fractional turn by fp64 sincospi, rounded to fp32 --
+// the same values as the stored complex64 Phi (fp64 exp rounded to complex64) except in
+// vanishingly rare double-rounding cases, so the in-register codes match stored copies.
 __device__ __forceinline__ void phi_entry(double tau, float* re, float* im) {
-  const double fr = tau - rint(tau);            // in [-1/2, 1/2]
-  float s, c;
-  sincospif(2.0f * (float)fr, &s, &c);
-  *re = c;
-  *im = -s;
+  const double fr = tau - rint(tau);            // in [-1/2, 1/2], exact
+  double s, c;
+  sincospi(2.0 * fr, &s, &c);
+  *re = (float)c;
+  *im = (float)(-s);
 }
 
 template <bool QUANT>

@@ -822,6 +822,11 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
     // more, smaller slices while that keeps <= 1 CTA per SM and >= 4096 a-values per CTA
     // (measured: 2 CTAs per SM or clusters of 16 are slower -- more cluster barriers)
     while (CL < kClusterMax && (int64_t)CL * 2 * nrhs <= 148 && N / (2 * CL) >= 4096) CL *= 2;
+    {
+      static int cl_env = -1;                        // profiling override (IHT_THR_CL = 1, 2, 4, 8)
+      if (cl_env < 0) cl_env = getenv("IHT_THR_CL") ? atoi(getenv("IHT_THR_CL")) : 0;
+      if (cl_env > 0 && (int64_t)cl_env * kClusterSlice >= N) CL = cl_env;
+    }
     const int slice = (int)(((N + CL - 1) / CL + 31) / 32 * 32);   // 16-byte aligned slices
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(CL, nrhs);

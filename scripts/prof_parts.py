@@ -41,6 +41,13 @@ if which in ("all", "c5"):
     G = torch.randn(B, N, device='cuda')
     print(f"c5 forward_batched   {timeit(lambda: iht.forward_batched(F, xi, xv, nz, yh)):.1f} us")
     print(f"c5 threshold_batched {timeit(lambda: iht.threshold_batched(xi, xv, nz, G, 1e-3, s)):.1f} us")
+if which in ("all", "c2"):
+    N, s = 16384, 128
+    xi = torch.from_numpy(np.sort(rng.choice(N, s, replace=False)).astype(np.int32)).cuda()
+    xv = torch.randn(s, device='cuda')
+    nz = torch.full((1,), s, dtype=torch.int32, device='cuda')
+    g = torch.randn(N, device='cuda')
+    print(f"c2 threshold         {timeit(lambda: iht.threshold(xi, xv, nz, g, 1.0, s)):.1f} us")
 if which in ("all", "c4"):
     M, N, s = 65536, 262144, 1024
     (F,) = [iht.new_copy(M, N, 1, 4, 0, 77, 0, 1.0, device='cuda')]
