@@ -17,13 +17,13 @@
 // K order inside a 16-byte u8 chunk is permuted (row(p) below) identically on A and B.
 //
 // Roles per CTA (320 threads): warps 0-3 expand packed codes -> u8 A stages in TMEM
-// (tcgen05.st), meet at a named barrier and thread 0 issues the K-block's MMAs; warp 4
-// bulk-copies the packed codes (own ring of slots), warp 5 the r-limb image; warps 6-9 run
-// the epilogue.  A (TMEM) and B (shared memory) share one stage ring, freed by ONE
-// tcgen05.commit per K-block; a K-block is 16 MMAs (2/4-bit).  Handoffs cost MMA-pipe
-// time (scripts/microbench/pipe_bench.cu: 8-MMA K-blocks with split A/B rings and a
-// separate MMA warp ran at 105 clk per MMA, back-to-back issue at 64-68; the in-kernel
-// timeline probe showed the separate MMA warp's chain at ~1700 clk per K-block).  The
+// (tcgen05.st); warp 4 issues the MMAs (one thread); warp 5 bulk-copies the packed codes
+// (own ring of slots), warp 6 the r-limb image; warps 7-10 run the epilogue.
+// A (TMEM) and B (shared memory) share ONE stage ring: a stage is full when the 4 converter
+// warps and the limb producer (with its bulk-copy bytes) have arrived, and free after ONE
+// tcgen05.commit per K-block; a K-block is 16 MMAs (2/4-bit).  Each handoff costs MMA-pipe
+// time (scripts/microbench/pipe_bench.cu: 8-MMA K-blocks with split A/B rings ran at
+// 105 clk per MMA, one ring with 16-MMA K-blocks at 74, back-to-back issue 64-68).  The
 // accumulators are double-buffered so the epilogue of tile t overlaps the MMAs of t+1.
 #include <stdio.h>
 #include <stdlib.h>
@@ -33,7 +33,7 @@
 namespace iht {
 
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
-constexpr int kBThreads = 320;         // 10 warps (roles above)
+constexpr int kBThreads = 352;         // 11 warps (roles above)
 
 // Per bit width: tile-steps (512/b rows, 1 KiB of a 16-column tile) per K-block, so that a
 // K-block is 16 MMAs (K = 32 each) at 2 and 4 bits and 8 at 8 bits; A stages fill the 256
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   uint64_t* bar = reinterpret_cast<uint64_t*>(sP + PKS * PK);
   uint64_t* pk_full = bar;                        // [PKS]  tx
   uint64_t* pk_free = pk_full + kPkSlotsMax;      // [PKS]  4 converter warps
-  uint64_t* st_full = pk_free + kPkSlotsMax;      // [ST]   B producer (+ tx): the limb stage landed
+  uint64_t* st_full = pk_free + kPkSlotsMax;      // [ST]   4 converter warps + B producer (+ tx)
   uint64_t* st_free = st_full + kStagesMax;       // [ST]   one tcgen05.commit per K-block
   uint64_t* acc_full = st_free + kStagesMax;      // [2]    tcgen05.commit
   uint64_t* acc_free = acc_full + 2;              // [2]    4 epilogue warps
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       mbar_init2(smem_u32(&pk_free[i]), 4);
     }
     for (int i = 0; i < ST; ++i) {
-      mbar_init2(smem_u32(&st_full[i]), 1);
+      mbar_init2(smem_u32(&st_full[i]), 5);
       mbar_init2(smem_u32(&st_free[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {   // TMEM (warp 4 allocates and frees): 2 accumulators (<= 128 columns each) + ST A stages
+  if (warp == 4) {   // TMEM: 2 accumulator buffers (NB <= 128 columns each) + ST A stages
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512)
                  : "memory");
@@ -186,88 +186,100 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
 
   if (a.tlog && threadIdx.x == 0) a.tlog[blockIdx.x * 64 + 63] = clock64();
   if (warp < 4) {
-    // ------------------------------------------- converters + MMA issue (thread 0)
-    // The four converter warps expand the K-block's codes into the A stage (TMEM), meet at
-    // a named barrier, and thread 0 issues the MMAs at once: the A handoff costs no
-    // mbarrier round trip (measured: the commit -> wake -> arrive -> wake -> issue chain of
-    // a separate MMA warp took ~1700 clk per K-block, longer than the K-block's 16 MMAs).
+    // ---------------------------------------------------------------- converters
     const int n = warp * 32 + lane;              // pixel row inside the tile (0..127)
     const int ct = n >> 4, cc = n & 15;           // column tile / column inside the tile
-    const uint32_t idesc = idesc_i8(kBT, NB);
     int ps = 0, ss = 0;
     uint32_t pph = 0, sph = 0;
     bool s_wrapped = false;
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      for (int kb = 0; kb < a.nkb; ++kb) {
+        if (a.probe & 8) {                        // probe: hand the A stage over untouched
+          if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
+          __syncwarp();
+          if (lane == 0) mbar_arrive2(smem_u32(&st_full[ss]));
+          if (++ss == ST) { ss = 0; sph ^= 1u; s_wrapped = true; }
+          continue;
+        }
+        const int tsn = min(TS, a.ksteps - kb * TS);   // tile-steps present (ragged last K-block)
+        mbar_wait2(smem_u32(&pk_full[ps]), pph);
+        if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
+        const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
+        // one tile-step at a time: 64 packed bytes of this pixel -> 512/b u8 codes -> TMEM
+#pragma unroll 1
+        for (int ts = 0; ts < TS; ++ts) {
+          constexpr int OW = 512 / BITS / 4;        // u32 outputs per tile-step (64, 32 or 16)
+          uint32_t out[OW];
+          if (ts < tsn) {
+            const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;
+            const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
+                                 reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
+            const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
+                                    w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
+#pragma unroll
+            for (int q = 0; q < OW / 4; ++q) {       // 16-byte chunk q of this tile-step
+              if (BITS == 2) {            // chunk = packed word q (16 codes)
+                const uint32_t x = w[q];
+                out[4 * q + 0] = x & 0x03030303u;
+                out[4 * q + 1] = (x >> 2) & 0x03030303u;
+                out[4 * q + 2] = (x >> 4) & 0x03030303u;
+                out[4 * q + 3] = (x >> 6) & 0x03030303u;
+              } else if (BITS == 4) {     // chunk = packed words 2q, 2q+1
+                const uint32_t x0 = w[2 * q], x1 = w[2 * q + 1];
+                out[4 * q + 0] = x0 & 0x0F0F0F0Fu;
+                out[4 * q + 1] = (x0 >> 4) & 0x0F0F0F0Fu;
+                out[4 * q + 2] = x1 & 0x0F0F0F0Fu;
+                out[4 * q + 3] = (x1 >> 4) & 0x0F0F0F0Fu;
+              } else {                    // chunk = packed words 4q..4q+3 (bytes)
+                out[4 * q + 0] = w[4 * q];
+                out[4 * q + 1] = w[4 * q + 1];
+                out[4 * q + 2] = w[4 * q + 2];
+                out[4 * q + 3] = w[4 * q + 3];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < OW; ++q) out[q] = 0u;   // past the strip: code 0 (zero limbs anyway)
+          }
+          if (!(a.probe & 4)) {
+#pragma unroll
+            for (int c0 = 0; c0 < OW; c0 += 8)
+              asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                               ta + (uint32_t)(ts * OW + c0)),
+                           "r"(out[c0]), "r"(out[c0 + 1]), "r"(out[c0 + 2]), "r"(out[c0 + 3]), "r"(out[c0 + 4]),
+                           "r"(out[c0 + 5]), "r"(out[c0 + 6]), "r"(out[c0 + 7])
+                           : "memory");
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));     // packed slot consumed
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive2(smem_u32(&st_full[ss]));
+        if (++ps == PKS) { ps = 0; pph ^= 1u; }
+        if (++ss == ST) { ss = 0; sph ^= 1u; s_wrapped = true; }
+      }
+    }
+    (void)CH;
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = idesc_i8(kBT, NB);
+    int ss = 0;
+    uint32_t sph = 0;
     int t = 0;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
       const int ab = t & 1;
+      if (t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t] = clock64();
       const uint32_t dtm = tmem + ab * acc_stride;
-      if (a.tlog && threadIdx.x == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t] = clock64();
       for (int kb = 0; kb < a.nkb; ++kb) {
-        if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);   // A stage ss (and B) reusable
-        if (!(a.probe & 8)) {
-          const int tsn = min(TS, a.ksteps - kb * TS);   // tile-steps present (ragged last K-block)
-          mbar_wait2(smem_u32(&pk_full[ps]), pph);
-          const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
-          // one tile-step at a time: 64 packed bytes of this pixel -> 512/b u8 codes -> TMEM
-#pragma unroll 1
-          for (int ts = 0; ts < TS; ++ts) {
-            constexpr int OW = 512 / BITS / 4;        // u32 outputs per tile-step (64, 32 or 16)
-            uint32_t out[OW];
-            if (ts < tsn) {
-              const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;
-              const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
-                                   reinterpret_cast<const uint4*>(src)[2], reinterpret_cast<const uint4*>(src)[3]};
-              const uint32_t w[16] = {w4[0].x, w4[0].y, w4[0].z, w4[0].w, w4[1].x, w4[1].y, w4[1].z, w4[1].w,
-                                      w4[2].x, w4[2].y, w4[2].z, w4[2].w, w4[3].x, w4[3].y, w4[3].z, w4[3].w};
-#pragma unroll
-              for (int q = 0; q < OW / 4; ++q) {       // 16-byte chunk q of this tile-step
-                if (BITS == 2) {            // chunk = packed word q (16 codes)
-                  const uint32_t x = w[q];
-                  out[4 * q + 0] = x & 0x03030303u;
-                  out[4 * q + 1] = (x >> 2) & 0x03030303u;
-                  out[4 * q + 2] = (x >> 4) & 0x03030303u;
-                  out[4 * q + 3] = (x >> 6) & 0x03030303u;
-                } else if (BITS == 4) {     // chunk = packed words 2q, 2q+1
-                  const uint32_t x0 = w[2 * q], x1 = w[2 * q + 1];
-                  out[4 * q + 0] = x0 & 0x0F0F0F0Fu;
-                  out[4 * q + 1] = (x0 >> 4) & 0x0F0F0F0Fu;
-                  out[4 * q + 2] = x1 & 0x0F0F0F0Fu;
-                  out[4 * q + 3] = (x1 >> 4) & 0x0F0F0F0Fu;
-                } else {                    // chunk = packed words 4q..4q+3 (bytes)
-                  out[4 * q + 0] = w[4 * q];
-                  out[4 * q + 1] = w[4 * q + 1];
-                  out[4 * q + 2] = w[4 * q + 2];
-                  out[4 * q + 3] = w[4 * q + 3];
-                }
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < OW; ++q) out[q] = 0u;   // past the strip: code 0 (zero limbs anyway)
-            }
-            if (!(a.probe & 4)) {
-#pragma unroll
-              for (int c0 = 0; c0 < OW; c0 += 8)
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                                 ta + (uint32_t)(ts * OW + c0)),
-                             "r"(out[c0]), "r"(out[c0 + 1]), "r"(out[c0 + 2]), "r"(out[c0 + 3]), "r"(out[c0 + 4]),
-                             "r"(out[c0 + 5]), "r"(out[c0 + 6]), "r"(out[c0 + 7])
-                             : "memory");
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive2(smem_u32(&pk_free[ps]));     // packed slot consumed
-          if (++ps == PKS) { ps = 0; pph ^= 1u; }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");                 // the A stage is complete
-        if (threadIdx.x == 0) {
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (kb == 0 && t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
-          mbar_wait2(smem_u32(&st_full[ss]), sph);                   // B stage ss landed
-          if (a.tlog && t == 0 && kb < 16) a.tlog[blockIdx.x * 64 + 40 + kb] = clock64();
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (a.probe & 2) {                                          // probe: no tensor work
+        mbar_wait2(smem_u32(&st_full[ss]), sph);
+        if (a.tlog && lane == 0 && t == 0 && kb < 16) a.tlog[blockIdx.x * 64 + 40 + kb] = clock64();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          if (a.probe & 2) {                        // probe: no tensor work
             mbar_arrive2(smem_u32(&st_free[ss]));
             if (kb == a.nkb - 1) mbar_arrive2(smem_u32(&acc_full[ab]));
           } else {
@@ -291,11 +303,12 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                            : "memory");
           }
         }
-        if (++ss == ST) { ss = 0; sph ^= 1u; s_wrapped = true; }
+        __syncwarp();
+        if (++ss == ST) { ss = 0; sph ^= 1u; }
       }
-      if (a.tlog && threadIdx.x == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t + 1] = clock64();
+      if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t + 1] = clock64();
     }
-  } else if (warp == 4) {
+  } else if (warp == 5) {
     // ---------------------------------------------------------------- packed-code producer
     // lanes 0-7 each copy one column tile's tile-steps of the K-block (contiguous in the
     // tiled layout), so the 8 requests of a slot are issued in parallel
@@ -320,7 +333,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         if (++ps == PKS) { ps = 0; ph ^= 1u; wrapped = true; }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 6) {
     // ---------------------------------------------------------------- r-limb (B) producer
     int ss = 0;
     uint32_t sph = 0;
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 6-9)
+    // ---------------------------------------------------------------- epilogue (warps 7-10)
     const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
     int t = 0;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
@@ -370,7 +383,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive2(smem_u32(&acc_free[ab]));
-      if (a.tlog && warp == 6 && lane == 0 && t < 8) a.tlog[blockIdx.x * 64 + 32 + t] = clock64();
+      if (a.tlog && warp == 7 && lane == 0 && t < 8) a.tlog[blockIdx.x * 64 + 32 + t] = clock64();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
