@@ -320,7 +320,9 @@ typedef struct {
   uint64_t seed;        /* quantiser key for y-hat                                       */
   int32_t trace;        /* 1: keep every iterate x^[n] (see iht_solver_trace)            */
   int32_t use_graph;    /* 1: capture the n_iter loop into one CUDA graph (default)      */
-  iht_comm* comm;       /* NULL: single GPU; else g is all-reduced (sum) every iteration */
+  iht_comm* comm;       /* NULL: single GPU; else the rows are sharded (single observation:
+                           c_y max- and g sum-all-reduced every iteration) or the columns
+                           (batched); world 1 runs the same collectives on one rank      */
   int32_t profile;      /* 1: record a CUDA event pair around every adjoint launch      */
   int32_t nrhs;         /* B independent observations sharing Phi (BASELINE config 5);
                            0 or 1: one observation.  B > 1 runs the batched path: sparse

@@ -38,6 +38,9 @@ constexpr int kBThreads = 352;         // 11 warps (roles above)
 // Per bit width: tile-steps (512/b rows, 1 KiB of a 16-column tile) per K-block, so that a
 // K-block is 16 MMAs (K = 32 each) at 2 and 4 bits and 8 at 8 bits; A stages fill the 256
 // TMEM columns left by the two accumulators; B stages take 128 KiB of shared memory.
+// Measured (in-kernel timeline probe, config 5): every K-block handoff costs the MMA pipe
+// ~300-400 clk whatever the depth, so fewer, larger K-blocks win: 2 stages x 16 MMAs ran
+// at 87 clk per MMA (MMA-only), 4 stages x 8 MMAs at 100, against 64 back to back.
 template <int BITS> struct BCfg {
   static constexpr int TS = BITS == 8 ? 4 : BITS;       // tile-steps per K-block
   static constexpr int KBR = TS * 512 / BITS;           // rows (= u8 bytes per pixel row) per K-block
@@ -125,6 +128,7 @@ struct BatchArgs {
   const int* Sb;           // [B][2] limb sums
   float* g;                // [B][N]
   long long* tlog;         // probe 32: per-CTA clock64 stamps [cta][64] (profiling only)
+  int ep32;                // 1: the integer epilogue fits int32 (Rpad (L-1) < 21700), else fp64
 };
 
 template <int BITS>
@@ -149,6 +153,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   float* ep_scale = reinterpret_cast<float*>(tmem_slot + 4);            // [B] sigma 2^-F_b
   long long* ep_off = reinterpret_cast<long long*>(ep_scale + 256);    // [B] (L-1) S_b
+  int* ep_off32 = reinterpret_cast<int*>(ep_off + 256);                // [B] same, int32 path
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -181,6 +186,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
     ep_scale[b] = a.sigma * ldexpf(1.0f, -a.Fb[b]);
     ep_off[b] = (long long)(a.L - 1) * ((long long)a.Sb[2 * b] + 256ll * a.Sb[2 * b + 1]);
+    ep_off32[b] = (int)ep_off[b];
   }
   __syncthreads();
 
@@ -278,20 +284,31 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         mbar_wait2(smem_u32(&st_full[ss]), sph);
         if (a.tlog && lane == 0 && t == 0 && kb < 16) a.tlog[blockIdx.x * 64 + 40 + kb] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // warp-uniform operands (shuffled from lane 0 so the compiler keeps them uniform)
+        const uint32_t atm_u = __shfl_sync(0xffffffffu, tmem + a_col0 + (uint32_t)(ss * ACOLS), 0);
+        const uint32_t bbase_u = __shfl_sync(0xffffffffu, smem_u32(sB + ss * BSZ), 0);
+        const uint32_t dtm_u = __shfl_sync(0xffffffffu, dtm, 0);
+        const uint32_t idesc_u = __shfl_sync(0xffffffffu, idesc, 0);
+        const uint32_t acc0_u = __shfl_sync(0xffffffffu, kb > 0 ? 1u : 0u, 0);
+        const uint32_t nb128_u = __shfl_sync(0xffffffffu, (uint32_t)NB * 128u, 0);
         if (lane == 0) {
           if (a.probe & 2) {                        // probe: no tensor work
             mbar_arrive2(smem_u32(&st_free[ss]));
             if (kb == a.nkb - 1) mbar_arrive2(smem_u32(&acc_full[ab]));
           } else {
-            const uint32_t atm = tmem + a_col0 + (uint32_t)(ss * ACOLS), bbase = smem_u32(sB + ss * BSZ);
+            // base descriptor / TMEM address once per K-block; the per-MMA K offsets are added
+            // to the descriptor's 14-bit start-address field (no carry: stages < 256 KiB), so
+            // the 16 issues stay on uniform registers instead of a broadcast per MMA
+            const uint64_t bd0 = sw128_desc(bbase_u);
+            const uint32_t nb128 = nb128_u;
 #pragma unroll
             for (int kk = 0; kk < NKS; ++kk) {
-              const uint64_t bd = sw128_desc(bbase + (kk >> 2) * (NB * 128) + (kk & 3) * 32);
-              const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+              const uint64_t bd = bd0 + (uint64_t)(((uint32_t)(kk >> 2) * nb128 + (uint32_t)(kk & 3) * 32u) >> 4);
+              const uint32_t acc = kk > 0 ? 1u : acc0_u;
               asm volatile(
                   "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtm),
-                  "r"(atm + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc), "r"(acc)
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtm_u),
+                  "r"(atm_u + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc_u), "r"(acc)
                   : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -372,11 +389,21 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
             : "r"(taddr + (uint32_t)c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (n < a.N) {
+          // g = sigma 2^-F (2 (D0 + 256 D1) - (L-1) S): exact integers, then one rounding
+          if (a.ep32) {
 #pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            const int b = (c0 + e) >> 1;
-            const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
-            if (b < a.Breal) a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
+            for (int e = 0; e < 16; e += 2) {
+              const int b = (c0 + e) >> 1;
+              const int W = 2 * ((int)v[e] + (int)v[e + 1] * 256) - ep_off32[b];
+              if (b < a.Breal) a.g[(int64_t)b * a.N + n] = __fmul_rn(__int2float_rn(W), ep_scale[b]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              const int b = (c0 + e) >> 1;
+              const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
+              if (b < a.Breal) a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
+            }
           }
         }
       }
@@ -488,7 +515,7 @@ static size_t batched_smem(int bits, int B) {
   const size_t pk = bits == 2 ? (size_t)BCfg<2>::PK * BCfg<2>::PKSLOTS
                   : bits == 4 ? (size_t)BCfg<4>::PK * BCfg<4>::PKSLOTS : (size_t)BCfg<8>::PK * BCfg<8>::PKSLOTS;
   return 1024 + (size_t)ST * 2 * B * KBB + pk + (size_t)(2 * kPkSlotsMax + 2 * kStagesMax + 4) * 8 + 16 +
-         256 * 4 + 256 * 8;
+         256 * 4 + 256 * 8 + 256 * 4;
 }
 
 }  // namespace iht
@@ -558,6 +585,7 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     b.B = bp;
     b.Breal = nb;
     b.probe = probe_flags();
+    b.ep32 = (double)Rpad * (L - 1) < 21700.0 ? 1 : 0;    // 771 Rpad (L-1) 128 < 2^31
     static long long* tlog = nullptr;
     if ((b.probe & 32) && tlog == nullptr) cudaMalloc(&tlog, 1024 * 64 * sizeof(long long));
     b.tlog = (b.probe & 32) ? tlog : nullptr;

@@ -448,7 +448,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->batched = batched;
   S->world = world;
   S->rank = cfg->comm ? cfg->comm->rank : 0;
-  S->rowshard = !batched && world > 1;
+  S->rowshard = !batched && cfg->comm != nullptr;  // any world size (world 1 exercises the same path)
   S->colshard = batched && cfg->comm != nullptr;   // any world size (world 1 exercises the same path)
   // NCCL kernels may not sit inside a conditional body graph: the adaptive row-sharded
   // run drives its shrink loop from the host

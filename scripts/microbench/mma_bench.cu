@@ -17,14 +17,15 @@ __host__ __device__ constexpr uint32_t idesc(int kind, int M, int N) {
                    : ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24));
 }
 
-template <int KIND, bool ATMEM, int N, int GROUP, bool WAIT>
+template <int KIND, bool ATMEM, int N, int GROUP, bool WAIT, bool SPREAD = false>
 __global__ void __launch_bounds__(128, 1) bench(int iters, long long* cyc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem)[i] = SPREAD ? (i * 2654435761u) : 0u;   // random bytes vs zeros
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(&bar)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -45,12 +46,14 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long* cyc) {
     for (int it = 0; it < iters; it += GROUP) {
 #pragma unroll
       for (int g = 0; g < GROUP; ++g) {
-        const int kk = g & 3;
-        const uint64_t bd = sw128_desc(bbase + kk * 32);
+        const int kk = SPREAD ? (g & 15) : (g & 3);
+        // SPREAD: like adjoint_batched_kernel, 16 distinct 32-byte K slices over 4 SW128 atoms of a
+        // 128-row B stage (16 KiB apart), A from 16 distinct TMEM column groups
+        const uint64_t bd = sw128_desc(bbase + (SPREAD ? (kk >> 2) * 16384 + (kk & 3) * 32 : kk * 32));
         const uint32_t acc = (it + g) > 0 ? 1u : 0u;
 #define MMA_T(K) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t" \
                        "tcgen05.mma.cta_group::1.kind::" K " [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem), \
-                       "r"(tmem + 256 + (uint32_t)(kk * 8)), "l"(bd), "r"(id), "r"(acc) : "memory")
+                       "r"(tmem + 256 + (uint32_t)((kk * 8) & 255)), "l"(bd), "r"(id), "r"(acc) : "memory")
 #define MMA_S(K) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t" \
                        "tcgen05.mma.cta_group::1.kind::" K " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem), "l"(ad), "l"(bd), \
                        "r"(id), "r"(acc) : "memory")
@@ -78,12 +81,12 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long* cyc) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int KIND, bool ATMEM, int N, int GROUP, bool WAIT>
+template <int KIND, bool ATMEM, int N, int GROUP, bool WAIT, bool SPREAD = false>
 void run(const char* name, int sms) {
   const int iters = 8192;
   long long* d;
   cudaMalloc(&d, sms * sizeof(long long));
-  auto k = bench<KIND, ATMEM, N, GROUP, WAIT>;
+  auto k = bench<KIND, ATMEM, N, GROUP, WAIT, SPREAD>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   k<<<sms, 128, 100 * 1024>>>(iters, d);
   cudaEvent_t e0, e1;
@@ -102,7 +105,7 @@ void run(const char* name, int sms) {
   mean /= sms;
   const int K = KIND == 0 ? 32 : 16;
   const double macs = (double)sms * iters * 128.0 * N * K;
-  printf("%-40s %s  %.1f clk/MMA  %.3f ms  %.1f T(MAC*2)/s\n", name, cudaGetErrorString(err), mean / iters, ms,
+  fprintf(stderr, "%-45s %s  %.1f clk/MMA  %.3f ms  %.1f T(MAC*2)/s\n", name, cudaGetErrorString(err), mean / iters, ms,
          2.0 * macs / (ms * 1e-3) / 1e12);
   cudaFree(d);
 }
@@ -120,5 +123,7 @@ int main() {
   run<0, true, 128, 8, true>("i8 A=TMEM N=128 commit+wait every 8", sms);
   run<0, true, 128, 32, true>("i8 A=TMEM N=128 commit+wait every 32", sms);
   run<0, true, 128, 8, false>("i8 A=TMEM N=128 commit every 8", sms);
+  run<0, true, 128, 64, false, true>("i8 A=TMEM N=128 spread operands, random B", sms);
+  run<0, false, 128, 64, false, true>("i8 A=SMEM N=128 spread operands, random B", sms);
   return 0;
 }

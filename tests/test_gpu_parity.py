@@ -331,3 +331,25 @@ def test_solver_host_io_and_determinism():
     torch.cuda.synchronize()
     assert torch.equal(di.cpu(), oi) and torch.equal(dv.cpu(), ov)
     sol.close()
+
+
+def test_solver_world1_row_shard_path():
+    """The row-sharded code path (c_y max-all-reduce, g sum-all-reduce through NCCL, and the
+    host-driven shrink loop of the adaptive step) at world size 1 gives bit-identical results
+    to the plain run."""
+    p = CASES["gauss8bit"]()
+    c = OQ.scale_c(p.phi)
+    pool = _pool(p.phi, p.b_phi, p.K, c, p.seed)
+    comm = iht.Comm(0, 1, 0)
+    try:
+        for adaptive in (False, True):
+            ref = iht.Solver(pool, p.s, 12, p.mu, p.b_y, p.seed, adaptive=adaptive)
+            ri, rv, rn = [t.cpu().clone() for t in ref.run(_to_dev(p.y))]
+            sol = iht.Solver(pool, p.s, 12, p.mu, p.b_y, p.seed, comm=comm, adaptive=adaptive)
+            gi, gv, gn = sol.run(_to_dev(p.y))
+            torch.cuda.synchronize()
+            assert torch.equal(gi.cpu(), ri) and torch.equal(gv.cpu(), rv) and torch.equal(gn.cpu(), rn)
+            sol.close()
+            ref.close()
+    finally:
+        comm.close()
