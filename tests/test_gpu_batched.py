@@ -311,3 +311,18 @@ def test_batched_solver_world1_column_shard_path():
     finally:
         comm.close()
     ref.close()
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_adjoint_batched_odd_level_mode(bits):
+    """Odd level mode (2^{b-1}+1 levels, exact zero) on the tcgen05 path."""
+    M, N, B = 700, 333, 16
+    phi = _phi(M, N, True, seed=bits)
+    c = OQ.scale_c(phi)
+    (A,) = iht.quantize(_to_dev(phi), bits, 1, SEED, [9], float(c))
+    Ad = OQ.dequantize(OQ.quantize_matrix(phi, bits, 1, SEED, 9, c=c)[0], c, bits, 1)
+    rng = np.random.default_rng(bits)
+    R = np.stack([stack(rng.standard_normal(M) + 1j * rng.standard_normal(M), M) for _ in range(B)]).astype(np.float32)
+    Gm = iht.adjoint_batched(A, _to_dev(R)).cpu().numpy()
+    for b in range(B):
+        assert rel_l2(Gm[b], OI.adjoint(Ad, unstack(R[b], M, 2))) < TOL_T
