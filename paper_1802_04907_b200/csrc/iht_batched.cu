@@ -209,13 +209,9 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         }
         const int tsn = min(TS, a.ksteps - kb * TS);   // tile-steps present (ragged last K-block)
         mbar_wait2(smem_u32(&pk_full[ps]), pph);
-        if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
-        const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
-        // one tile-step at a time: 64 packed bytes of this pixel -> 512/b u8 codes -> TMEM
-#pragma unroll 1
-        for (int ts = 0; ts < TS; ++ts) {
-          constexpr int OW = 512 / BITS / 4;        // u32 outputs per tile-step (64, 32 or 16)
-          uint32_t out[OW];
+        constexpr int OW = 512 / BITS / 4;        // u32 outputs per tile-step (64, 32 or 16)
+        // one tile-step: 64 packed bytes of this pixel -> 512/b u8 codes (registers)
+        auto convert = [&](int ts, uint32_t* out) {
           if (ts < tsn) {
             const uint8_t* src = sP + ps * PK + ct * (TS * 1024) + ts * 1024 + cc * 64;
             const uint4 w4[4] = {reinterpret_cast<const uint4*>(src)[0], reinterpret_cast<const uint4*>(src)[1],
@@ -247,6 +243,9 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
 #pragma unroll
             for (int q = 0; q < OW; ++q) out[q] = 0u;   // past the strip: code 0 (zero limbs anyway)
           }
+        };
+        const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
+        auto store = [&](int ts, const uint32_t* out) {
           if (!(a.probe & 4)) {
 #pragma unroll
             for (int c0 = 0; c0 < OW; c0 += 8)
@@ -255,6 +254,19 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                            "r"(out[c0]), "r"(out[c0 + 1]), "r"(out[c0 + 2]), "r"(out[c0 + 3]), "r"(out[c0 + 4]),
                            "r"(out[c0 + 5]), "r"(out[c0 + 6]), "r"(out[c0 + 7])
                            : "memory");
+          }
+        };
+        {
+          // the first tile-step is converted BEFORE waiting for the stage to be free, so only
+          // the stores sit on the MMA -> converter -> MMA handoff chain
+          uint32_t out[OW];
+          convert(0, out);
+          if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
+          store(0, out);
+#pragma unroll 1
+          for (int ts = 1; ts < TS; ++ts) {
+            convert(ts, out);
+            store(ts, out);
           }
         }
         __syncwarp();
