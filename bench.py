@@ -301,6 +301,15 @@ def main():
     adj_avg = statistics.mean(adj_ms)
     adj_gbs = adj_bytes / (adj_avg / 1e3) / 1e9
     stream_gbs = iter_bytes * iters / (ms / 1e3) / 1e9     # per GPU
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "adjoint_traffic.json")
+    if os.path.exists(tp):
+        try:
+            d = json.load(open(tp))
+            key = f"{p.name}:b{p.b_phi}:gpus{world}:v{args.variant}"
+            traffic = d.get(key)
+        except Exception:
+            traffic = None
     if B > 1:   # (a7) tensor-core bound: algorithmic int8 ops 2 R N B (one multiply-add per code per snapshot)
         tpeak, tpeak_kind = measured_tensor_peak_int8()
         adj_ops = 2.0 * R * ncols * B
@@ -313,15 +322,6 @@ def main():
                 "launches_timed": len(adj_ms), "code_bytes_per_launch": copy_bytes,
                 "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside the "
                        "solver graph, last timed step; ops = 2 R N B useful (x2 executed: two int8 limbs of r)"}
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "adjoint_traffic.json")
-    if os.path.exists(tp):
-        try:
-            d = json.load(open(tp))
-            key = f"{p.name}:b{p.b_phi}:gpus{world}:v{args.variant}"
-            traffic = d.get(key)
-        except Exception:
-            traffic = None
 
     if rank != 0:
         return 0

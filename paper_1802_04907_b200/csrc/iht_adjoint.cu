@@ -26,6 +26,8 @@
 //      (the sum is order-free in exact integer arithmetic).
 //      The MMA takes the MACs off the ALU so the kernel can stay on the HBM roof;
 //      this is still a GEMV (N = 3 useful of 8 MMA columns), not a reshaped GEMM.
+#include <stdlib.h>
+
 #include "iht_internal.cuh"
 
 namespace iht {
@@ -199,6 +201,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t smem_addr) {
 //   [Fc, Sl, red] per-chunk exponents, exact per-limb integer sums of r_int, scratch
 template <int B>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs a) {
+  pdl_launch_dependents();
   constexpr int P = 8 / B;               // codes per byte
   constexpr int RPC = 128 / B;           // rows per 16-byte lane chunk
   constexpr int KSTEP = 4 * RPC;         // rows per warp k-step (4 lanes t)
@@ -264,6 +267,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
 #pragma unroll 1
   for (int j = 0; j < kRing; ++j) request(j);
 
+  // the code requests above read only the (constant) copy; r comes from the forward kernel
+  pdl_wait();
   // ---- prologue 1: per-chunk max |r| -> exponent F_c ---------------------------------
   for (int c = 0; c < nchunks; ++c) {
     float m = 0.0f;
@@ -419,6 +424,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
 
 __global__ void adjoint_reduce_kernel(const float* __restrict__ part, int nK, int64_t N, float sigma,
                                       float* __restrict__ g) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float s = part[n];
@@ -444,6 +451,11 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   int64_t KR = min64(Rpad, kMaxKR);
   KR = (KR + 1023) / 1024 * 1024;
   while (KR > 1024 && ntask * ((Rpad + KR - 1) / KR) < 4 * warps_full) KR = (KR / 2 + 1023) / 1024 * 1024;
+  {
+    static int kr_env = -1;                       // profiling override (IHT_ADJ_KR, rows)
+    if (kr_env < 0) kr_env = getenv("IHT_ADJ_KR") ? atoi(getenv("IHT_ADJ_KR")) : 0;
+    if (kr_env >= 1024) KR = min64((int64_t)kr_env / 1024 * 1024, kMaxKR);
+  }
   p.KR = (int)KR;
   int d = 4;                            // KC = 1024 d <= kChunkRows, dividing KR
   while ((KR / 1024) % d) --d;
@@ -531,7 +543,7 @@ extern "C" int iht_adjoint(const iht_qmat* A, const float* r, float* g, int vari
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); \
       attr_set = true;                                                                            \
     }                                                                                             \
-    adjoint_mma_kernel<BB><<<grid, kMmaWarps * 32, p.smem, st>>>(a);                              \
+    IHT_CUDA_CHECK(launch_pdl(adjoint_mma_kernel<BB>, grid, dim3(kMmaWarps * 32), p.smem, st, a));  \
   } while (0)
   if (A->bits == 2) IHT_ADJ0(2);
   else if (A->bits == 4) IHT_ADJ0(4);
@@ -539,8 +551,8 @@ extern "C" int iht_adjoint(const iht_qmat* A, const float* r, float* g, int vari
 #undef IHT_ADJ0
   IHT_LAUNCH_CHECK();
   if (p.nK > 1) {
-    adjoint_reduce_kernel<<<(unsigned)ceil_div<int64_t>(A->cols, 256), 256, 0, st>>>(
-        static_cast<const float*>(ws), p.nK, A->cols, sigma, g);
+    IHT_CUDA_CHECK(launch_pdl(adjoint_reduce_kernel, dim3((unsigned)ceil_div<int64_t>(A->cols, 256)), dim3(256), 0,
+                              st, static_cast<const float*>(ws), p.nK, A->cols, sigma, g));
     IHT_LAUNCH_CHECK();
   }
   return IHT_OK;

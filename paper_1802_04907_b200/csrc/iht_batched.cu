@@ -133,6 +133,7 @@ struct BatchArgs {
 
 template <int BITS>
 __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs a) {
+  pdl_launch_dependents();
   using C = BCfg<BITS>;
   constexpr int TS = C::TS, KBB = C::KBR, NKS = C::NKS, PK = C::PK, ACOLS = C::ACOLS;
   constexpr int ST = C::STAGES, PKS = C::PKSLOTS;
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();                               // the limb image and F_b, S_b (batched_limbs_kernel)
   const uint32_t acc_stride = 128;                                      // columns per accumulator
   const uint32_t a_col0 = 256;                                          // first A-stage column
   for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
@@ -442,6 +444,8 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
                                                             int nkb, uint8_t* __restrict__ bimg, int* __restrict__ Fb,
                                                             int* __restrict__ Sb) {
   constexpr int KBR = BCfg<BITS>::KBR;
+  pdl_launch_dependents();
+  pdl_wait();                               // R (forward)
   const int b = blockIdx.x;                 // b >= nreal: zero padding snapshot (MMA N granularity)
   const bool live = b < nreal;
   const float* r = R + (int64_t)(live ? b : 0) * Rpad;
@@ -611,16 +615,16 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     const size_t smem = batched_smem(A->bits, bp);
 #define IHT_BATCH(BB)                                                                                  \
   do {                                                                                                 \
-    batched_limbs_kernel<BB><<<bp, 256, 0, st>>>(Rc, (int)Rpad, bp, nb, nkb, bimg, Fb, Sb);           \
-    IHT_LAUNCH_CHECK();                                                                                \
+    IHT_CUDA_CHECK(launch_pdl(batched_limbs_kernel<BB>, dim3(bp), dim3(256), 0, st, Rc, (int)Rpad, bp, nb, \
+                              nkb, bimg, Fb, Sb));                                                     \
     static bool attr = false;                                                                          \
     if (!attr) {                                                                                       \
       IHT_CUDA_CHECK(cudaFuncSetAttribute(adjoint_batched_kernel<BB>,                                  \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));   \
       attr = true;                                                                                     \
     }                                                                                                  \
-    adjoint_batched_kernel<BB><<<min(b.ntiles, sms), kBThreads, smem, st>>>(b);                        \
-    IHT_LAUNCH_CHECK();                                                                                \
+    IHT_CUDA_CHECK(launch_pdl(adjoint_batched_kernel<BB>, dim3(min(b.ntiles, sms)), dim3(kBThreads), smem, st, \
+                              b));                                                                     \
   } while (0)
     if (A->bits == 2) IHT_BATCH(2);
     else if (A->bits == 4) IHT_BATCH(4);

@@ -37,6 +37,8 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   __shared__ float part[kFwdThreads / 32][kFwdWords][CPW];
   __shared__ int64_t sidx[kFwdStage];   // tiled byte offset of each staged support column
   __shared__ float sval[kFwdStage];
+  pdl_launch_dependents();
+  pdl_wait();                                   // x (previous H_s) and y-hat
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = lane >> 3, wl = lane & 7;
   const int b = blockIdx.y;
@@ -157,13 +159,12 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* codes = static_cast<const uint8_t*>(F->codes);
 #define IHT_FWD(BB)                                                                             \
-  forward_kernel<BB><<<dim3(blocks, nrhs), kFwdThreads, 0, st>>>(                            \
-      codes, F->strip_bytes, words_total, (int)F->rows, (int)iht_rows_pad(F->rows), L, sigma, x_idx, x_val, \
-      x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen)
+  IHT_CUDA_CHECK(launch_pdl(forward_kernel<BB>, dim3(blocks, nrhs), dim3(kFwdThreads), 0, st, codes,      \
+                            F->strip_bytes, words_total, (int)F->rows, (int)iht_rows_pad(F->rows), L, sigma, \
+                            x_idx, x_val, x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen))
   if (F->bits == 2) IHT_FWD(2);
   else if (F->bits == 4) IHT_FWD(4);
   else IHT_FWD(8);
 #undef IHT_FWD
-  IHT_LAUNCH_CHECK();
   return IHT_OK;
 }

@@ -80,6 +80,31 @@ __device__ __forceinline__ float q_scale_factor(float c, int L) {
   return c == 0.0f ? 0.0f : __fdiv_rn((float)(L - 1), __fmul_rn(2.0f, c));
 }
 
+// ---------------------------------------------------- programmatic dependent launch
+// The solver's kernels are launched with programmatic stream serialization: a kernel lets
+// the next grid begin launching as soon as it starts (pdl_launch_dependents) and waits for
+// its predecessor's completion and memory only where it first reads the predecessor's
+// outputs (pdl_wait) -- the launch latency and the setup before that point overlap the
+// predecessor.  Both are no-ops when the kernel was not launched that way.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ inline int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 

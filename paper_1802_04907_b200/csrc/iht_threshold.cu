@@ -558,6 +558,8 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   if (mu_dev) mu = mu_dev[blockIdx.y];
   int32_t* cidx = reinterpret_cast<int32_t*>(dsm + (size_t)slice * 4);        // [kClWarps][kWarpCand]
   float* cval = reinterpret_cast<float*>(cidx + kClWarps * kWarpCand);        // [kClWarps][kWarpCand]
+  int32_t* pidx = reinterpret_cast<int32_t*>(cval + kClWarps * kWarpCand);    // packed list (index order)
+  float* pval = reinterpret_cast<float*>(pidx + kClWarps * kWarpCand);
   __shared__ ClShared cs;
   __shared__ int tot[2048];
   __shared__ int scratch[kClWarps];
@@ -567,6 +569,8 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_launch_dependents();
+  pdl_wait();                                   // g (adjoint) and x (previous H_s)
   const int b = blockIdx.y;
   x_idx += (int64_t)b * ldx;
   x_val += (int64_t)b * ldx;
@@ -686,26 +690,20 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   int any_ovf = 0;
   for (int p = 0; p < CL; ++p) any_ovf |= cluster.map_shared_rank(cs.flags, p)[1];
   if (!any_ovf) {
-    // pack the warp lists in order: warp w's entries move down to the running offset
-    static_assert(kWarpCand <= kClThreads, "one entry per thread per warp list");
-    int nc = min(wgt[0], kWarpCand);
-    for (int w = 1; w < kClWarps; ++w) {
-      const int c0 = min(wgt[w], kWarpCand);
-      int32_t ii = 0;
-      float vv = 0.0f;
-      if (tid < c0) {
-        ii = cidx[w * kWarpCand + tid];
-        vv = cval[w * kWarpCand + tid];
-      }
-      __syncthreads();                                // reads before the (lower, overlapping) writes
-      if (tid < c0) {
-        cidx[nc + tid] = ii;
-        cval[nc + tid] = vv;
-      }
-      nc += c0;
-      __syncthreads();
+    // pack the warp lists in order into the second buffer: every warp copies its own list
+    // to its running offset at once
+    int off = 0, nc = 0;
+    for (int w = 0; w < kClWarps; ++w) {
+      const int cw = min(wgt[w], kWarpCand);
+      if (w == warp) off = nc;
+      nc += cw;
     }
-    cluster_select(cluster, cs, buf, nc, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; },
+    for (int j = lane; j < min(wgt[warp], kWarpCand); j += 32) {
+      pidx[off + j] = cidx[warp * kWarpCand + j];
+      pval[off + j] = cval[warp * kWarpCand + j];
+    }
+    __syncthreads();
+    cluster_select(cluster, cs, buf, nc, [&](int i) { return pval[i]; }, [&](int i) { return pidx[i]; },
                    all ? 0u : (d1 << 20), target, all, tot, scratch, wgt, weq, wtake, wbase, sh, out_idx, out_val,
                    out_nnz + b);
   } else {
@@ -793,7 +791,7 @@ static int thr_attrs() {
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kClusterSlice * 4 + kClWarps * kWarpCand * 8));
+                                        kClusterSlice * 4 + kClWarps * kWarpCand * 16));
     g_thr_attr = true;
   }
   return IHT_OK;
@@ -831,15 +829,17 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(CL, nrhs);
     lc.blockDim = dim3(kClThreads);
-    lc.dynamicSmemBytes = (size_t)slice * 4 + (size_t)kClWarps * kWarpCand * 8;
+    lc.dynamicSmemBytes = (size_t)slice * 4 + (size_t)kClWarps * kWarpCand * 16;
     lc.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = 2;
     IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
                                       N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe()));
     return IHT_OK;

@@ -48,6 +48,10 @@ if which in ("all", "c2"):
     nz = torch.full((1,), s, dtype=torch.int32, device='cuda')
     g = torch.randn(N, device='cuda')
     print(f"c2 threshold         {timeit(lambda: iht.threshold(xi, xv, nz, g, 1.0, s)):.1f} us")
+    (A2,) = [iht.new_copy(4096, N, 1, 2, 0, 77, 0, 1.0, device='cuda')]
+    A2.codes.random_(0, 255)
+    r2 = torch.randn(iht.vec_len(4096, 1), device='cuda')
+    print(f"c2 adjoint           {timeit(lambda: iht.adjoint(A2, r2)):.1f} us")
 if which in ("all", "c4"):
     M, N, s = 65536, 262144, 1024
     (F,) = [iht.new_copy(M, N, 1, 4, 0, 77, 0, 1.0, device='cuda')]
