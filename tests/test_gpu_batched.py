@@ -326,3 +326,20 @@ def test_adjoint_batched_odd_level_mode(bits):
     Gm = iht.adjoint_batched(A, _to_dev(R)).cpu().numpy()
     for b in range(B):
         assert rel_l2(Gm[b], OI.adjoint(Ad, unstack(R[b], M, 2))) < TOL_T
+
+
+def test_batched_solver_nan_snapshot_isolated():
+    """A non-finite observation poisons only its own snapshot (out_nnz = -1); the others
+    are unaffected and equal the run without it."""
+    B = 8
+    p, Y = _radio_batch(B, n_iter=5, K=10)
+    pool = iht.quantize(_to_dev(p.phi), p.b_phi, 0, p.seed, list(range(p.K)), float(OQ.scale_c(p.phi)))
+    sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, nrhs=B)
+    ri, rv, rn = [t.cpu().clone() for t in sol.run(_to_dev(Y))]
+    Y2 = Y.copy()
+    Y2[5, 7] = np.nan
+    gi, gv, gn = [t.cpu().clone() for t in sol.run(_to_dev(Y2))]
+    assert int(gn[5]) == -1
+    keep = [b for b in range(B) if b != 5]
+    assert torch.equal(gn[keep], rn[keep]) and torch.equal(gi[keep], ri[keep]) and torch.equal(gv[keep], rv[keep])
+    sol.close()

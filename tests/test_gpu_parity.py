@@ -353,3 +353,31 @@ def test_solver_world1_row_shard_path():
             ref.close()
     finally:
         comm.close()
+
+
+def test_solver_edge_cases():
+    """n* = 0 returns x = 0 (empty support); s = 0 keeps nothing; a NaN in y reaches
+    H_s and is reported as IHT_EDOMAIN by the host-IO run."""
+    p = CASES["gauss8bit"]()
+    c = OQ.scale_c(p.phi)
+    pool = _pool(p.phi, p.b_phi, 2, c, p.seed)
+    sol = iht.Solver(pool, p.s, 0, p.mu, p.b_y, p.seed)
+    _, _, n = sol.run(_to_dev(p.y))
+    torch.cuda.synchronize()
+    assert int(n.item()) == 0
+    sol.close()
+    sol = iht.Solver(pool, 0, 5, p.mu, p.b_y, p.seed)
+    _, _, n = sol.run(_to_dev(p.y))
+    torch.cuda.synchronize()
+    assert int(n.item()) == 0
+    sol.close()
+    y = p.y.copy()
+    y[3] = np.nan
+    sol = iht.Solver(pool, p.s, 3, p.mu, p.b_y, p.seed)
+    oi = torch.empty(p.s, dtype=torch.int32).pin_memory()
+    ov = torch.empty(p.s, dtype=torch.float32).pin_memory()
+    on = torch.empty(1, dtype=torch.int32).pin_memory()
+    with pytest.raises(iht._lib.IhtError) as e:
+        sol.run_host(torch.from_numpy(y).pin_memory(), oi, ov, on)
+    assert e.value.status == iht._lib.IHT_EDOMAIN
+    sol.close()
