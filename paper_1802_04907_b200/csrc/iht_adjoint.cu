@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   int* Fc = reinterpret_cast<int*>(limbs + 3 * a.limb_stride);
   int* Sl = Fc + ((nchunks + 1) & ~1);                     // [chunk][3] limb sums of r_int
   float* red = reinterpret_cast<float*>(Sl + 3 * nchunks);  // [nchunks][kMmaWarps] scratch
+  int& nonfinite = *reinterpret_cast<int*>(red + nchunks * kMmaWarps);   // r holds a NaN / inf
 
   const int kr = blockIdx.y;
   const int64_t row0 = (int64_t)kr * a.KR;
@@ -270,20 +271,27 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   // the code requests above read only the (constant) copy; r comes from the forward kernel
   pdl_wait();
   // ---- prologue 1: per-chunk max |r| -> exponent F_c ---------------------------------
+  // (max over |r| bit patterns: a NaN or inf in r is caught and makes g NaN, so that H_s
+  // reports the domain error)
+  if (tid == 0) nonfinite = 0;
   for (int c = 0; c < nchunks; ++c) {
-    float m = 0.0f;
+    unsigned int m = 0;
     for (int i = tid; i < a.KC; i += blockDim.x) {
       const int64_t row = row0 + (int64_t)c * a.KC + i;
-      if (row < a.Rpad) m = fmaxf(m, fabsf(__ldg(a.r + row)));
+      if (row < a.Rpad) m = max(m, __float_as_uint(__ldg(a.r + row)) & 0x7FFFFFFFu);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) red[c * kMmaWarps + warp] = m;
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) red[c * kMmaWarps + warp] = __uint_as_float(m);
   }
   __syncthreads();
   for (int c = tid; c < nchunks; c += blockDim.x) {
-    float m = 0.0f;
-    for (int w = 0; w < kMmaWarps; ++w) m = fmaxf(m, red[c * kMmaWarps + w]);
+    unsigned int mb = 0;
+    for (int w = 0; w < kMmaWarps; ++w) mb = max(mb, __float_as_uint(red[c * kMmaWarps + w]));
+    if (mb >= 0x7F800000u) {
+      nonfinite = 1;
+      mb = 0;
+    }
+    const float m = __uint_as_float(mb);
     int e = 0;
     if (m > 0.0f) frexpf(m, &e);            // m in [2^{e-1}, 2^e)
     Fc[c] = (m > 0.0f) ? min(22 - e, 126) : 0;   // |r| 2^F < 2^22 (clamped for tiny r)
@@ -411,6 +419,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
     }
     const int64_t c0 = task * 16 + g8, c1 = c0 + 8;
     if (t == 0) {
+      if (nonfinite) accf0 = accf1 = __int_as_float(0x7FC00000);
       if (a.nK == 1) {
         if (c0 < a.N) a.g[c0] = a.sigma * accf0;
         if (c1 < a.N) a.g[c1] = a.sigma * accf1;
@@ -464,7 +473,7 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   p.limb_stride = p.KR + 64;
   const int nchunks = p.KR / p.KC;
   p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
-           sizeof(float) * nchunks * kMmaWarps;
+           sizeof(float) * nchunks * kMmaWarps + 16;
   int per_sm = (int)(size_t)min64(4, (size_t)(227 * 1024) / p.smem);
   if (per_sm < 1) per_sm = 1;
   p.ctas_x = (int)max64(1, min64((ntask + kMmaWarps - 1) / kMmaWarps,

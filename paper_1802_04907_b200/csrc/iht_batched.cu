@@ -33,6 +33,7 @@
 namespace iht {
 
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
+constexpr int kNonFinite = 1000;       // F_b marker: r_b holds a NaN / inf -> g_b = NaN
 constexpr int kBThreads = 352;         // 11 warps (roles above)
 
 // Per bit width: tile-steps (512/b rows, 1 KiB of a 16-column tile) per K-block, so that a
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   const uint32_t acc_stride = 128;                                      // columns per accumulator
   const uint32_t a_col0 = 256;                                          // first A-stage column
   for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
-    ep_scale[b] = a.sigma * ldexpf(1.0f, -a.Fb[b]);
+    ep_scale[b] = a.Fb[b] == kNonFinite ? __int_as_float(0x7FC00000) : a.sigma * ldexpf(1.0f, -a.Fb[b]);
     ep_off[b] = (long long)(a.L - 1) * ((long long)a.Sb[2 * b] + 256ll * a.Sb[2 * b + 1]);
     ep_off32[b] = (int)ep_off[b];
   }
@@ -452,25 +453,30 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
   __shared__ float red[8];
   __shared__ int ired[2][8];
   __shared__ int Fs;
-  float m = 0.0f;
+  // max |r| over bit patterns: a NaN / inf in r_b marks the snapshot (F = kNonFinite) and
+  // its g becomes NaN, so that its H_s reports the domain error
+  unsigned int m = 0;
   if (live)
     for (int i = threadIdx.x * 4; i < Rpad; i += blockDim.x * 4) {
       const float4 v = *reinterpret_cast<const float4*>(r + i);
-      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      m = max(max(m, __float_as_uint(v.x) & 0x7FFFFFFFu), __float_as_uint(v.y) & 0x7FFFFFFFu);
+      m = max(max(m, __float_as_uint(v.z) & 0x7FFFFFFFu), __float_as_uint(v.w) & 0x7FFFFFFFu);
     }
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = __uint_as_float(m);
   __syncthreads();
   if (threadIdx.x == 0) {
-    float mm = 0.0f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, red[w]);
+    unsigned int mb = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mb = max(mb, __float_as_uint(red[w]));
+    const bool bad = mb >= 0x7F800000u;
+    const float mm = bad ? 0.0f : __uint_as_float(mb);
     int e = 0;
     if (mm > 0.0f) frexpf(mm, &e);
-    Fs = mm > 0.0f ? min(14 - e, 126) : 0;          // |r| 2^F < 2^14 -> two limbs
+    Fs = bad ? kNonFinite : (mm > 0.0f ? min(14 - e, 126) : 0);   // |r| 2^F < 2^14 -> two limbs
     Fb[b] = Fs;
   }
   __syncthreads();
-  const float scale = ldexpf(1.0f, Fs);
+  const float scale = Fs == kNonFinite ? 0.0f : ldexpf(1.0f, Fs);
   const int NB = 2 * B;
   int s0 = 0, s1 = 0;
   for (int ch = threadIdx.x; ch < nkb * KBR / 16; ch += blockDim.x) {   // rows past Rpad: zero limbs
