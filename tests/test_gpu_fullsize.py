@@ -4,6 +4,9 @@ oracle can compute one by one.
 
 * config 2 (4096 x 16384, 2-bit, K = 400 copies): codes of whole copies bit-exact; two
   teacher-forced iterations (forward, adjoint, threshold) against the dense oracle.
+* config 5 (2304 x 65536 complex radio, 2-bit, B = 64, K = 400): sampled code blocks bit-exact,
+  the batched tcgen05 adjoint on sampled pixels, the batched forward on true supports, the
+  exact top-64 of all 64 snapshots; config 3 (its snapshot 0) through the GEMV adjoint.
 * config 4 (65536 x 262144, 4-bit, K = 2, 16 GiB of codes): the device absmax equals
   the oracle's c (tests/golden/config4_scale.json, written by scripts/golden_config4.py
   from oracle/ only); random code tiles bit-exact; adjoint on 64 sampled columns,
@@ -171,3 +174,89 @@ def test_config4_adjoint_forward_threshold_sampled(config4):
     k = int(on.item())
     assert oi[:k].cpu().numpy().tolist() == ri.tolist()
     np.testing.assert_array_equal(ov[:k].cpu().numpy(), rv.astype(np.float32))
+
+
+# ------------------------------------------------------------------------------ config 3 / 5
+@pytest.fixture(scope="module")
+def config5():
+    """Config 5 (config 3's radio Phi, 2304 x 65536 complex, 2-bit, B = 64 snapshots) built as
+    bench.py builds it (column shard of the whole Phi at world size 1, K = 400 copies)."""
+    p = G.config_problem(5)
+    pool, c, _, rows, row0 = build_pool(p, 0, 1, _dev(), False, shard="cols")
+    torch.cuda.synchronize()
+    return p, pool, c
+
+
+def _radio_cols(p, cid, c, cols):
+    """Oracle codes -> dequantised columns `cols` of copy cid (complex, M x len(cols))."""
+    blk = np.ascontiguousarray(p.phi[:, cols])
+    out = np.empty((p.M, len(cols)), np.complex128)
+    for j, n in enumerate(cols):            # one column at a time: global column index n
+        q, _ = OQ.quantize_matrix(blk[:, j:j + 1], p.b_phi, 0, p.seed, cid, c=c, col_offset=int(n))
+        out[:, j] = OQ.dequantize(q, c, p.b_phi, 0)[:, 0]
+    return out
+
+
+def test_config5_codes_adjoint_forward_threshold_sampled(config5):
+    p, pool, c = config5
+    assert len(pool) == 400
+    c_ref = OQ.scale_c(p.phi)
+    assert np.float32(c) == c_ref                                          # (a1) exact
+    rng = np.random.default_rng(55)
+    # codes: random 64-column blocks of copies 0, 1 and 399, all rows and both planes
+    for cid in (0, 1, 399):
+        c0 = int(rng.integers(0, p.N - 64)) // 16 * 16
+        ref, _ = OQ.quantize_matrix(np.ascontiguousarray(p.phi[:, c0:c0 + 64]), p.b_phi, 0, p.seed, cid, c=c_ref,
+                                    col_offset=c0)
+        np.testing.assert_array_equal(_tile_codes(pool[cid], p.M, p.N, 2, p.b_phi, 0, p.M, c0, 64), ref)
+    B = p.meta["batch_y"].shape[1]
+    Y = np.ascontiguousarray(p.meta["batch_y"].T)                          # (B, M)
+    Yd = _to_dev(Y)
+    yhat, _ = iht.quantize_vec_batched(Yd, p.b_y, 0, p.seed, iht.absmax_batched(Yd))
+    # iteration 1 of every snapshot, teacher-forced: r = y-hat (x = 0), g on 48 sampled pixels
+    G_dev = iht.adjoint_batched(pool[0], yhat).cpu().numpy()
+    cols = np.sort(rng.choice(p.N, 48, replace=False))
+    A0 = _radio_cols(p, 0, c_ref, cols)
+    for b in rng.choice(B, 8, replace=False):
+        y_codes, c_y = OQ.quantize_vector(Y[b], p.b_y, 0, p.seed, snapshot=int(b))
+        y_hat = OQ.dequantize(y_codes, c_y, p.b_y, 0)
+        assert rel_l2(yhat[b].cpu().numpy(), stack(y_hat, p.M)) < 1e-6
+        g_ref = OI.adjoint(A0, y_hat)
+        assert rel_l2(G_dev[b, cols], g_ref) < 1e-3                      # tensor-core path bar
+    # forward over each snapshot's true support (s = 64 columns), copy 1
+    xi = np.stack([np.asarray(x, np.int32) for x in p.meta["batch_x_idx"]])
+    xv = np.stack([np.asarray(v, np.float32) for v in p.meta["batch_x_val"]])
+    nz = np.full(B, p.s, np.int32)
+    R = iht.forward_batched(pool[1], _to_dev(xi), _to_dev(xv), _to_dev(nz), yhat).cpu().numpy()
+    for b in rng.choice(B, 4, replace=False):
+        F1 = _radio_cols(p, 1, c_ref, xi[b])
+        y_codes, c_y = OQ.quantize_vector(Y[b], p.b_y, 0, p.seed, snapshot=int(b))
+        r_ref = OI.forward(F1, np.arange(p.s), xv[b].astype(np.float64), OQ.dequantize(y_codes, c_y, p.b_y, 0))
+        assert rel_l2(unstack(R[b], p.M, 2), r_ref) < TOL
+    # exact per-snapshot top-64 over N = 65536 on the fp32 a the kernel sees
+    mu = np.float32(p.mu)
+    zero = np.zeros((B, p.s), np.int32)
+    oi, ov, on = iht.threshold_batched(_to_dev(zero), _to_dev(zero.astype(np.float32)), _to_dev(np.zeros(B, np.int32)),
+                                       _to_dev(G_dev), float(mu), p.s)
+    oi, ov, on = oi.cpu().numpy(), ov.cpu().numpy(), on.cpu().numpy()
+    for b in range(B):
+        a32 = (mu * G_dev[b]).astype(np.float32)
+        ri, rv = OI.hard_threshold(a32.astype(np.float64), p.s)
+        assert oi[b, :on[b]].tolist() == ri.tolist()
+        np.testing.assert_array_equal(ov[b, :on[b]], rv.astype(np.float32))
+
+
+def test_config3_single_snapshot_teacher_forced(config5):
+    """Config 3 = snapshot 0 of config 5's problem through the single-observation path: the
+    int8-MMA GEMV adjoint of the same copy agrees with the oracle on sampled pixels."""
+    p, pool, c = config5
+    c_ref = OQ.scale_c(p.phi)
+    y0 = np.ascontiguousarray(p.meta["batch_y"][:, 0])
+    yd = _to_dev(y0)
+    yhat, _ = iht.quantize_vec(yd, p.b_y, 0, p.seed, iht.absmax(yd))
+    g = iht.adjoint(pool[0], yhat).cpu().numpy()
+    rng = np.random.default_rng(33)
+    cols = np.sort(rng.choice(p.N, 48, replace=False))
+    y_codes, c_y = OQ.quantize_vector(y0, p.b_y, 0, p.seed)
+    g_ref = OI.adjoint(_radio_cols(p, 0, c_ref, cols), OQ.dequantize(y_codes, c_y, p.b_y, 0))
+    assert rel_l2(g[cols], g_ref) < TOL
