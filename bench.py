@@ -262,6 +262,9 @@ def main():
     adj_ms = sol.adjoint_times_ms()
     out_idx, out_val, out_nnz = sol.out_idx, sol.out_val, sol.out_nnz
     nnz = [int(v) for v in out_nnz.cpu()]
+    if min(nnz) < 0:   # a poisoned (non-finite) iterate lets kernels exit early: not a valid run
+        raise SystemExit(f"bench: the iteration diverged (support size {min(nnz)}): step mu = {p.mu} "
+                         "is unstable for this workload (reading c9)")
     launches_per_run = sol.launches_per_run()
 
     # ---- end-to-end through the public API with host buffers --------------------------

@@ -203,6 +203,14 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     bool s_wrapped = false;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
+        if (a.probe & 64) {                       // probe 64: no handoffs after the first round
+          if (!s_wrapped) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive2(smem_u32(&st_full[ss]));
+          }
+          if (++ss == ST) { ss = 0; sph ^= 1u; s_wrapped = true; }
+          continue;
+        }
         if (a.probe & 8) {                        // probe: hand the A stage over untouched
           if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
           __syncwarp();
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t] = clock64();
       const uint32_t dtm = tmem + ab * acc_stride;
       for (int kb = 0; kb < a.nkb; ++kb) {
-        mbar_wait2(smem_u32(&st_full[ss]), sph);
+        if (!(a.probe & 64) || (t == 0 && kb < ST)) mbar_wait2(smem_u32(&st_full[ss]), sph);   // probe 64: first round only
         if (a.tlog && lane == 0 && t == 0 && kb < 16) a.tlog[blockIdx.x * 64 + 40 + kb] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         // warp-uniform operands (shuffled from lane 0 so the compiler keeps them uniform)
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     uint32_t ph = 0;
     bool wrapped = false;
     const int64_t last_tile = (a.N + 15) / 16 - 1;
-    for (int tile = (a.probe & 8) ? a.ntiles : blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    for (int tile = (a.probe & (8 | 64)) ? a.ntiles : blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
         const int tsn = min(TS, a.ksteps - kb * TS);
         const uint32_t bytes = (uint32_t)(tsn * 1024);
@@ -372,7 +380,11 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     bool wrapped = false;
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
-        if (wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
+        if (a.probe & 64) {                       // probe 64: fill the stages once, then stop
+          if (wrapped) break;
+        } else if (wrapped) {
+          mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
+        }
         if (lane == 0) {
           if ((a.probe & 1) && wrapped) {
             mbar_arrive2(smem_u32(&st_full[ss]));                 // probe: reuse the stale stage

@@ -89,10 +89,11 @@ __device__ void find_bin(const int* hist, int nbins, int target, int* d_out, int
 // order: radix select of the s-th largest key, then ordered compaction (ties -> lowest
 // index, zeros never kept).  All 1024 threads of the CTA call it.  Writes out_*;
 // returns nothing; *out_nnz = total (or -1 when nan_flag).
-template <class Val, class Idx>
+template <int NT = kThrThreads, class Val, class Idx>
 __device__ void select_ordered(int n, int s, Val val, Idx idx, int32_t* __restrict__ out_idx,
                                float* __restrict__ out_val, int32_t* __restrict__ out_nnz, int nan_flag,
                                int* hist, int* scratch, int* wgt, int* weq, int* wtake, int* wbase, int* sh) {
+  constexpr int kThrThreads = NT, kThrWarps = NT / 32;   // shadow: all NT threads of the CTA call it
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned int T = 0;
   int need = 0;
@@ -114,7 +115,7 @@ __device__ void select_ordered(int n, int s, Val val, Idx idx, int32_t* __restri
           atomicAdd(&hist[(key >> sh_) & (nb - 1)], 1);
       }
       __syncthreads();
-      find_bin(hist, nb, target, &sh[0], &sh[1], scratch);
+      find_bin<NT>(hist, nb, target, &sh[0], &sh[1], scratch);
       prefix |= (unsigned int)sh[0] << sh_;
       target -= sh[1];
       __syncthreads();
@@ -415,6 +416,7 @@ struct ClShared {
   int hist[2][2048];
   int flags[2];        // [0] NaN or poisoned input, [1] a warp's candidate list overflowed
   int counts[2];       // [0] keys > T, [1] keys == T (ordered compaction)
+  int ncand;           // candidates after extraction (gather path)
 };
 
 // Histogram pass over the local list (pass index `pass`, 11/11/9 bits) summed over the
@@ -454,7 +456,7 @@ template <class Val, class Gidx>
 __device__ void cluster_select(cg::cluster_group& cluster, ClShared& cs, int& buf, int n, Val val, Gidx gidx,
                                unsigned int prefix, int target, bool all, int* tot, int* scratch, int* wgt, int* weq,
                                int* wtake, int* wbase, int* sh, int32_t* __restrict__ out_idx,
-                               float* __restrict__ out_val, int32_t* __restrict__ out_nnz) {
+                               float* __restrict__ out_val, int32_t* __restrict__ out_nnz, int probe = 0) {
   const int CL = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -466,6 +468,7 @@ __device__ void cluster_select(cg::cluster_group& cluster, ClShared& cs, int& bu
       prefix |= (unsigned int)sh[0] << (pass == 1 ? 9 : 0);
       target -= sh[1];
       __syncthreads();
+      if (probe == 4 + pass) return;                // profiling probe: stop after this pass
     }
     T = prefix;
     need = target;
@@ -685,10 +688,42 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   if (lane == 0) wgt[warp] = wc;
   if (probe == 3) { cluster.sync(); return; }
   const int ovf = __syncthreads_or(wc > kWarpCand);
-  if (tid == 0) cs.flags[1] = ovf;
+  if (tid == 0) {
+    int nc = 0;
+    for (int w = 0; w < kClWarps; ++w) nc += min(wgt[w], kWarpCand);
+    cs.flags[1] = ovf;
+    cs.ncand = nc;                                  // this CTA's candidates (valid without overflow)
+  }
   cluster.sync();
-  int any_ovf = 0;
-  for (int p = 0; p < CL; ++p) any_ovf |= cluster.map_shared_rank(cs.flags, p)[1];
+  int any_ovf = 0, total = 0, base = 0;
+  for (int p = 0; p < CL; ++p) {
+    const int* rf = cluster.map_shared_rank(cs.flags, p);
+    const int c = *cluster.map_shared_rank(&cs.ncand, p);
+    any_ovf |= rf[1];
+    if (p < rank) base += c;
+    total += c;
+  }
+  if (!any_ovf && total <= kClWarps * kWarpCand && probe != 9) {   // probe 9: per-pass cluster path (A/B)
+    // few candidates (the usual case): every CTA stores its ordered lists into rank 0's
+    // packed buffer at its cluster offset (DSMEM stores, ranks in index order), then rank 0
+    // alone finishes the select on them -- two cluster barriers instead of one per pass.
+    // The candidates hold every key with digit >= d1 (>= s of them unless fewer nonzero
+    // keys exist), so their top-s, ties to the lowest index, is the top-s of a.
+    int32_t* gidx = cluster.map_shared_rank(pidx, 0);
+    float* gval = cluster.map_shared_rank(pval, 0);
+    int off = base;
+    for (int w = 0; w < warp; ++w) off += min(wgt[w], kWarpCand);
+    for (int j = lane; j < min(wgt[warp], kWarpCand); j += 32) {
+      gidx[off + j] = cidx[warp * kWarpCand + j];
+      gval[off + j] = cval[warp * kWarpCand + j];
+    }
+    cluster.sync();                                 // rank 0's list complete; nobody reads remote memory after
+    if (rank != 0) return;
+    if (probe == 4) return;
+    select_ordered<kClThreads>(total, s, [&](int i) { return pval[i]; }, [&](int i) { return pidx[i]; }, out_idx,
+                               out_val, out_nnz + b, 0, tot, scratch, wgt, weq, wtake, wbase, sh);
+    return;
+  }
   if (!any_ovf) {
     // pack the warp lists in order into the second buffer: every warp copies its own list
     // to its running offset at once
@@ -703,9 +738,10 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
       pval[off + j] = cval[warp * kWarpCand + j];
     }
     __syncthreads();
+    if (probe == 4) { cluster.sync(); return; }
     cluster_select(cluster, cs, buf, nc, [&](int i) { return pval[i]; }, [&](int i) { return pidx[i]; },
                    all ? 0u : (d1 << 20), target, all, tot, scratch, wgt, weq, wtake, wbase, sh, out_idx, out_val,
-                   out_nnz + b);
+                   out_nnz + b, probe);
   } else {
     const int64_t base_idx = col_offset + lo;
     cluster_select(cluster, cs, buf, n, [&](int i) { return as[i]; }, [&](int i) { return base_idx + i; },

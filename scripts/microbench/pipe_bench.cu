@@ -42,14 +42,15 @@ __device__ __forceinline__ void mbar_spin(uint32_t m, uint32_t ph) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
+__global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc, int rnd) {
   constexpr int ST = Cfg<MODE>::ST, KPB = Cfg<MODE>::KPB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t a_full[16], a_free[16], b_full[16], b_free[16], acc_full[2], acc_free[2], done;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem)[i] = rnd ? (uint32_t)(i * 2654435761u + 12345u) ^ ((uint32_t)i >> 7) * 40503u : 0u;
   if (threadIdx.x == 0) {
     for (int i = 0; i < ST; ++i) {
       mbar_init(su32(&a_full[i]), MODE >= 8 ? 5 : 4); mbar_init(su32(&a_free[i]), 1);
@@ -67,6 +68,18 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tslot;
+  if (rnd && warp < 4) {
+    for (int c = 0; c < 256; ++c) {
+      uint32_t x = (uint32_t)(threadIdx.x * 7919u + c * 104729u) * 2654435761u;
+      x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+      if (rnd == 1) x &= 0x03030303u;
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + 256 + c + ((uint32_t)(warp * 32) << 16)), "r"(x) : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp < 4 && MODE >= 2) {
     int s = 0; uint32_t ph = 0; bool wr = false;
     for (int kb = 0; kb < nkb; ++kb) {
@@ -144,20 +157,21 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc) {
 }
 
 template <int MODE>
-void run(const char* name, int sms) {
+void run(const char* name, int sms, int rnd = 0) {
   const int nkb = 18 * 114;
   long long* d;
   cudaMalloc(&d, sms * sizeof(long long));
   auto k = pipe<MODE>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  k<<<sms, 352, 140 * 1024>>>(nkb, d);
+  k<<<sms, 352, 140 * 1024>>>(nkb, d, rnd);
   cudaError_t err = cudaDeviceSynchronize();
   long long h[256];
   cudaMemcpy(h, d, sms * sizeof(long long), cudaMemcpyDeviceToHost);
   double mean = 0;
   for (int i = 0; i < sms; ++i) mean += h[i];
   mean /= sms;
-  printf("%-60s %s  %.1f clk/MMA\n", name, cudaGetErrorString(err), mean / (nkb * (double)Cfg<MODE>::KPB));
+  printf("%-60s rnd=%d %s  %.1f clk/MMA\n", name, rnd, cudaGetErrorString(err), mean / (nkb * (double)Cfg<MODE>::KPB));
+  fflush(stdout);
   cudaFree(d);
 }
 
@@ -165,6 +179,10 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<1>("1: issue + commit per K-block, no waits", sms);
+  run<1>("1: issue + commit per K-block, no waits", sms, 1);
+  run<1>("1: issue + commit per K-block, no waits", sms, 2);
+  run<11>("11: 8 with 16 MMAs per K-block, 2 stages", sms, 1);
+  run<11>("11: 8 with 16 MMAs per K-block, 2 stages", sms, 2);
   run<2>("2: + converter handoff (a_full/a_free, 4 stages), lane-0 wait", sms);
   run<3>("3: + 6 spinning warps", sms);
   run<4>("4: handoff, all 32 MMA-warp lanes wait", sms);

@@ -181,6 +181,7 @@ def _a32(x_idx, x_val, g, mu):
 
 @pytest.mark.parametrize("N,s", [(1024, 16), (16384, 128), (262144, 1024), (1001, 37), (5, 3), (1, 1),
                                  (100, 100), (100, 150), (3000, 0), (131073, 64), (262145, 1024),   # fused cluster
+                                 (262144, 5000), (20000, 4500),        # fused, > 4096 candidates: per-pass path
                                  (300000, 100), (300000, 7000)])                                   # multi-kernel
 def test_threshold_exact_selection(N, s):
     """Selection on identical fp32 a is exact: GPU H_s = oracle H_s of the same a."""
@@ -208,6 +209,23 @@ def test_threshold_ties_and_zeros():
     many = np.full(70000, 0.5, np.float32)                           # massive tie
     idx, _ = _thr([], [], many, 1.0, 1000)
     assert idx.tolist() == list(range(1000))
+
+
+@pytest.mark.parametrize("N", [16384, 65536, 262144])
+def test_threshold_ties_across_cluster(N):
+    """Gathered select (few candidates): ties at T spread over every CTA of the cluster;
+    the lowest indices win across CTA boundaries."""
+    rng = np.random.default_rng(N)
+    g = (0.01 * rng.standard_normal(N)).astype(np.float32)
+    tie = np.sort(rng.choice(N, 300, replace=False))
+    g[tie] = np.where(rng.random(300) < 0.5, 2.0, -2.0).astype(np.float32)
+    big = tie[::7][:20]
+    g[big] = 3.0
+    idx, val = _thr([], [], g, 1.0, 100)
+    ri, rv = OI.hard_threshold(g.astype(np.float64), 100)
+    np.testing.assert_array_equal(idx, ri)
+    rest = [i for i in tie if i not in set(big.tolist())][:80]
+    assert sorted(big.tolist() + rest) == idx.tolist()
 
 
 def test_threshold_nan_domain_error():

@@ -195,8 +195,11 @@ def radio_phi(pos, wavelength, grid):
 
 
 def radio_problem(*, cfg_id, A=48, radius_m=30.0, freq_hz=150e6, grid=256, n_src=64, n_iter=200,
-                  b_phi=2, b_y=8, K=2, noise_frac=0.01, name=None, batch=1):
+                  b_phi=2, b_y=8, K=2, noise_frac=0.01, name=None, batch=1, mu_scale=0.1):
     """Synthetic radio interferometer (BASELINE config 3, batch=64 -> config 5).
+    Fixed step mu = mu_scale / M (reading c9): the columns have |Phi_kp| = 1, so 1/M
+    normalises them, but the coherent radio Phi diverges at 1/M and 1/4M (|x| -> inf,
+    scripts/step_study.py); 1/10 M stays bounded.
     Sources: n_src pixels drawn without replacement among pixels with
     l^2 + m^2 < 1 (reading c19), log-normal(0,1) fluxes; complex noise
     e = (sigma/sqrt 2)(n1 + i n2), sigma = noise_frac * rms visibility (c17)."""
@@ -217,7 +220,7 @@ def radio_problem(*, cfg_id, A=48, radius_m=30.0, freq_hz=150e6, grid=256, n_src
         ys.append((vis + e).astype(np.complex64))
     M = A * A
     spec = ProblemSpec(name or f"radio-{A}ant-{grid}px", cfg_id, M, grid * grid, True, n_src, n_iter,
-                       1.0 / M, b_phi, b_y, K, quant_seed(cfg_id), xs[0], vs[0], ys[0], phi)
+                       mu_scale / M, b_phi, b_y, K, quant_seed(cfg_id), xs[0], vs[0], ys[0], phi)
     spec.meta.update(antennas=pos, wavelength=wavelength, l=l, m=m)
     if batch > 1:
         spec.meta.update(batch_x_idx=xs, batch_x_val=vs, batch_y=np.stack(ys, axis=1))
@@ -227,7 +230,9 @@ def radio_problem(*, cfg_id, A=48, radius_m=30.0, freq_hz=150e6, grid=256, n_src
 # BASELINE.json configs (index = cfg_id)
 CONFIGS = {
     1: dict(kind="gauss", M=256, N=1024, s=16, values="normal", n_iter=100, b_phi=4, b_y=8),
-    2: dict(kind="gauss", M=4096, N=16384, s=128, values="sign", n_iter=200, b_phi=2, b_y=8),
+    # config 2: BASELINE states no step; mu = 1 diverges at 2 bits (|x| -> inf by iteration
+    # 195, scripts/step_study.py), mu = 1/4 recovers the support (reading c9)
+    2: dict(kind="gauss", M=4096, N=16384, s=128, values="sign", n_iter=200, b_phi=2, b_y=8, mu=0.25),
     3: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8),
     4: dict(kind="gauss", M=65536, N=262144, s=1024, values="normal", n_iter=100, b_phi=4, b_y=8),
     5: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8, batch=64),
@@ -247,7 +252,7 @@ def config_problem(cfg_id, K=None, materialize=None, b_phi=None):
         if materialize is None:
             materialize = cfg_id != 4
         return gaussian_problem(c["M"], c["N"], c["s"], cfg_id=cfg_id, values=c["values"],
-                                n_iter=c["n_iter"], b_phi=c["b_phi"], b_y=c["b_y"], K=K,
+                                n_iter=c["n_iter"], mu=c.get("mu", 1.0), b_phi=c["b_phi"], b_y=c["b_y"], K=K,
                                 materialize=materialize, name=f"config{cfg_id}")
     if K is None:
         K = 2 * c["n_iter"]
