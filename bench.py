@@ -233,8 +233,11 @@ def main():
     else:
         y_shard = p.y[row0:row0 + rows]
     y_dev = torch.from_numpy(y_shard).to(dev)
+    # the timed solver has no profiling events in its graph (they would separate the kernels
+    # and defeat programmatic dependent launch); a second, profiled solver over the same
+    # pool times the adjoint launches for the roofline after the timed region
     sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, adjoint_variant=args.variant, comm=comm,
-                     profile=True, nrhs=B, adaptive=args.adaptive)
+                     profile=False, nrhs=B, adaptive=args.adaptive)
     setup_s = time.perf_counter() - t_setup
 
     # ---- device-resident timed region -----------------------------------------------
@@ -259,7 +262,13 @@ def main():
     barrier()
     clocks = clk.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    adj_ms = sol.adjoint_times_ms()
+    sol_prof = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, adjoint_variant=args.variant, comm=comm,
+                          profile=True, nrhs=B, adaptive=args.adaptive)
+    for _ in range(2):
+        sol_prof.run(y_dev)
+    torch.cuda.synchronize()
+    adj_ms = sol_prof.adjoint_times_ms()
+    sol_prof.close()
     out_idx, out_val, out_nnz = sol.out_idx, sol.out_val, sol.out_nnz
     nnz = [int(v) for v in out_nnz.cpu()]
     if min(nnz) < 0:   # a poisoned (non-finite) iterate lets kernels exit early: not a valid run
@@ -323,8 +332,8 @@ def main():
                 "algorithmic_ops_per_launch": adj_ops,
                 "executed_int8_ops_per_launch": 2 * adj_ops, "avg_launch_ms": adj_avg,
                 "launches_timed": len(adj_ms), "code_bytes_per_launch": copy_bytes,
-                "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside the "
-                       "solver graph, last timed step; ops = 2 R N B useful (x2 executed: two int8 limbs of r)"}
+                "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside a "
+                       "profiled copy of the solver graph (run after the timed region); ops = 2 R N B useful (x2 executed: two int8 limbs of r)"}
 
     if rank != 0:
         return 0
@@ -371,7 +380,7 @@ def main():
                      "peak_kind": peak_kind, "traffic": traffic,
                      "algorithmic_bytes_per_launch": adj_bytes, "avg_launch_ms": adj_avg,
                      "launches_timed": len(adj_ms),
-                     "how": "CUDA event pair around every adjoint inside the solver graph, last timed step"},
+                     "how": "CUDA event pair around every adjoint inside a profiled copy of the solver graph, run after the timed region"},
         "cpu_baseline": cb,
         "e2e": e2e,
         "gpu_launches": int(launches_per_run * args.steps),
