@@ -132,7 +132,8 @@ struct AdjArgs {
   int64_t N;
   int64_t Rpad;          // stacked rows (incl. padding)
   int KR;                // rows per K-range (CTA pass), multiple of 256, <= kMaxKR
-  int KC;                // rows per fixed-point chunk, divides KR
+  int KRp;               // KR rounded up to whole 1024-row requests (limb planes; rows >= KR are zero)
+  int KC;                // rows per fixed-point chunk, divides KRp
   int nK;                // number of K-ranges
   int L;
   float sigma;
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   constexpr int KSTEP = 4 * RPC;         // rows per warp k-step (4 lanes t)
   constexpr int NMMA = 2 * P;            // MMAs per k-step
   extern __shared__ __align__(16) uint8_t smem[];
-  const int nchunks = a.KR / a.KC;
+  const int nchunks = a.KRp / a.KC;
   uint8_t* ring = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMmaWarps * kRing * kSlot);   // [warp][slot]
   uint8_t* limbs = smem + kMmaWarps * kRing * kSlot + kMmaWarps * kRing * 8;
@@ -225,7 +226,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   const int64_t ntask = (a.N + 15) / 16;
   const int64_t wid = (int64_t)blockIdx.x * kMmaWarps + warp;
   const int64_t wstride = (int64_t)gridDim.x * kMmaWarps;
-  const int nsteps = (int)(min64(a.KR, a.Rpad - row0) / KSTEP);     // last K-range may be short
+  const int64_t rend = min64(row0 + a.KR, a.Rpad);                 // rows of this K-range
+  const int nsteps = (int)((rend - row0) / KSTEP);                  // last K-range may be short
   const uint8_t* kbase = a.codes + (row0 * B / 8 >> 6) * 1024 + t * 16;   // K-range offset in a tile
   auto task_ptr = [&](int64_t task, const uint8_t*& b0, const uint8_t*& b1) {
     const uint8_t* b = kbase + task * 16 * a.strip_bytes;
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
     unsigned int m = 0;
     for (int i = tid; i < a.KC; i += blockDim.x) {
       const int64_t row = row0 + (int64_t)c * a.KC + i;
-      if (row < a.Rpad) m = max(m, __float_as_uint(__ldg(a.r + row)) & 0x7FFFFFFFu);
+      if (row < rend) m = max(m, __float_as_uint(__ldg(a.r + row)) & 0x7FFFFFFFu);
     }
     m = __reduce_max_sync(0xffffffffu, m);
     if (lane == 0) red[c * kMmaWarps + warp] = __uint_as_float(m);
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   // ---- prologue 2: r -> three balanced signed 8-bit limbs, permuted per lane chunk -----
   // item = (lane chunk ch, byte-register rho): rows ch*RPC + pos(rho, i), i = 0..3
   {
-    const int items = a.KR / RPC * (4 * P);
+    const int items = a.KRp / RPC * (4 * P);
     for (int it = tid; it < items; it += blockDim.x) {
       const int ch = it / (4 * P), rho = it % (4 * P);
       const int base = ch * RPC + (rho / P) * (32 / B) + (rho % P);
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int64_t row = row0 + base + P * i;
-        const float rv = row < a.Rpad ? __ldg(a.r + row) : 0.0f;
+        const float rv = row < rend ? __ldg(a.r + row) : 0.0f;   // zero limbs past the K-range
         const int ri = __float2int_rn(rv * scale);            // exact power-of-two scaling
         const int l0 = ((ri + 128) & 255) - 128;
         const int t1 = (ri - l0) >> 8;
@@ -438,12 +440,12 @@ __global__ void adjoint_reduce_kernel(const float* __restrict__ part, int nK, in
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float s = part[n];
-  for (int k = 1; k < nK; ++k) s += part[(int64_t)k * N + n];
-  g[n] = sigma * s;
+  for (int k = 1; k < nK; ++k) s = __fadd_rn(s, part[(int64_t)k * N + n]);   // thr_cluster_kernel: same order
+  g[n] = __fmul_rn(sigma, s);
 }
 
 struct AdjPlan {
-  int KR, KC, nK, limb_stride;
+  int KR, KRp, KC, nK, limb_stride;
   size_t smem;
   int ctas_x;
 };
@@ -457,21 +459,24 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   // tasks to give every warp of the GPU several tasks.
   // K-ranges and chunks are whole multiples of 1024 rows so that every chunk holds a
   // multiple of kPF k-steps for b = 2, 4, 8 (k-step = 512/b rows)
-  int64_t KR = min64(Rpad, kMaxKR);
-  KR = (KR + 1023) / 1024 * 1024;
-  while (KR > 1024 && ntask * ((Rpad + KR - 1) / KR) < 4 * warps_full) KR = (KR / 2 + 1023) / 1024 * 1024;
+  // nK equal K-ranges of KR rows (a multiple of 256, so a whole number of k-steps at every
+  // bit width); each CTA's limb planes are padded to whole 1024-row requests with zero limbs.
+  int64_t nK = (Rpad + kMaxKR - 1) / kMaxKR;
+  while (ntask * nK < 4 * warps_full && Rpad / (nK + 1) >= 1024) ++nK;
+  int64_t KR = ((Rpad + nK - 1) / nK + 255) / 256 * 256;
   {
     static int kr_env = -1;                       // profiling override (IHT_ADJ_KR, rows)
     if (kr_env < 0) kr_env = getenv("IHT_ADJ_KR") ? atoi(getenv("IHT_ADJ_KR")) : 0;
     if (kr_env >= 1024) KR = min64((int64_t)kr_env / 1024 * 1024, kMaxKR);
   }
   p.KR = (int)KR;
-  int d = 4;                            // KC = 1024 d <= kChunkRows, dividing KR
-  while ((KR / 1024) % d) --d;
+  p.KRp = (int)((KR + 1023) / 1024 * 1024);
+  int d = 4;                            // KC = 1024 d <= kChunkRows, dividing KRp
+  while ((p.KRp / 1024) % d) --d;
   p.KC = 1024 * d;
   p.nK = (int)((Rpad + KR - 1) / KR);
-  p.limb_stride = p.KR + 64;
-  const int nchunks = p.KR / p.KC;
+  p.limb_stride = p.KRp + 64;
+  const int nchunks = p.KRp / p.KC;
   p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
            sizeof(float) * nchunks * kMmaWarps + 16;
   int per_sm = (int)(size_t)min64(4, (size_t)(227 * 1024) / p.smem);
@@ -502,8 +507,22 @@ extern "C" int64_t iht_adjoint_ws_bytes(const iht_qmat* A) {
   return p.nK > 1 ? (int64_t)p.nK * A->cols * (int64_t)sizeof(float) : 0;
 }
 
+static int adjoint_impl(const iht_qmat* A, const float* r, float* g, int variant, void* ws, int64_t ws_bytes,
+                        void* stream, int* nparts, float* gsigma);
+
 extern "C" int iht_adjoint(const iht_qmat* A, const float* r, float* g, int variant, void* ws,
                            int64_t ws_bytes, void* stream) {
+  return adjoint_impl(A, r, g, variant, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+int iht_adjoint_parts(const iht_qmat* A, const float* r, float* g, void* ws, int64_t ws_bytes, void* stream,
+                      int* nparts, float* gsigma) {
+  if (nparts == nullptr || gsigma == nullptr) return IHT_EINVAL;
+  return adjoint_impl(A, r, g, 0, ws, ws_bytes, stream, nparts, gsigma);
+}
+
+static int adjoint_impl(const iht_qmat* A, const float* r, float* g, int variant, void* ws, int64_t ws_bytes,
+                        void* stream, int* nparts, float* gsigma) {
   if (A == nullptr || r == nullptr || g == nullptr) return IHT_EINVAL;
   if (A->codes == nullptr || (A->bits != 2 && A->bits != 4 && A->bits != 8)) return IHT_EINVAL;
   if (A->strip_bytes != iht_strip_bytes(A->rows, A->planes, A->bits)) return IHT_EINVAL;
@@ -536,6 +555,7 @@ extern "C" int iht_adjoint(const iht_qmat* A, const float* r, float* g, int vari
   a.N = A->cols;
   a.Rpad = A->planes * rows_pad(A->rows);
   a.KR = p.KR;
+  a.KRp = p.KRp;
   a.KC = p.KC;
   a.nK = p.nK;
   a.L = L;
@@ -559,6 +579,11 @@ extern "C" int iht_adjoint(const iht_qmat* A, const float* r, float* g, int vari
   else IHT_ADJ0(8);
 #undef IHT_ADJ0
   IHT_LAUNCH_CHECK();
+  if (nparts) {                       // solver: the fused threshold sums the partials
+    *nparts = p.nK > 1 ? p.nK : 0;
+    *gsigma = sigma;
+    return IHT_OK;
+  }
   if (p.nK > 1) {
     IHT_CUDA_CHECK(launch_pdl(adjoint_reduce_kernel, dim3((unsigned)ceil_div<int64_t>(A->cols, 256)), dim3(256), 0,
                               st, static_cast<const float*>(ws), p.nK, A->cols, sigma, g));

@@ -26,6 +26,19 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
                              int64_t ws_bytes, void* stream);
 // Kernel launches one iht_threshold_batched call makes for N columns (fused cluster path: 1).
 int iht_threshold_launches(int64_t N);
+// Solver-internal split of iht_adjoint (variant 0): with nK > 1 K-ranges it leaves the
+// unscaled partials part[nK][N] in ws and skips adjoint_reduce_kernel; *nparts = nK (0 when
+// g was written directly), *gsigma = sigma.  The fused threshold then forms
+// g = sigma (part_0 + ... + part_{nK-1}) itself, in the reduce kernel's order and rounding.
+int iht_adjoint_parts(const iht_qmat* A, const float* r, float* g, void* ws, int64_t ws_bytes, void* stream,
+                      int* nparts, float* gsigma);
+// iht_threshold_batched_mu (nrhs = 1, fused path only) reading g as nparts partial planes
+// (stride N) scaled by gsigma, also storing that g into gout (may be NULL); nparts = 0 is
+// the plain call.
+int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                        const float* g, int nparts, float gsigma, float* gout, float mu, int32_t s, int64_t N,
+                        int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
+                        void* stream);
 
 namespace iht {
 

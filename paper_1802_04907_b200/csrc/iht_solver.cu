@@ -306,6 +306,12 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
   IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz, 0, sizeof(int32_t) * B, st));
   const int K = (int)S->pool.size();
   const int64_t xslot = (int64_t)B * s;
+  // single observation, fixed step, int8-MMA adjoint, no g all-reduce, fused threshold:
+  // the adjoint's split-K partials go straight to the threshold (one launch fewer)
+  const bool fuse_parts = !S->fresh && !S->batched && !S->rowshard && S->cfg.step_mode == 0 &&
+                          S->cfg.adjoint_variant == 0 && iht_threshold_launches(S->N) == 1;
+  int nparts = 0;
+  float gsigma = 1.0f;
   for (int n = 1; n <= S->cfg.n_iter; ++n) {
     const int in_slot = S->cfg.trace ? (n - 1) : ((n - 1) & 1);
     const int out_slot = S->cfg.trace ? n : (n & 1);
@@ -334,6 +340,11 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       if ((rc = iht_adjoint_fresh(&S->fm, 2 * n - 2, S->r, S->g, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
         return rc;
       L += 2;
+    } else if (!S->batched && fuse_parts) {
+      // split-K partials summed inside the fused threshold (no adjoint_reduce_kernel)
+      if ((rc = iht_adjoint_parts(&A, S->r, S->g, S->ws_adj, S->ws_adj_bytes, st, &nparts, &gsigma)) != IHT_OK)
+        return rc;
+      L += 1;
     } else if (!S->batched) {
       if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
         return rc;
@@ -349,6 +360,11 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
     // (a6) update + H_s
     if (S->cfg.step_mode == 1) {
       if ((rc = enqueue_adaptive(S, st, n, A, xi, xv, xn, oi, ov, on, &L)) != IHT_OK) return rc;
+    } else if (nparts > 0) {
+      if ((rc = iht_threshold_parts(xi, xv, xn, s, static_cast<const float*>(S->ws_adj), nparts, gsigma, S->g,
+                                    S->cfg.mu, s, S->N, oi, ov, s, on, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+        return rc;
+      L += 1;
     } else if (!S->colshard) {
       if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)

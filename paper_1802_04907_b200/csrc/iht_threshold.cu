@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
     int64_t N, int64_t col_offset, int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
-    int32_t ldo, int32_t* __restrict__ out_nnz, int probe) {
+    int32_t ldo, int32_t* __restrict__ out_nnz, int probe, int nparts, float gsigma, float* __restrict__ gout) {
   extern __shared__ __align__(16) unsigned char dsm[];
   float* as = reinterpret_cast<float*>(dsm);                                  // [slice] (multiple of 4)
   if (mu_dev) mu = mu_dev[blockIdx.y];
@@ -588,15 +588,43 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   __syncthreads();
   // ---- (1) a = mu g and the histogram of the top 11 key bits; float4 when aligned
   int nan = 0;
-  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 15) == 0);
+  // nparts > 0 (solver, split-K adjoint): g = sigma (part_0 + ... + part_{P-1}), planes N
+  // apart, summed in adjoint_reduce_kernel's order and rounding
+  const bool vec = ((reinterpret_cast<uintptr_t>(g + lo) & 15) == 0) && (nparts == 0 || (N & 3) == 0);
   const int n4 = vec ? (n >> 2) : 0;
   constexpr int kLd = 8;                 // float4 loads in flight per thread (g is read once)
+  auto gsum1 = [&](int64_t e) {
+    if (nparts == 0) return __ldg(g + e);
+    float t = __ldg(g + e);
+    for (int k = 1; k < nparts; ++k) t = __fadd_rn(t, __ldg(g + (int64_t)k * N + e));
+    return __fmul_rn(gsigma, t);
+  };
   for (int i0 = 0; i0 < n4; i0 += kClThreads * kLd) {
     float4 v[kLd];
 #pragma unroll
     for (int u = 0; u < kLd; ++u) {
       const int i = i0 + u * kClThreads + tid;
       v[u] = i < n4 ? __ldg(reinterpret_cast<const float4*>(g + lo) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (nparts > 0) {
+      for (int k = 1; k < nparts; ++k) {
+#pragma unroll
+        for (int u = 0; u < kLd; ++u) {
+          const int i = i0 + u * kClThreads + tid;
+          if (i < n4) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(g + (int64_t)k * N + lo) + i);
+            v[u] = make_float4(__fadd_rn(v[u].x, w.x), __fadd_rn(v[u].y, w.y), __fadd_rn(v[u].z, w.z),
+                               __fadd_rn(v[u].w, w.w));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kLd; ++u) {
+        const int i = i0 + u * kClThreads + tid;
+        v[u] = make_float4(__fmul_rn(gsigma, v[u].x), __fmul_rn(gsigma, v[u].y), __fmul_rn(gsigma, v[u].z),
+                           __fmul_rn(gsigma, v[u].w));
+        if (gout && i < n4) reinterpret_cast<float4*>(gout + lo)[i] = v[u];   // g materialised once
+      }
     }
 #pragma unroll
     for (int u = 0; u < kLd; ++u) {
@@ -615,7 +643,9 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     }
   }
   for (int i = (n4 << 2) + tid; i < n; i += kClThreads) {
-    const float a1 = __fmul_rn(mu, g[lo + i]);
+    const float gv = gsum1(lo + i);
+    if (gout && nparts > 0) gout[lo + i] = gv;
+    const float a1 = __fmul_rn(mu, gv);
     as[i] = a1;
     const unsigned int k = __float_as_uint(a1) & 0x7FFFFFFFu;
     nan |= k > 0x7F800000u;
@@ -833,10 +863,32 @@ static int thr_attrs() {
   return IHT_OK;
 }
 
+static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                          const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
+                          int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
+                          int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream);
+
 int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                              const float* g, float mu, const float* mu_dev, int32_t s, int64_t N, int64_t col_offset,
                              int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws,
                              int64_t ws_bytes, void* stream) {
+  return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, mu_dev, s, N, col_offset, nrhs, out_idx,
+                        out_val, ldo, out_nnz, ws, ws_bytes, stream);
+}
+
+int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                        const float* g, int nparts, float gsigma, float* gout, float mu, int32_t s, int64_t N,
+                        int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
+                        void* stream) {
+  if (nparts < 0 || (nparts > 0 && iht_threshold_launches(N) != 1)) return IHT_EUNSUPPORTED;
+  return threshold_impl(x_idx, x_val, x_nnz, ldx, g, nparts, gsigma, gout, mu, nullptr, s, N, 0, 1, out_idx, out_val,
+                        ldo, out_nnz, ws, ws_bytes, stream);
+}
+
+static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                          const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
+                          int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
+                          int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream) {
   if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr ||
       s < 0 || N <= 0 || N > 0x7FFFFFFFll || nrhs <= 0 || nrhs > 65535 || ldo < s || ldx < 0 ||
       col_offset < 0 || col_offset + N > 0x7FFFFFFFll)
@@ -877,7 +929,8 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
     lc.attrs = at;
     lc.numAttrs = 2;
     IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
-                                      N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe()));
+                                      N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe(), nparts,
+                                      gsigma, gout));
     return IHT_OK;
   }
   ThrWs w{};

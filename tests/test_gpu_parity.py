@@ -255,6 +255,9 @@ CASES = {
                                             mu=0.15, K=60),
     "radio": lambda: G.radio_problem(cfg_id=23, A=12, grid=48, n_src=10, n_iter=30, K=60),
     "gauss8bit": lambda: G.gaussian_problem(700, 3001, 20, cfg_id=22, b_phi=8, n_iter=25, K=4),
+    # 3 K-ranges of the int8-MMA adjoint: the solver sums the split-K partials inside the
+    # fused threshold (no reduce kernel)
+    "splitk": lambda: G.gaussian_problem(2100, 4096, 20, cfg_id=24, b_phi=4, n_iter=15, mu=0.6, K=30),
 }
 
 
