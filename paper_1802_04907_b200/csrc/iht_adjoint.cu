@@ -125,6 +125,7 @@ constexpr int kMaxKR = 32768;          // rows of r limbs resident in shared mem
 constexpr int kReq = 4;                // k-steps (1 KiB tile-steps) per bulk request
 constexpr int kRing = 3;               // requests in flight per warp (shared-memory ring slots)
 constexpr int kSlot = kReq * 1024;     // bytes per ring slot
+static_assert(kMmaWarps * 32 == 256, "the prologue loops assume 256 threads");
 
 struct AdjArgs {
   const uint8_t* codes;
@@ -270,25 +271,40 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
 #pragma unroll 1
   for (int j = 0; j < kRing; ++j) request(j);
 
+  unsigned int* cmax = reinterpret_cast<unsigned int*>(red);   // [nchunks] max |r| bit pattern
+  for (int c = tid; c < nchunks; c += blockDim.x) cmax[c] = 0u;
+  if (tid == 0) nonfinite = 0;
+  __syncthreads();
   // the code requests above read only the (constant) copy; r comes from the forward kernel
   pdl_wait();
   // ---- prologue 1: per-chunk max |r| -> exponent F_c ---------------------------------
   // (max over |r| bit patterns: a NaN or inf in r is caught and makes g NaN, so that H_s
-  // reports the domain error)
-  if (tid == 0) nonfinite = 0;
-  for (int c = 0; c < nchunks; ++c) {
-    unsigned int m = 0;
-    for (int i = tid; i < a.KC; i += blockDim.x) {
-      const int64_t row = row0 + (int64_t)c * a.KC + i;
-      if (row < rend) m = max(m, __float_as_uint(__ldg(a.r + row)) & 0x7FFFFFFFu);
+  // reports the domain error).  float4 loads, 8 in flight per thread: a 1024-row
+  // group (256 float4) never straddles a chunk (KC is a multiple of 1024), so the chunk of
+  // each load is warp-uniform and one warp max + one shared atomicMax per load suffice.
+  {
+    const int n4 = (int)((rend - row0) >> 2);             // real rows (multiple of 256) / 4
+    const float4* r4 = reinterpret_cast<const float4*>(a.r + row0);
+    for (int j0 = 0; j0 < n4; j0 += 256 * 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * 256 + tid;
+        v[u] = j < n4 ? __ldg(r4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (j0 + u * 256 >= n4) break;
+        unsigned int m = max(max(__float_as_uint(v[u].x) & 0x7FFFFFFFu, __float_as_uint(v[u].y) & 0x7FFFFFFFu),
+                             max(__float_as_uint(v[u].z) & 0x7FFFFFFFu, __float_as_uint(v[u].w) & 0x7FFFFFFFu));
+        m = __reduce_max_sync(0xffffffffu, m);
+        if (lane == 0 && m) atomicMax(&cmax[((j0 + u * 256) * 4) / a.KC], m);
+      }
     }
-    m = __reduce_max_sync(0xffffffffu, m);
-    if (lane == 0) red[c * kMmaWarps + warp] = __uint_as_float(m);
   }
   __syncthreads();
   for (int c = tid; c < nchunks; c += blockDim.x) {
-    unsigned int mb = 0;
-    for (int w = 0; w < kMmaWarps; ++w) mb = max(mb, __float_as_uint(red[c * kMmaWarps + w]));
+    unsigned int mb = cmax[c];
     if (mb >= 0x7F800000u) {
       nonfinite = 1;
       mb = 0;
@@ -303,18 +319,35 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   // ---- prologue 2: r -> three balanced signed 8-bit limbs, permuted per lane chunk -----
   // item = (lane chunk ch, byte-register rho): rows ch*RPC + pos(rho, i), i = 0..3
   {
+    // items = KRp / 4, a multiple of 256: every warp runs the same trip count.  The r loads
+    // of kIt items per thread are issued before any of them is converted.
+    constexpr int kIt = 4;
     const int items = a.KRp / RPC * (4 * P);
-    for (int it = tid; it < items; it += blockDim.x) {
+    for (int it0 = tid; it0 < items; it0 += kIt * 256) {
+    float rvs[kIt][4];
+#pragma unroll
+    for (int q = 0; q < kIt; ++q) {
+      const int it = it0 + q * 256;
       const int ch = it / (4 * P), rho = it % (4 * P);
       const int base = ch * RPC + (rho / P) * (32 / B) + (rho % P);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t row = row0 + base + P * i;
+        rvs[q][i] = (it < items && row < rend) ? __ldg(a.r + row) : 0.0f;   // zero limbs past the K-range
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kIt; ++q) {
+      const int it = it0 + q * 256;
+      if (it >= items) break;                                 // warp-uniform
+      const int ch = it / (4 * P), rho = it % (4 * P);
       const int c = (ch * RPC) / a.KC;
       const float scale = ldexpf(1.0f, Fc[c]);
       uint32_t l0w = 0, l1w = 0, l2w = 0;
       int s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int64_t row = row0 + base + P * i;
-        const float rv = row < rend ? __ldg(a.r + row) : 0.0f;   // zero limbs past the K-range
+        const float rv = rvs[q][i];
         const int ri = __float2int_rn(rv * scale);            // exact power-of-two scaling
         const int l0 = ((ri + 128) & 255) - 128;
         const int t1 = (ri - l0) >> 8;
@@ -339,6 +372,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         atomicAdd(&Sl[3 * c + 1], s1);
         atomicAdd(&Sl[3 * c + 2], s2);
       }
+    }
     }
   }
   __syncthreads();
