@@ -117,6 +117,8 @@ struct BatchArgs {
   int nkb;                 // K-blocks = ceil(Rpad / KBR); the last may be ragged (fewer tile-steps)
   int ksteps;              // tile-steps of a strip = Rpad / (512 / b)
   int ntiles;              // ceil(N / 128)
+  int nfull;               // work units [0, nfull): whole tiles u; then 2 (ntiles - nfull) half units:
+  int nunits;              // tile nfull + (u - nfull) / 2, snapshot half (u - nfull) & 1 (N = B MMA columns)
   int B;                   // MMA snapshots (padded to a multiple of 8; 2B <= 128)
   int Breal;               // snapshots actually written (<= B)
   int probe;               // 0; profiling probes (IHT_BATCHED_PROBE): 1 no B copies, 2 no MMAs, 4 no TMEM
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     int ps = 0, ss = 0;
     uint32_t pph = 0, sph = 0;
     bool s_wrapped = false;
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < a.nunits; u += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
         if (a.probe & 64) {                       // probe 64: no handoffs after the first round
           if (!s_wrapped) {
@@ -293,12 +295,16 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     (void)CH;
   } else if (warp == 4) {
     // ---------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = idesc_i8(kBT, NB);
     int ss = 0;
     uint32_t sph = 0;
     int t = 0;
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+    for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++t) {
       const int ab = t & 1;
+      const int half = u < a.nfull ? -1 : ((u - a.nfull) & 1);
+      // a half unit multiplies the tile by snapshot-limb rows [half NB/2, (half+1) NB/2) of B:
+      // an 8 KiB-aligned offset inside every SW128 atom column (8-row groups of 1 KiB)
+      const uint32_t idesc = idesc_i8(kBT, half < 0 ? NB : NB / 2);
+      const uint32_t hoff = half < 0 ? 0u : (uint32_t)(half * NB * 64);
       if (t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t] = clock64();
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         // warp-uniform operands (shuffled from lane 0 so the compiler keeps them uniform)
         const uint32_t atm_u = __shfl_sync(0xffffffffu, tmem + a_col0 + (uint32_t)(ss * ACOLS), 0);
-        const uint32_t bbase_u = __shfl_sync(0xffffffffu, smem_u32(sB + ss * BSZ), 0);
+        const uint32_t bbase_u = __shfl_sync(0xffffffffu, smem_u32(sB + ss * BSZ) + hoff, 0);
         const uint32_t dtm_u = __shfl_sync(0xffffffffu, dtm, 0);
         const uint32_t idesc_u = __shfl_sync(0xffffffffu, idesc, 0);
         const uint32_t acc0_u = __shfl_sync(0xffffffffu, kb > 0 ? 1u : 0u, 0);
@@ -356,7 +362,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     uint32_t ph = 0;
     bool wrapped = false;
     const int64_t last_tile = (a.N + 15) / 16 - 1;
-    for (int tile = (a.probe & (8 | 64)) ? a.ntiles : blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    for (int u = (a.probe & (8 | 64)) ? a.nunits : blockIdx.x; u < a.nunits; u += gridDim.x) {
+      const int tile = u < a.nfull ? u : a.nfull + ((u - a.nfull) >> 1);
       for (int kb = 0; kb < a.nkb; ++kb) {
         const int tsn = min(TS, a.ksteps - kb * TS);
         const uint32_t bytes = (uint32_t)(tsn * 1024);
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     int ss = 0;
     uint32_t sph = 0;
     bool wrapped = false;
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < a.nunits; u += gridDim.x) {
       for (int kb = 0; kb < a.nkb; ++kb) {
         if (a.probe & 64) {                       // probe 64: fill the stages once, then stop
           if (wrapped) break;
@@ -401,13 +408,17 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     // ---------------------------------------------------------------- epilogue (warps 7-10)
     const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
     int t = 0;
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+    for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++t) {
       const int ab = t & 1;
+      const int tile = u < a.nfull ? u : a.nfull + ((u - a.nfull) >> 1);
+      const int half = u < a.nfull ? -1 : ((u - a.nfull) & 1);
+      const int ncol = half < 0 ? NB : NB / 2;          // accumulator columns of this unit
+      const int cbase = half < 0 ? 0 : half * (NB / 2);  // its first snapshot-limb column
       mbar_wait2(smem_u32(&acc_full[ab]), (uint32_t)((t >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t n = (int64_t)tile * kBT + quarter * 32 + lane;
       const uint32_t taddr = tmem + ab * acc_stride + ((uint32_t)(quarter * 32) << 16);
-      for (int c0 = 0; c0 < ((a.probe & 16) ? 0 : NB); c0 += 16) {   // probe 16: no epilogue work
+      for (int c0 = 0; c0 < ((a.probe & 16) ? 0 : ncol); c0 += 16) {   // probe 16: no epilogue work
         uint32_t v[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -420,14 +431,14 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           if (a.ep32) {
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {
-              const int b = (c0 + e) >> 1;
+              const int b = (cbase + c0 + e) >> 1;
               const int W = 2 * ((int)v[e] + (int)v[e + 1] * 256) - ep_off32[b];
               if (b < a.Breal) a.g[(int64_t)b * a.N + n] = __fmul_rn(__int2float_rn(W), ep_scale[b]);
             }
           } else {
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {
-              const int b = (c0 + e) >> 1;
+              const int b = (cbase + c0 + e) >> 1;
               const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
               if (b < a.Breal) a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
             }
@@ -616,6 +627,20 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     b.nkb = nkb;
     b.ksteps = ksteps;
     b.ntiles = (int)((A->cols + kBT - 1) / kBT);
+    // last partial wave: split its tiles into snapshot halves (N = B MMA columns) when that
+    // fits one more wave, so no CTA runs a whole extra tile (config 5: 512 tiles on 148 SMs,
+    // 4 -> 3.5 tile-times); the A codes of a split tile are converted by both halves
+    {
+      const int grid = min(b.ntiles, sms), tail = b.ntiles % grid;
+      b.nfull = b.ntiles;
+      b.nunits = b.ntiles;
+      static int split_env = -1;                  // profiling override (IHT_BATCHED_SPLIT=0: off)
+      if (split_env < 0) split_env = getenv("IHT_BATCHED_SPLIT") ? atoi(getenv("IHT_BATCHED_SPLIT")) : 1;
+      if (split_env && b.ntiles > grid && tail > 0 && 2 * tail <= grid && (2 * bp) % 32 == 0) {
+        b.nfull = b.ntiles - tail;
+        b.nunits = b.nfull + 2 * tail;
+      }
+    }
     b.B = bp;
     b.Breal = nb;
     b.probe = probe_flags();
@@ -652,7 +677,7 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
       static long long h[1024 * 64];
       cudaStreamSynchronize(st);
       cudaMemcpy(h, b.tlog, sizeof(long long) * 64 * min(b.ntiles, sms), cudaMemcpyDeviceToHost);
-      for (int c : {0, 1, 100}) {
+      for (int c : {0, 1, 100, 140}) {
         if (c >= min(b.ntiles, sms)) continue;
         const long long* r = h + c * 64;
         const long long t0 = r[63];

@@ -66,7 +66,9 @@ def test_absmax_and_quantize_vec_batched_bit_exact(cplx, bits, B):
 # ------------------------------------------------------------------ (a7) batched adjoint
 BADJ = [(300, 500, False, 2, 8), (144, 2304, True, 2, 8), (1000, 1000, False, 4, 16), (1000, 700, False, 8, 16),
         (2304, 1500, True, 2, 64), (513, 129, True, 4, 24), (256, 16, False, 2, 8), (300, 500, False, 2, 5),
-        (144, 300, True, 2, 72)]
+        (144, 300, True, 2, 72),
+        # more tiles than SMs: the last partial wave runs as snapshot halves (N = B columns)
+        (256, 22784, False, 2, 16), (100, 24000, True, 8, 48), (100, 24000, True, 4, 40)]
 
 
 @pytest.mark.parametrize("M,N,cplx,bits,B", BADJ)
