@@ -57,8 +57,8 @@ def _compile(src, obj, verbose):
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")
     log = obj + ".ptxas.txt"
-    with open(log, "w") as f:
-        f.write(res.stderr)
+    with open(log, "w") as f:      # register / spill / smem report (compile times dropped: stable diffs)
+        f.write("".join(l for l in res.stderr.splitlines(True) if "Compile time" not in l))
     if verbose:
         print(f"[build] {os.path.basename(src)}", file=sys.stderr)
     return obj
