@@ -7,6 +7,7 @@ mkdir -p $OUT
 for args in "--config 4" "--config 4 --bits 2 --no-cpu-baseline" "--config 4 --bits 8 --no-cpu-baseline" \
             "--config 5" "--config 5 --bits 4 --no-cpu-baseline" "--config 5 --bits 8 --no-cpu-baseline" \
             "--config 2" "--config 3" "--config 1" "--config 2 --adaptive --no-cpu-baseline" \
+            "--config 2 --fresh --no-cpu-baseline" \
             "--config 4 --variant 1 --no-cpu-baseline --no-e2e --steps 3"; do
   name=$(echo "$args" | tr -d ' -' )
   timeout 900 python bench.py $args > $OUT/${TAG}_${name}.json 2> $OUT/${TAG}_${name}.err
