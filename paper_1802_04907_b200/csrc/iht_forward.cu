@@ -6,10 +6,10 @@
 // strips each support column is a contiguous run of R codes, so the scale-and-add
 // streams s * R * b / 8 bytes (0.4% of the adjoint's bytes at config 4).
 //
-// Mapping: a CTA owns a window of 8 consecutive 32-bit code words of every strip
-// (8 * 32/b stacked rows); each warp load instruction covers 4 support columns x 8 words
-// (one 32-byte sector per column), 8 such loads in flight per lane; partial sums are
-// combined in a fixed order (shuffles, then shared memory), so r is deterministic.
+// Mapping: a CTA owns a window of WPC = 8 (or 32) consecutive 32-bit code words of every
+// strip (WPC * 32/b stacked rows); each warp load instruction covers 32/WPC support
+// columns x WPC words, 8 such loads in flight per lane; partial sums are combined in a
+// fixed order (shuffles, then shared memory), so r is deterministic.
 // Batched (config 5): grid row blockIdx.y = snapshot b, with its own x_b, y-hat_b, r_b.
 // Column shards: x holds GLOBAL indices; only [col_offset, col_offset + cols) are local.
 #include "iht_internal.cuh"
@@ -17,7 +17,9 @@
 namespace iht {
 
 constexpr int kFwdThreads = 256;       // 8 warps
-constexpr int kFwdWords = 8;           // 32-bit code words (8 * 32/b rows) per CTA and plane chunk
+// WPC = 32-bit code words (WPC * 32/b rows) per CTA: 8 (lane = 4 column slots x 8 words),
+// or 32 for many small batched problems (lane = word, one column per warp load, 4x fewer
+// CTAs: config 5's 64 snapshots x 36 CTAs at 64 registers per thread were 3.9 waves)
 constexpr int kFwdUnroll = 8;          // support columns in flight per lane
 constexpr int kFwdStage = 1536;        // support entries staged in shared memory per round (18 KiB)
 
@@ -26,7 +28,7 @@ constexpr int kFwdStage = 1536;        // support entries staged in shared memor
 // The snapshot's support (idx, val) is staged in shared memory first, so the code loads
 // depend on a shared-memory read only.  Partial sums: shuffle over the 4 column slots,
 // then over the 8 warps through shared memory, both in a fixed order (deterministic).
-template <int B>
+template <int B, int kFwdWords>
 __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     const uint8_t* __restrict__ codes, int64_t strip_bytes, int64_t words_total, int rows, int rpad, int L,
     float sigma, const int32_t* __restrict__ x_idx, const float* __restrict__ x_val,
@@ -40,7 +42,8 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   pdl_launch_dependents();
   pdl_wait();                                   // x (previous H_s) and y-hat
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = lane >> 3, wl = lane & 7;
+  constexpr int CS = 32 / kFwdWords;            // column slots per warp load
+  const int c = lane / kFwdWords, wl = lane % kFwdWords;
   const int b = blockIdx.y;
   x_idx += (int64_t)b * ldx;
   x_val += (int64_t)b * ldx;
@@ -70,20 +73,20 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     sval[j] = ok ? x_val[st0 + j] : 0.0f;
   }
   __syncthreads();
-  for (int jb = warp * 4; jb < nst; jb += 32 * kFwdUnroll) {   // warp-uniform trip count
+  for (int jb = warp * CS; jb < nst; jb += 8 * CS * kFwdUnroll) {   // warp-uniform trip count
     const int j0 = jb + c;
     uint32_t w[kFwdUnroll];
     float xv[kFwdUnroll];
 #pragma unroll
     for (int u = 0; u < kFwdUnroll; ++u) {
-      const int j = j0 + 32 * u;
+      const int j = j0 + 8 * CS * u;
       const bool ok = j < nst && live;
       xv[u] = j < nst ? sval[j] : 0.0f;
       w[u] = ok ? __ldg(reinterpret_cast<const uint32_t*>(codes + sidx[j] + kofs)) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < kFwdUnroll; ++u) {
-      if (!__any_sync(0xffffffffu, j0 + 32 * u < nst)) break;     // warp-uniform: skip empty slots
+      if (!__any_sync(0xffffffffu, j0 + 8 * CS * u < nst)) break;     // warp-uniform: skip empty slots
       xs = __fadd_rn(xs, xv[u]);
 #pragma unroll
       for (int i = 0; i < CPW; ++i) {
@@ -99,8 +102,8 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
 #pragma unroll
   for (int i = 0; i < CPW; ++i) {
     acc[i] = __fsub_rn(__fmul_rn(2.0f, acc[i]), xl);
-    acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], 8));
-    acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], 16));
+#pragma unroll
+    for (int o = kFwdWords; o < 32; o <<= 1) acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], o));
   }
   if (c == 0) {
 #pragma unroll
@@ -153,18 +156,27 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
   const int L = num_levels(F->bits, F->level_mode);
   const float sigma = F->scale_c / (float)(L - 1);
   const int64_t words_total = F->strip_bytes / 4;
-  const unsigned blocks = (unsigned)ceil_div<int64_t>(words_total, kFwdWords);
+  const unsigned blocks8 = (unsigned)ceil_div<int64_t>(words_total, 8);
+  const unsigned blocks32 = (unsigned)ceil_div<int64_t>(words_total, 32);
+  // many CTAs of tiny work (batched, small support): 4x wider CTAs, about one wave
+  const bool wide = nrhs > 1 && (int64_t)blocks8 * nrhs > 4 * (int64_t)kNumSMs;
   const int64_t vlen = iht_vec_len(F->rows, F->planes);
   if (F->rows > 0x7FFFFFFF) return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   const uint8_t* codes = static_cast<const uint8_t*>(F->codes);
-#define IHT_FWD(BB)                                                                             \
-  IHT_CUDA_CHECK(launch_pdl(forward_kernel<BB>, dim3(blocks, nrhs), dim3(kFwdThreads), 0, st, codes,      \
+#define IHT_FWD(BB, WW, NBLK)                                                                   \
+  IHT_CUDA_CHECK(launch_pdl(forward_kernel<BB, WW>, dim3(NBLK, nrhs), dim3(kFwdThreads), 0, st, codes,    \
                             F->strip_bytes, words_total, (int)F->rows, (int)iht_rows_pad(F->rows), L, sigma, \
                             x_idx, x_val, x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen))
-  if (F->bits == 2) IHT_FWD(2);
-  else if (F->bits == 4) IHT_FWD(4);
-  else IHT_FWD(8);
+  if (wide) {
+    if (F->bits == 2) IHT_FWD(2, 32, blocks32);
+    else if (F->bits == 4) IHT_FWD(4, 32, blocks32);
+    else IHT_FWD(8, 32, blocks32);
+  } else {
+    if (F->bits == 2) IHT_FWD(2, 8, blocks8);
+    else if (F->bits == 4) IHT_FWD(4, 8, blocks8);
+    else IHT_FWD(8, 8, blocks8);
+  }
 #undef IHT_FWD
   return IHT_OK;
 }

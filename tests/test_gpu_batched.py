@@ -103,7 +103,10 @@ def test_adjoint_batched_zero_snapshot():
 
 # ------------------------------------------------------------------ (a4) batched forward
 @pytest.mark.parametrize("M,N,cplx,bits,B,s", [(300, 1001, False, 2, 5, 9), (144, 2304, True, 2, 64, 64),
-                                                (1000, 700, False, 8, 3, 0)])
+                                                (1000, 700, False, 8, 3, 0),
+                                                # > 4 x 148 narrow CTAs: the 32-word-per-CTA layout
+                                                (2304, 300, True, 2, 64, 64), (3000, 200, False, 4, 40, 30),
+                                                (1100, 150, False, 8, 100, 17)])
 def test_forward_batched_parity_and_shards(M, N, cplx, bits, B, s):
     phi = _phi(M, N, cplx, seed=7)
     c = OQ.scale_c(phi)
