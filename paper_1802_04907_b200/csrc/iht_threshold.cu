@@ -702,18 +702,27 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const unsigned int lt = (1u << lane) - 1u;
   int32_t* my_idx = cidx + warp * kWarpCand;
   float* my_val = cval + warp * kWarpCand;
-  for (int i0 = wlo; i0 < whi; i0 += 32) {
-    const int i = i0 + lane;
-    const float av = i < whi ? as[i] : 0.0f;
-    const unsigned int key = __float_as_uint(av) & 0x7FFFFFFFu;
-    const bool sel = i < whi && key > 0u && (key >> 20) >= d1;
-    const unsigned int bs = __ballot_sync(0xffffffffu, sel);
-    const int pos = wc + __popc(bs & lt);
-    if (sel && pos < kWarpCand) {
-      my_idx[pos] = (int32_t)(col_offset + lo + i);
-      my_val[pos] = av;
+  constexpr int kExU = 4;                           // shared-memory loads in flight per lane
+  for (int i00 = wlo; i00 < whi; i00 += 32 * kExU) {
+    float avs[kExU];
+#pragma unroll
+    for (int u = 0; u < kExU; ++u) {
+      const int i = i00 + 32 * u + lane;
+      avs[u] = i < whi ? as[i] : 0.0f;
     }
-    wc += __popc(bs);
+#pragma unroll
+    for (int u = 0; u < kExU; ++u) {
+      const int i = i00 + 32 * u + lane;
+      const unsigned int key = __float_as_uint(avs[u]) & 0x7FFFFFFFu;
+      const bool sel = i < whi && key > 0u && (key >> 20) >= d1;
+      const unsigned int bs = __ballot_sync(0xffffffffu, sel);
+      const int pos = wc + __popc(bs & lt);
+      if (sel && pos < kWarpCand) {
+        my_idx[pos] = (int32_t)(col_offset + lo + i);
+        my_val[pos] = avs[u];
+      }
+      wc += __popc(bs);
+    }
   }
   if (lane == 0) wgt[warp] = wc;
   if (probe == 3) { cluster.sync(); return; }
@@ -750,6 +759,43 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     cluster.sync();                                 // rank 0's list complete; nobody reads remote memory after
     if (rank != 0) return;
     if (probe == 4) return;
+    if (total <= kClThreads) {
+      // at most one candidate per thread: its rank among the candidates (keys greater, or
+      // equal at a lower index -- the list is in index order) decides it directly; kept
+      // iff rank < s (candidates have key > 0), written at the count of kept ones before it
+      const int i = tid;
+      const bool have = i < total;
+      const float vi = have ? pval[i] : 0.0f;
+      const unsigned int ki = __float_as_uint(vi) & 0x7FFFFFFFu;
+      int rk = 0;
+      int j = 0;
+      for (; j + 4 <= total; j += 4) {              // broadcast reads, 4 in flight
+        const unsigned int k0 = __float_as_uint(pval[j]) & 0x7FFFFFFFu, k1 = __float_as_uint(pval[j + 1]) & 0x7FFFFFFFu,
+                           k2 = __float_as_uint(pval[j + 2]) & 0x7FFFFFFFu, k3 = __float_as_uint(pval[j + 3]) & 0x7FFFFFFFu;
+        rk += (k0 > ki || (k0 == ki && j < i)) + (k1 > ki || (k1 == ki && j + 1 < i)) +
+              (k2 > ki || (k2 == ki && j + 2 < i)) + (k3 > ki || (k3 == ki && j + 3 < i));
+      }
+      for (; j < total; ++j) {
+        const unsigned int kj = __float_as_uint(pval[j]) & 0x7FFFFFFFu;
+        rk += kj > ki || (kj == ki && j < i);
+      }
+      const bool sel = have && rk < s;
+      const unsigned int bs = __ballot_sync(0xffffffffu, sel);
+      if (lane == 0) wgt[warp] = __popc(bs);
+      __syncthreads();
+      int pos = __popc(bs & lt);
+      for (int w = 0; w < warp; ++w) pos += wgt[w];
+      if (sel) {
+        out_idx[pos] = pidx[i];                     // out_idx / out_val point at snapshot b already
+        out_val[pos] = vi;
+      }
+      if (tid == 0) {
+        int kept = 0;
+        for (int w = 0; w < kClWarps; ++w) kept += wgt[w];
+        out_nnz[b] = kept;
+      }
+      return;
+    }
     select_ordered<kClThreads>(total, s, [&](int i) { return pval[i]; }, [&](int i) { return pidx[i]; }, out_idx,
                                out_val, out_nnz + b, 0, tot, scratch, wgt, weq, wtake, wbase, sh);
     return;
