@@ -30,6 +30,7 @@
 // compaction takes per-CTA (greater, equal) counts, an exclusive scan over the cluster
 // gives each CTA its output offset and its share of the lowest-index ties.  No global
 // atomics, no workspace memset, no candidate-capacity limit.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <cooperative_groups.h>
@@ -555,7 +556,16 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
     int64_t N, int64_t col_offset, int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
-    int32_t ldo, int32_t* __restrict__ out_nnz, int probe, int nparts, float gsigma, float* __restrict__ gout) {
+    int32_t ldo, int32_t* __restrict__ out_nnz, int probe, int nparts, float gsigma, float* __restrict__ gout,
+    long long* __restrict__ tl) {
+  // profiling timeline (IHT_THR_TL): globaltimer stamps of CTA ranks 0, 1 of snapshot 0
+  auto stamp = [&](int k) {
+    if (tl && threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 2) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tl[blockIdx.x * 16 + k] = t;
+    }
+  };
   extern __shared__ __align__(16) unsigned char dsm[];
   float* as = reinterpret_cast<float*>(dsm);                                  // [slice] (multiple of 4)
   if (mu_dev) mu = mu_dev[blockIdx.y];
@@ -574,6 +584,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   pdl_wait();                                   // g (adjoint) and x (previous H_s)
+  stamp(0);
   const int b = blockIdx.y;
   x_idx += (int64_t)b * ldx;
   x_val += (int64_t)b * ldx;
@@ -669,6 +680,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     }
   }
   nan = __syncthreads_or(nan);
+  stamp(1);
   if (tid == 0) cs.flags[0] = nan | poisoned;
   if (probe == 1) return;                           // profiling probe (IHT_THR_PROBE): phases' cost
   cluster.sync();
@@ -686,6 +698,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     cluster.sync();
     return;
   }
+  stamp(2);
   if (probe == 2) { cluster.sync(); return; }
   const bool all = (int64_t)s >= N;
   unsigned int d1 = 0;
@@ -702,29 +715,48 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const unsigned int lt = (1u << lane) - 1u;
   int32_t* my_idx = cidx + warp * kWarpCand;
   float* my_val = cval + warp * kWarpCand;
-  constexpr int kExU = 4;                           // shared-memory loads in flight per lane
-  for (int i00 = wlo; i00 < whi; i00 += 32 * kExU) {
-    float avs[kExU];
+  // lane = 4 consecutive entries (one 16-byte shared load) of a 128-entry chunk; chunks
+  // without a candidate (almost all: candidates are ~s of N) cost one vote
+  for (int i00 = wlo; i00 < whi; i00 += 128) {
+    const int ib = i00 + 4 * lane;
+    float v[4];
+    if (ib + 3 < whi) {
+      const float4 q = *reinterpret_cast<const float4*>(as + ib);   // wlo, i00 multiples of 32: aligned
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
 #pragma unroll
-    for (int u = 0; u < kExU; ++u) {
-      const int i = i00 + 32 * u + lane;
-      avs[u] = i < whi ? as[i] : 0.0f;
+      for (int e = 0; e < 4; ++e) v[e] = ib + e < whi ? as[ib + e] : 0.0f;
     }
+    unsigned int f = 0u;
 #pragma unroll
-    for (int u = 0; u < kExU; ++u) {
-      const int i = i00 + 32 * u + lane;
-      const unsigned int key = __float_as_uint(avs[u]) & 0x7FFFFFFFu;
-      const bool sel = i < whi && key > 0u && (key >> 20) >= d1;
-      const unsigned int bs = __ballot_sync(0xffffffffu, sel);
-      const int pos = wc + __popc(bs & lt);
-      if (sel && pos < kWarpCand) {
-        my_idx[pos] = (int32_t)(col_offset + lo + i);
-        my_val[pos] = avs[u];
+    for (int e = 0; e < 4; ++e) {
+      const unsigned int key = __float_as_uint(v[e]) & 0x7FFFFFFFu;
+      f |= (unsigned int)(ib + e < whi && key > 0u && (key >> 20) >= d1) << e;
+    }
+    if (__any_sync(0xffffffffu, f)) {
+      const int cnt = __popc(f);
+      int incl = cnt;                               // inclusive scan over lanes (index order)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
-      wc += __popc(bs);
+      int pos = wc + incl - cnt;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if ((f >> e) & 1u) {
+          if (pos < kWarpCand) {
+            my_idx[pos] = (int32_t)(col_offset + lo + ib + e);
+            my_val[pos] = v[e];
+          }
+          ++pos;
+        }
+      }
+      wc += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
   if (lane == 0) wgt[warp] = wc;
+  stamp(3);
   if (probe == 3) { cluster.sync(); return; }
   const int ovf = __syncthreads_or(wc > kWarpCand);
   if (tid == 0) {
@@ -756,7 +788,9 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
       gidx[off + j] = cidx[warp * kWarpCand + j];
       gval[off + j] = cval[warp * kWarpCand + j];
     }
+    stamp(4);
     cluster.sync();                                 // rank 0's list complete; nobody reads remote memory after
+    stamp(5);
     if (rank != 0) return;
     if (probe == 4) return;
     if (total <= kClThreads) {
@@ -794,6 +828,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
         for (int w = 0; w < kClWarps; ++w) kept += wgt[w];
         out_nnz[b] = kept;
       }
+      stamp(6);
       return;
     }
     select_ordered<kClThreads>(total, s, [&](int i) { return pval[i]; }, [&](int i) { return pidx[i]; }, out_idx,
@@ -895,6 +930,19 @@ extern "C" int64_t iht_threshold_batched_ws_bytes(int64_t N, int32_t s, int32_t 
 
 extern "C" int64_t iht_threshold_ws_bytes(int64_t N, int32_t s) { return iht_threshold_batched_ws_bytes(N, s, 1); }
 
+static long long* thr_timeline() {
+  static long long* p = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    on = getenv("IHT_THR_TL") ? atoi(getenv("IHT_THR_TL")) : 0;   // profiling only
+    if (on) {
+      cudaMalloc(&p, 32 * sizeof(long long));
+      cudaMemset(p, 0, 32 * sizeof(long long));
+    }
+  }
+  return p;
+}
+
 static bool g_thr_attr = false;
 
 static int thr_attrs() {
@@ -976,7 +1024,18 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
     lc.numAttrs = 2;
     IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
                                       N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe(), nparts,
-                                      gsigma, gout));
+                                      gsigma, gout, thr_timeline()));
+    if (thr_timeline()) {   // profiling: per-phase times of ranks 0, 1 of snapshot 0 (stderr)
+      static long long h[32];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, thr_timeline(), sizeof(h), cudaMemcpyDeviceToHost);
+      for (int c = 0; c < 2 && c < CL; ++c) {
+        fprintf(stderr, "thr CL=%d rank %d ns:", CL, c);
+        for (int k = 1; k < 7; ++k) fprintf(stderr, " %lld", h[c * 16 + k] > 0 ? h[c * 16 + k] - h[c * 16] : -1);
+        fprintf(stderr, "\n");
+      }
+      cudaMemset(thr_timeline(), 0, sizeof(h));
+    }
     return IHT_OK;
   }
   ThrWs w{};
