@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
       const float vi = have ? pval[i] : 0.0f;
       const unsigned int ki = __float_as_uint(vi) & 0x7FFFFFFFu;
       int rk = 0;
-      int j = 0;
+      int j = warp * 32 < total ? 0 : total;        // warps without a candidate skip the loop
       for (; j + 4 <= total; j += 4) {              // broadcast reads, 4 in flight
         const unsigned int k0 = __float_as_uint(pval[j]) & 0x7FFFFFFFu, k1 = __float_as_uint(pval[j + 1]) & 0x7FFFFFFFu,
                            k2 = __float_as_uint(pval[j + 2]) & 0x7FFFFFFFu, k3 = __float_as_uint(pval[j + 3]) & 0x7FFFFFFFu;
