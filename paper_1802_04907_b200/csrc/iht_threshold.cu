@@ -684,12 +684,32 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   if (tid == 0) cs.flags[0] = nan | poisoned;
   if (probe == 1) return;                           // profiling probe (IHT_THR_PROBE): phases' cost
   cluster.sync();
+  // cluster-wide histogram: every remote (DSMEM) load of this thread is issued before any
+  // is summed -- 2048 / 512 bins x CL ranks, one round trip instead of 4 CL
   int bad = 0;
-  for (int p = 0; p < CL; ++p) bad |= cluster.map_shared_rank(cs.flags, p)[0];
-  for (int q = tid; q < 2048; q += kClThreads) {
-    int acc = 0;
-    for (int p = 0; p < CL; ++p) acc += cluster.map_shared_rank(cs.hist[0], p)[q];
-    tot[q] = acc;
+  {
+    int hv[2048 / kClThreads][kClusterMax];
+    int fv[kClusterMax];
+#pragma unroll
+    for (int p = 0; p < kClusterMax; ++p) {
+      if (p < CL) {
+        const int* rh = cluster.map_shared_rank(cs.hist[0], p);
+        fv[p] = cluster.map_shared_rank(cs.flags, p)[0];
+#pragma unroll
+        for (int u = 0; u < 2048 / kClThreads; ++u) hv[u][p] = rh[tid + u * kClThreads];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2048 / kClThreads; ++u) {
+      int acc = 0;
+#pragma unroll
+      for (int p = 0; p < kClusterMax; ++p)
+        if (p < CL) acc += hv[u][p];
+      tot[tid + u * kClThreads] = acc;
+    }
+#pragma unroll
+    for (int p = 0; p < kClusterMax; ++p)
+      if (p < CL) bad |= fv[p];
   }
   buf = 1;
   __syncthreads();
@@ -767,12 +787,23 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   }
   cluster.sync();
   int any_ovf = 0, total = 0, base = 0;
-  for (int p = 0; p < CL; ++p) {
-    const int* rf = cluster.map_shared_rank(cs.flags, p);
-    const int c = *cluster.map_shared_rank(&cs.ncand, p);
-    any_ovf |= rf[1];
-    if (p < rank) base += c;
-    total += c;
+  {
+    int ov[kClusterMax], nv[kClusterMax];          // all remote loads first, then the sums
+#pragma unroll
+    for (int p = 0; p < kClusterMax; ++p) {
+      if (p < CL) {
+        ov[p] = cluster.map_shared_rank(cs.flags, p)[1];
+        nv[p] = *cluster.map_shared_rank(&cs.ncand, p);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < kClusterMax; ++p) {
+      if (p < CL) {
+        any_ovf |= ov[p];
+        if (p < rank) base += nv[p];
+        total += nv[p];
+      }
+    }
   }
   if (!any_ovf && total <= kClWarps * kWarpCand && probe != 9) {   // probe 9: per-pass cluster path (A/B)
     // few candidates (the usual case): every CTA stores its ordered lists into rank 0's
