@@ -49,6 +49,16 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   x_val += (int64_t)b * ldx;
   if (yhat) yhat += (int64_t)b * vlen;
   r += (int64_t)b * vlen;
+  // y-hat of this thread's output rows (final loop below), loaded before the support so
+  // that its latency overlaps the code loads instead of ending the chain
+  constexpr int kOutPer = (kFwdWords * CPW + kFwdThreads - 1) / kFwdThreads;
+  float ypre[kOutPer];
+#pragma unroll
+  for (int k = 0; k < kOutPer; ++k) {
+    const int t = threadIdx.x + k * kFwdThreads;
+    const int64_t m = (int64_t)blockIdx.x * kFwdWords * CPW + t;
+    ypre[k] = (yhat && t < kFwdWords * CPW && m < (int64_t)words_total * CPW) ? yhat[m] : 0.0f;
+  }
   int nnz = x_nnz[b];
   nnz = nnz < 0 ? 0 : (nnz > max_nnz ? max_nnz : nnz);
   const int64_t word = (int64_t)blockIdx.x * kFwdWords + wl;
@@ -111,14 +121,17 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   }
   __syncthreads();
   // one output row per thread, over the 8 warps in a fixed order; coalesced r writes
-  for (int t = threadIdx.x; t < kFwdWords * CPW; t += kFwdThreads) {
+#pragma unroll
+  for (int k = 0; k < kOutPer; ++k) {
+    const int t = threadIdx.x + k * kFwdThreads;
+    if (t >= kFwdWords * CPW) break;
     const int ww = t / CPW, i = t % CPW;
     const int64_t m = ((int64_t)blockIdx.x * kFwdWords + ww) * CPW + i;   // stacked row p * rpad + local row
     if (m >= (int64_t)words_total * CPW) continue;
     float s = part[0][ww][i];
 #pragma unroll
     for (int w2 = 1; w2 < kFwdThreads / 32; ++w2) s = __fadd_rn(s, part[w2][ww][i]);
-    const float yv = yhat ? yhat[m] : 0.0f;      // NULL y-hat: partial product (column shards)
+    const float yv = ypre[k];                    // 0 for a NULL y-hat: partial product (column shards)
     r[m] = (int)(m % rpad) < rows ? __fsub_rn(yv, __fmul_rn(sigma, s)) : 0.0f;  // pad rows: 0
   }
 }
