@@ -479,12 +479,22 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
   // max |r| over bit patterns: a NaN / inf in r_b marks the snapshot (F = kNonFinite) and
   // its g becomes NaN, so that its H_s reports the domain error
   unsigned int m = 0;
-  if (live)
-    for (int i = threadIdx.x * 4; i < Rpad; i += blockDim.x * 4) {
-      const float4 v = *reinterpret_cast<const float4*>(r + i);
-      m = max(max(m, __float_as_uint(v.x) & 0x7FFFFFFFu), __float_as_uint(v.y) & 0x7FFFFFFFu);
-      m = max(max(m, __float_as_uint(v.z) & 0x7FFFFFFFu), __float_as_uint(v.w) & 0x7FFFFFFFu);
+  if (live) {
+    constexpr int kU = 8;                   // float4 loads in flight per thread
+    for (int i0 = threadIdx.x * 4; i0 < Rpad; i0 += blockDim.x * 4 * kU) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * blockDim.x * 4;
+        v[u] = i < Rpad ? *reinterpret_cast<const float4*>(r + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        m = max(max(m, __float_as_uint(v[u].x) & 0x7FFFFFFFu), __float_as_uint(v[u].y) & 0x7FFFFFFFu);
+        m = max(max(m, __float_as_uint(v[u].z) & 0x7FFFFFFFu), __float_as_uint(v[u].w) & 0x7FFFFFFFu);
+      }
     }
+  }
   m = __reduce_max_sync(0xffffffffu, m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = __uint_as_float(m);
   __syncthreads();
