@@ -236,8 +236,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
     b0 = b + (cc0 < a.N ? g8 : 0) * 64;
     b1 = b + (cc0 + 8 < a.N ? g8 + 8 : 0) * 64;
   };
-  // the loop runs npad k-steps per task (nsteps rounded up to whole requests); a padded
-  // step multiplies whatever its smem half holds by zero limbs
+  // the request loop runs npad k-steps per task (nsteps rounded up to whole requests); the
+  // padded steps past nsteps are skipped (config 3: 9 real k-steps of 12 per task)
   const int npad = (nsteps + kReq - 1) / kReq * kReq;
   const uint32_t ring_w = (uint32_t)__cvta_generic_to_shared(ring + warp * kRing * kSlot);
   const uint32_t bar_w = (uint32_t)__cvta_generic_to_shared(bars + warp * kRing);
@@ -397,6 +397,13 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
 #pragma unroll
         for (int h = 0; h < kReq; ++h) {
           const int ks = ks0 + h;
+          if (ks >= nsteps) {                    // past the K-range (request padding): no work,
+            if (h == kReq - 1) {                 // warp-uniform; the slot is still refilled once
+              __syncwarp();
+              request(slot);
+            }
+            continue;
+          }
           const uint32_t src = ring_w + slot * kSlot + h * 1024 + g8 * 64 + t * 16;
           const uint4 s0 = lds128(src), s1 = lds128(src + 512);
           uint32_t bw[4 * P];
