@@ -394,16 +394,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
       for (int j = 0; j < P; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
       for (int ks0 = kc; ks0 < kend; ks0 += kReq) {
         mbar_wait(bar_w + 8 * slot, parity);    // the kReq tile-steps of this request landed
-#pragma unroll
-        for (int h = 0; h < kReq; ++h) {
+        // one k-step h of this request: fragments from the ring slot, limbs, NMMA MMAs; the
+        // slot is refilled after the request's last k-step has its fragments
+        auto kstep = [&](int h) {
           const int ks = ks0 + h;
-          if (ks >= nsteps) {                    // past the K-range (request padding): no work,
-            if (h == kReq - 1) {                 // warp-uniform; the slot is still refilled once
-              __syncwarp();
-              request(slot);
-            }
-            continue;
-          }
           const uint32_t src = ring_w + slot * kSlot + h * 1024 + g8 * 64 + t * 16;
           const uint4 s0 = lds128(src), s1 = lds128(src + 512);
           uint32_t bw[4 * P];
@@ -433,6 +427,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
           }
 #pragma unroll
           for (int u = 0; u < NMMA; ++u) mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
+        };
+        if (ks0 + kReq <= nsteps) {              // whole request (all but a task's last, or all)
+#pragma unroll
+          for (int h = 0; h < kReq; ++h) kstep(h);
+        } else {                                 // the last request: skip the padding k-steps
+#pragma unroll
+          for (int h = 0; h < kReq; ++h) {
+            if (ks0 + h < nsteps) {
+              kstep(h);
+            } else if (h == kReq - 1) {          // warp-uniform; the slot is still refilled once
+              __syncwarp();
+              request(slot);
+            }
+          }
         }
         if (++slot == kRing) {
           slot = 0;

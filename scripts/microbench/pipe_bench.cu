@@ -34,9 +34,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t m, uint32_t ph) {
   asm volatile("{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(m), "r"(ph) : "memory");
 }
 constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-template <int MODE> struct Cfg { static constexpr int ST = MODE == 10 ? 8 : (MODE == 11 ? 2 : (MODE == 15 ? 16 : 4));
+template <int MODE> struct Cfg { static constexpr int ST = MODE == 10 ? 8 : ((MODE == 11 || MODE == 16) ? 2 : (MODE == 15 ? 16 : 4));
                                   static constexpr bool FENCE = MODE != 12;
-                                  static constexpr int KPB = MODE == 11 ? 16 : 8; };
+                                  static constexpr int KPB = (MODE == 11 || MODE == 16) ? 16 : 8; };
 __device__ __forceinline__ void mbar_spin(uint32_t m, uint32_t ph) {
   asm volatile("{\n\t.reg .pred p;\n\tS_%=:\n\tmbarrier.test_wait.parity.shared.b64 p, [%0], %1;\n\t@!p bra S_%=;\n\t}" ::"r"(m), "r"(ph) : "memory");
 }
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc, int rnd)
   __shared__ uint64_t a_full[16], a_free[16], b_full[16], b_free[16], acc_full[2], acc_free[2], done;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x)
+  for (int i = threadIdx.x; i < 136 * 1024 / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem)[i] = rnd ? (uint32_t)(i * 2654435761u + 12345u) ^ ((uint32_t)i >> 7) * 40503u : 0u;
   if (threadIdx.x == 0) {
     for (int i = 0; i < ST; ++i) {
@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(352, 1) pipe(int nkb, long long* cyc, int rnd)
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < KPB; ++kk) {
-            const uint64_t bd = sw128_desc(bbase + (MODE >= 5 ? (s & 3) * 32768 : 0) + ((kk >> 2) & 1) * (128 * 128) + (kk & 3) * 32);
+            const uint64_t bd = MODE == 16
+                ? sw128_desc(bbase + (s & 1) * 65536 + (kk >> 2) * (128 * 128) + (kk & 3) * 32)   // kernel-like 64 KiB stages
+                : sw128_desc(bbase + (MODE >= 5 ? (s & 3) * 32768 : 0) + ((kk >> 2) & 1) * (128 * 128) + (kk & 3) * 32);
             const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                          "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + (MODE >= 6 ? ab * 128 : 0)),
@@ -183,6 +185,7 @@ int main() {
   run<1>("1: issue + commit per K-block, no waits", sms, 2);
   run<11>("11: 8 with 16 MMAs per K-block, 2 stages", sms, 1);
   run<11>("11: 8 with 16 MMAs per K-block, 2 stages", sms, 2);
+  run<16>("16: 11 with the kernel's 64 KiB B stages (4 atom columns)", sms, 1);
   run<2>("2: + converter handoff (a_full/a_free, 4 stages), lane-0 wait", sms);
   run<3>("3: + 6 spinning warps", sms);
   run<4>("4: handoff, all 32 MMA-warp lanes wait", sms);
