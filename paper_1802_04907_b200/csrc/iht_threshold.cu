@@ -728,6 +728,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     d1 = (unsigned int)sh[0];
     target = s - sh[1];
   }
+  stamp(7);
   // ---- (2) candidates: key > 0 and digit >= d1, per-warp ordered lists (contiguous ranges)
   const int span = ((n + kClWarps - 1) / kClWarps + 31) / 32 * 32;
   const int wlo = warp * span, whi = min(n, wlo + span);
@@ -1062,7 +1063,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
       cudaMemcpy(h, thr_timeline(), sizeof(h), cudaMemcpyDeviceToHost);
       for (int c = 0; c < 2 && c < CL; ++c) {
         fprintf(stderr, "thr CL=%d rank %d ns:", CL, c);
-        for (int k = 1; k < 7; ++k) fprintf(stderr, " %lld", h[c * 16 + k] > 0 ? h[c * 16 + k] - h[c * 16] : -1);
+        for (int k = 1; k < 8; ++k) fprintf(stderr, " %lld", h[c * 16 + k] > 0 ? h[c * 16 + k] - h[c * 16] : -1);
         fprintf(stderr, "\n");
       }
       cudaMemset(thr_timeline(), 0, sizeof(h));
