@@ -385,6 +385,11 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   const bool bload = g8 < 3;
   int slot = 0;
   uint32_t parity = 0;
+  // B fragments: lanes g8 < 3 reload them every k-step; the others (B columns 3..7) hold
+  // zeros for the whole kernel instead of re-zeroing 4P registers per k-step
+  uint32_t bw[4 * P];
+#pragma unroll
+  for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
   for (int64_t task = wid; task < ntask; task += wstride) {
     float accf0 = 0.0f, accf1 = 0.0f;     // lanes t == 0: columns c0, c1
     for (int kc = 0, c = 0; kc < npad; kc += spc, ++c) {
@@ -400,10 +405,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
           const int ks = ks0 + h;
           const uint32_t src = ring_w + slot * kSlot + h * 1024 + g8 * 64 + t * 16;
           const uint4 s0 = lds128(src), s1 = lds128(src + 512);
-          uint32_t bw[4 * P];
-#pragma unroll
-          for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
-          if (bload) {
+          if (bload) {                           // other lanes keep the zeros set once below
             const uint32_t bp = limb_n + (uint32_t)(ks * 4 + t) * (16 * P);
 #pragma unroll
             for (int q = 0; q < P; ++q) {
