@@ -45,3 +45,14 @@ def test_radio_generator_properties():
     l, m = p.meta["l"], p.meta["m"]
     assert np.all(l[p.x_idx] ** 2 + m[p.x_idx] ** 2 < 1.0)
     assert np.all(p.x_val > 0)
+
+
+def test_config_steps_follow_reading_c9():
+    """Fixed steps of the BASELINE configs (DESIGN reading c9): config 1 and 4 the stated
+    mu = 1, config 2 mu = 1/4 (mu = 1 diverges at 2 bits), radio mu = 1/(10 M)."""
+    assert G.CONFIGS[1].get("mu", 1.0) == 1.0 and G.CONFIGS[4].get("mu", 1.0) == 1.0
+    assert G.CONFIGS[2]["mu"] == 0.25
+    p = G.radio_problem(cfg_id=99, A=6, grid=16, n_src=3, n_iter=2, K=2)
+    assert p.mu == 0.1 / p.M
+    q = G.gaussian_problem(64, 128, 4, cfg_id=98, n_iter=2, mu=0.25, K=2)
+    assert q.mu == 0.25
