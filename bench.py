@@ -32,6 +32,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+def _baseline_metric():
+    """BASELINE.json's metric string, printed verbatim by both arms."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:
+        return "IHT iter/s & \u03a6-stream HBM GB/s (% of peak), 2/4/8-bit \u03a6, 1\u20138 B200"
+
+
+METRIC = _baseline_metric()
 PAPER_CONTEXT = "paper: CPU 4-bit 4.19x / 8-bit 2.84x vs 32-bit (Haswell E3-1285L v3, P:587); " \
                 "FPGA 2&8-bit 9.19x to 90% support (P:578) -- context only, other hardware"
 
@@ -121,6 +131,7 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- problem setup
 L2_FLUSH_BYTES = 256 << 20      # > the 126 MB L2 of a B200
+TIMED_REGIONS = 3               # each of --steps steps; the median region is reported
 
 
 def make_problem(args):
@@ -132,44 +143,173 @@ def make_problem(args):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def oracle_sample(p, steps=None):
-    """Time the float64 oracle (as it stands) on bounded samples of the workload: the
-    first R0 and 2*R0 measurement rows (all N columns), K = 1 copy (the same
-    forward/adjoint work per iteration as K = 2, half the one-time quantisation),
-    n iterations each, with the copies pre-quantised (one-time preprocess, excluded
-    as on the GPU).  Per-iteration time is fitted as t(rows) = a + b rows and
-    extrapolated to the full M rows."""
+ORACLE_FULL_COMPONENTS = 1 << 29    # problems up to this many real components are timed whole
+
+
+def _gen_rows_job(job):
+    """Input generator (workloads.gen, no method arithmetic): rows [r0, r0 + n) of a
+    counter-Gaussian Phi."""
+    from workloads.gen import gaussian_block
+    key, N, r0, n, sd = job
+    return gaussian_block(key, N, r0, n, 0, N, sd)
+
+
+def _quant_rows_job(job):
+    """The oracle's own quantiser on a block of rows (global row offset r0; codes depend only
+    on global indices, pinned by tests/test_oracle_quantize.py block/whole equality)."""
+    from oracle import quantize as OQ
+    phi, bits, seed, copy_id, c, r0 = job
+    return OQ.quantize_matrix(phi, bits, 0, seed, copy_id, c=c, row_offset=r0)[0]
+
+
+def _parallel(fn, jobs, workers):
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    if workers <= 1 or len(jobs) <= 1:
+        return [fn(j) for j in jobs]
+    with cf.ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
+        return list(ex.map(fn, jobs))
+
+
+def _oracle_sample_problems(p, sizes, workers):
+    """{R: (phi, y, pool)} of the first R rows of the workload for each R in `sizes`, for the
+    oracle: Phi rows from the input generator, one copy quantised by the oracle's quantiser
+    (in row blocks on `workers` processes: one-time preprocessing, excluded from the
+    per-iteration times as on the GPU), dequantised once.  A smaller sample is a row prefix
+    of the largest (codes depend only on global indices)."""
     import numpy as np
     from oracle import iht as OI
     from oracle import quantize as OQ
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
-    r0 = max(1, min(p.M // 2, (1 << 23) // (p.N * p.planes)))
-    r0 = 1 << int(np.floor(np.log2(r0)))
-    n_it = 3 if steps is None else max(1, steps)
-    B = p.meta.get("batch_y").shape[1] if "batch_y" in p.meta else 1
-    times = []
-    for rows in (r0, 2 * r0):
-        phi = p.phi_rows(0, rows)
-        y = p.meta["batch_y"][:rows, 0] if B > 1 else p.y[:rows]
-        pool = OI.CopyPool(phi, p.b_phi, 0, p.seed, OQ.scale_c(phi), cache=2)
-        pool.dequantized(0)                                   # one-time preprocess
-        t0 = time.perf_counter()
-        OI.qniht(phi, y, p.s, n_it, p.mu, p.b_phi, p.b_y, p.seed, 1, record=False, pool=pool)
-        times.append((time.perf_counter() - t0) / n_it)
-    b = max((times[1] - times[0]) / r0, 0.0)
-    a = max(times[0] - b * r0, 0.0)
-    per_iter = (a + b * p.M) * B
-    return {"value": 1.0 / per_iter, "unit": "iter/s", "cores": threads, "kind": "oracle",
-            "sample": f"rows 0..{r0 - 1} and 0..{2 * r0 - 1} of {p.M}, all {p.N} columns, K=1 copy, "
-                      f"{n_it} float64 iterations each (copy quantisation excluded); per-iteration time "
-                      f"fitted a + b*rows ({times[0] * 1e3:.1f} / {times[1] * 1e3:.1f} ms) and extrapolated "
-                      f"to {p.M} rows" + (f", one snapshot timed and multiplied by the batch B={B} "
-                                          f"(the oracle runs snapshots independently)" if B > 1 else ""),
-            "host_cores": os.cpu_count()}
+    rows = max(sizes)
+    blk = max(1, -(-rows // max(1, workers)))
+    spans = [(r, min(blk, rows - r)) for r in range(0, rows, blk)]
+    if p.phi is not None:
+        phi = p.phi[:rows]
+    else:
+        phi = np.concatenate(_parallel(_gen_rows_job, [(p.phi_key, p.N, r, n, p.phi_sd) for r, n in spans],
+                                       workers))
+    c = OQ.scale_c(phi)
+    codes = np.concatenate(_parallel(_quant_rows_job, [(phi[r:r + n], p.b_phi, p.seed, 0, c, r) for r, n in spans],
+                                     workers), axis=1)
+
+    class _Pool(OI.CopyPool):          # the oracle's pool, its one copy quantised above
+        def __init__(self, R):
+            super().__init__(phi[:R], p.b_phi, 0, p.seed, c, cache=1)
+            self.R = R
+
+        def codes(self, copy_id):
+            assert copy_id == 0
+            return codes[:, :self.R]
+
+    B = p.meta["batch_y"].shape[1] if "batch_y" in p.meta else 1
+    y = p.meta["batch_y"][:, 0] if B > 1 else p.y
+    out = {}
+    for R in sizes:
+        pool = _Pool(R)
+        pool.dequantized(0)
+        out[R] = (phi[:R], y[:R], pool)
+    return out
+
+
+def _time_oracle_iters(p, phi, y, pool, n, warmup, threads):
+    """Per-iteration wall times (time.perf_counter between consecutive iterations; the first
+    `warmup` + 1 intervals, which include qniht's one-time setup, are dropped) of the oracle's
+    qniht as it stands, K = 1 copy (the same forward/adjoint/H_s work per iteration as K = 2)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import iht as OI
+    stamps = []
+    with threadpool_limits(limits=threads):
+        OI.qniht(phi, y, p.s, n + warmup + 1, p.mu, p.b_phi, p.b_y, p.seed, 1, record=False, pool=pool,
+                 iter_hook=lambda _n: stamps.append(time.perf_counter()))
+    d = [b - a for a, b in zip(stamps, stamps[1:])]
+    return d[warmup:]
+
+
+def oracle_baseline(p, n=5, warmup=0, passes=2):
+    """The float64 oracle (oracle.iht.qniht, as it stands) timed on this host: the median
+    per-iteration time (the paper's per-iteration median), once with all cores and
+    once single-threaded.  Problems up to 2^29 real components are timed whole; config 4
+    (65536 x 262144, 17 G components) on its first R1 = 512 and R2 = 1024 rows (all N
+    columns), the per-iteration time fitted as a + b rows (forward and adjoint scale with the
+    rows, H_s does not) and evaluated at M.  A batch of B snapshots costs B single-snapshot
+    solves (the oracle runs them independently).  `passes` independent all-core passes show
+    the run-to-run agreement."""
+    import numpy as np
+    cores = len(os.sched_getaffinity(0))
+    t_prep = time.perf_counter()
+    whole = p.R * p.N <= ORACLE_FULL_COMPONENTS
+    sizes = [p.M] if whole else [512, 1024]
+    samples = _oracle_sample_problems(p, sizes, cores)
+    prep_s = time.perf_counter() - t_prep
+    B = p.meta["batch_y"].shape[1] if "batch_y" in p.meta else 1
+
+    def per_iter(threads, w):
+        med = {R: statistics.median(_time_oracle_iters(p, *samples[R], n, w, threads)) for R in sizes}
+        if whole:
+            return med[p.M] * B, med
+        R1, R2 = sizes
+        b = max((med[R2] - med[R1]) / (R2 - R1), 0.0)
+        a = max(med[R1] - b * R1, 0.0)
+        return (a + b * p.M) * B, med
+
+    runs = [per_iter(cores, warmup if i == 0 else 0) for i in range(passes)]
+    single, single_med = per_iter(1, 0)
+    all_core = statistics.median([r[0] for r in runs])
+    vals = [1.0 / r[0] for r in runs]
+    fmt = lambda med: ", ".join(f"{R} rows {t * 1e3:.1f} ms" for R, t in med.items())   # noqa: E731
+    sample = (f"whole problem ({p.M}x{p.N}{', complex' if p.complex else ''})" if whole else
+              f"rows 0..511 and 0..1023 of {p.M}, all {p.N} columns; median per-iteration time fitted "
+              f"a + b*rows and evaluated at {p.M} rows") + \
+        f"; K=1 copy quantised by the oracle (one-time, excluded); median of {n} per-iteration " \
+        f"times per size (all cores: {fmt(runs[0][1])}; 1 thread: {fmt(single_med)})" + \
+        (f"; one snapshot timed x B={B}" if B > 1 else "")
+    return {"value": 1.0 / all_core, "unit": "iter/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "single_thread": {"value": 1.0 / single, "cores": 1},
+            "passes_all_cores": vals, "pass_agreement": min(vals) / max(vals),
+            "host_cores": os.cpu_count(), "prep_s": prep_s}
+
+
+def _free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_cmd(n, argv, port):
+    """The torchrun command line that runs this script on n ranks of one node (one process
+    per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def relaunch_under_torchrun(n):
+    """`python bench.py --gpus N` without a launcher: start the N ranks under torchrun and pass
+    their output through (rank 0 prints the JSON line)."""
+    cmd = relaunch_cmd(n, sys.argv[1:], _free_port())
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
+    return subprocess.call(cmd, env=env)
+
+
+def workload_config(p, args, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    B = p.meta["batch_y"].shape[1] if "batch_y" in p.meta else 1
+    return {
+        "workload": f"{p.name}: {'complex radio' if p.complex else 'real Gaussian'} {p.M}x{p.N}, "
+                    f"{p.b_phi}-bit Phi, {p.b_y}-bit y, s={p.s}, n*={p.n_iter}, mu={p.mu:g}, K={p.K} copies"
+                    + (f", B={B} snapshots per iteration (one iter = all B)" if B > 1 else ""),
+        "M": p.M, "N": p.N, "b_phi": p.b_phi, "b_y": p.b_y, "s": p.s, "n_iter": p.n_iter, "K": p.K,
+        "batch": B,
+        "parallelism": (f"column-sharded x{world}" + (", NCCL all-reduce of r + all-gather of top-s candidates"
+                                                      if world > 1 else "") if B > 1 else
+                        f"row-sharded x{world}" + (", NCCL reduce-scatter of g + sharded top-s + all-gather of "
+                                                   "candidates per iteration" if world > 1 else "")),
+        "adjoint_variant": args.variant,
+        "step": "adaptive mu-hat with accept/shrink loop (Algorithm 1, P:350-363)" if args.adaptive
+                else f"fixed mu = {p.mu:g}",
+        "copies": "fresh: drawn on the fly from the resident fp32 Phi, K = 2 n* (NEXT-2)" if args.fresh
+                  else f"pool of K = {p.K} stored quantised copies",
+    }
 
 
 # ----------------------------------------------------------------------------- main
@@ -178,24 +318,26 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world == 1 and args.gpus > 1:
-        print(json.dumps({"error": "--gpus N>1 must be launched with torchrun"}))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch_under_torchrun(args.gpus)
+    if world != args.gpus and args.impl == "ours":
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         return 2
 
     if args.impl == "reference":
+        # the oracle arm: rank 0 alone runs it on the host cores; other ranks exit at once
         if rank != 0:
             return 0
         p = make_problem(args)
-        for _ in range(max(0, args.warmup)):
-            pass
-        cb = oracle_sample(p, steps=max(1, args.steps))
-        line = {"impl": "reference", "metric": "IHT iter/s", "value": cb["value"], "unit": "iter/s",
-                "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        cb = oracle_baseline(p, n=max(1, args.steps), warmup=max(0, args.warmup))
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "iter/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": p.name, "M": p.M, "N": p.N, "b_phi": p.b_phi, "s": p.s,
-                           "n_iter": p.n_iter},
+                "config": workload_config(p, args, args.gpus),
                 "cpu_baseline": cb,
-                "e2e": {"value": cb["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "e2e": {"value": cb["value"], "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "note": "the float64 CPU oracle (oracle/, as it stands) on this host's cores; a step = one "
+                        "oracle iteration on the bounded sample named in cpu_baseline.sample"}
         print(json.dumps(line))
         return 0
 
@@ -288,14 +430,18 @@ def main():
         barrier()
         return t, clk.stop()
 
-    ms_dev, clocks = timed_region()
-    # a hardware / thermal slowdown during the timed region invalidates it: measure once more
-    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
-    if max_over_ranks(1.0 if bad & set(clocks.get("reasons") or []) else 0.0) > 0.0:   # all ranks agree
-        first = clocks
-        ms_dev, clocks = timed_region()
-        clocks = dict(clocks, remeasured_after=sorted(bad & set(first.get("reasons") or [])) or ["another rank"])
-    ms = max_over_ranks(ms_dev)
+    # a fixed number of timed regions (none depends on another's result): the reported time is
+    # the median region, every raw time and each region's clock sample are kept
+    regions = []
+    for _ in range(TIMED_REGIONS):
+        t_dev, clk = timed_region()
+        regions.append((max_over_ranks(t_dev), clk))
+    region_ms = [r[0] for r in regions]
+    ms = statistics.median(region_ms)
+    med = min(range(len(regions)), key=lambda i: abs(region_ms[i] - ms))
+    clocks = dict(regions[med][1], regions=[{"ms": r[0], "sm_mhz": r[1].get("sm_mhz"),
+                                             "reasons": r[1].get("reasons")} for r in regions],
+                  reasons_any_region=sorted({x for r in regions for x in (r[1].get("reasons") or [])}))
     sol_prof = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, adjoint_variant=args.variant, comm=comm,
                           profile=True, nrhs=B, adaptive=args.adaptive)
     for _ in range(2):
@@ -373,14 +519,15 @@ def main():
         return 0
     cb = None
     if not args.no_cpu_baseline and world == 1:
-        cb = oracle_sample(p)
+        cb = oracle_baseline(p)
     line = {
-        "metric": "IHT iter/s (Phi-stream HBM GB/s, % of peak)",
+        "metric": METRIC,
         "value": value,
         "unit": "iter/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": max(3, args.warmup),
+        "region_ms": region_ms,
         "ms_per_step": ms / args.steps,
         "higher_is_better": True,
         "scaling": "strong",
@@ -388,24 +535,12 @@ def main():
         "dtype": ("u8 x s8 -> s32 tcgen05 (kind::i8) batched adjoint" if B > 1 else
                   "s8/s32 int8-MMA adjoint") + ", f32 forward/update",
         "data": "synthetic",
-        "config": {
-            "workload": f"{p.name}: {'complex radio' if p.complex else 'real Gaussian'} {p.M}x{p.N}, "
-                        f"{p.b_phi}-bit Phi, {p.b_y}-bit y, s={p.s}, n*={p.n_iter}, mu={p.mu:g}, K={p.K} copies"
-                        + (f", B={B} snapshots per iteration (one iter = all B)" if B > 1 else ""),
-            "M": p.M, "N": p.N, "b_phi": p.b_phi, "b_y": p.b_y, "s": p.s, "n_iter": p.n_iter, "K": p.K,
-            "batch": B,
-            "parallelism": (f"column-sharded x{world}" + (", NCCL all-reduce of r + all-gather of top-s candidates"
-                                                          if world > 1 else "") if B > 1 else
-                            f"row-sharded x{world}" + (", NCCL all-reduce of g per iteration" if world > 1 else "")),
+        "config": dict(workload_config(p, args, world), **{
             "l2": (lambda res: f"inputs > L2: {res / 2**30:.2f} GiB per GPU streamed from HBM" if not resident
                    else f"pool {res / 2**20:.1f} MiB fits L2: L2 flushed (256 MiB write) before every timed step, "
                         "per-step event times summed")(copy_bytes if args.fresh else p.K * copy_bytes),
-            "adjoint_variant": args.variant,
-            "step": "adaptive mu-hat with accept/shrink loop (Algorithm 1, P:350-363)" if args.adaptive
-                    else f"fixed mu = {p.mu:g}",
-            "copies": "fresh: drawn on the fly from the resident fp32 Phi, K = 2 n* (NEXT-2)" if args.fresh
-                      else f"pool of K = {p.K} stored quantised copies",
-        },
+            "timing": f"{TIMED_REGIONS} timed regions of {args.steps} steps each (CUDA events, barrier + sync "
+                      f"on both sides, max over ranks); median region reported"}),
         "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
                 "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},
         "roofline": roof if B > 1 else
@@ -420,7 +555,11 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(launches_per_run * args.steps),
         "clocks": clocks,
-        "preprocess": {**prep, "c_phi": c_phi, "setup_s": setup_s},
+        "preprocess": {**prep, "c_phi": c_phi, "setup_s": setup_s,
+                       "quantize_frac_of_hbm": (prep["quantize_GBps"] / peak) if prep.get("quantize_GBps") else None,
+                       "quantize_note": "one fp32 read of Phi emits up to 8 copies per launch: algorithmic bytes "
+                                        "(4 + K b/8) per real component; event-timed quantiser launches only "
+                                        "(generation excluded)"},
         "result": {"support_size": nnz if B > 1 else nnz[0]},
         "snapshot_iter_per_s": value * B,
         "context": PAPER_CONTEXT,

@@ -119,7 +119,7 @@ class CopyPool:
 
 
 def qniht(phi, y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True,
-          x0=None, pool=None, snapshot=0):
+          x0=None, pool=None, snapshot=0, iter_hook=None):
     """Algorithm 1 with fixed step mu; returns QnihtResult.
 
     phi: float32 (M x N) or complex64 array; y: float32 / complex64 (M,).
@@ -128,6 +128,8 @@ def qniht(phi, y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True,
     time the iterations without the one-time quantisation of the copies.
     snapshot: index b of this observation among B sharing Phi (config 5); selects the
     Philox column of its y-hat (oracle.quantize.quantize_vector).
+    iter_hook: optional callable iter_hook(n) invoked after iteration n (timing
+    instrumentation for bench.py's CPU baseline; it sees nothing and changes nothing).
     """
     c_phi = Q.scale_c(phi)
     c_y = Q.scale_c(y)
@@ -153,6 +155,8 @@ def qniht(phi, y, s, n_iter, mu, b_phi, b_y, seed, K, level_mode=0, record=True,
         if record:
             res.trace.append(IterRecord(n, a_id, f_id, r, g, a, x_idx, x_val,
                                         margin_at_s(a, s)))
+        if iter_hook is not None:
+            iter_hook(n)
     res.x_idx, res.x_val = x_idx, x_val
     return res
 

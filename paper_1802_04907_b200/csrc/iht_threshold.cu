@@ -568,7 +568,6 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   };
   extern __shared__ __align__(16) unsigned char dsm[];
   float* as = reinterpret_cast<float*>(dsm);                                  // [slice] (multiple of 4)
-  if (mu_dev) mu = mu_dev[blockIdx.y];
   int32_t* cidx = reinterpret_cast<int32_t*>(dsm + (size_t)slice * 4);        // [kClWarps][kWarpCand]
   float* cval = reinterpret_cast<float*>(cidx + kClWarps * kWarpCand);        // [kClWarps][kWarpCand]
   int32_t* pidx = reinterpret_cast<int32_t*>(cval + kClWarps * kWarpCand);    // packed list (index order)
@@ -584,6 +583,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   pdl_wait();                                   // g (adjoint) and x (previous H_s)
+  if (mu_dev) mu = mu_dev[blockIdx.y];          // the adaptive step's mu: a predecessor's output too
   stamp(0);
   const int b = blockIdx.y;
   x_idx += (int64_t)b * ldx;

@@ -28,6 +28,28 @@ def shard_cols(N, world, rank):
     return cols, rank * cols
 
 
+def _timed(fn):
+    """Run fn() between two CUDA events on the current stream; returns the event pair."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn()
+    e1.record()
+    return e0, e1
+
+
+def _quantize_stats(t, qev, components, K, bits):
+    """Quantiser throughput ((4 + K b / 8) bytes per real component for one fp32
+    read emitting K copies) from the event-timed launches."""
+    import torch
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in qev)
+    t["quantize_ms"] = ms
+    t["quantize_launches"] = len(qev)
+    t["quantize_bytes"] = int(components * 4 + K * components * bits // 8)
+    t["quantize_GBps"] = t["quantize_bytes"] / (ms / 1e3) / 1e9 if ms > 0 else None
+
+
 def build_pool(p, rank, world, dev, dist_on, shard="rows"):
     """Generate (config 4: on the device, block-wise) and quantise this rank's shard of Phi
     (row shard, or column shard for the batched path) into the pool of K copies.
@@ -66,20 +88,22 @@ def build_pool(p, rank, world, dev, dist_on, shard="rows"):
             for k in range(p.K)]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    qev = []                       # CUDA event pairs around every quantiser launch (a2)
     if p.phi is None:
         for r in range(0, rows, blk):
             n = min(blk, rows - r)
             view = buf[:n]
             gauss_fill(view, p.phi_key, p.N, row0 + r, 0, p.phi_sd)
             for k0 in range(0, p.K, 8):
-                iht.quantize_rows(view, pool[k0:k0 + 8], r)
+                qev.append(_timed(lambda: iht.quantize_rows(view, pool[k0:k0 + 8], r)))
         del buf
     else:
         for k0 in range(0, p.K, 8):
-            iht.quantize_rows(phi, pool[k0:k0 + 8], 0)
+            qev.append(_timed(lambda: iht.quantize_rows(phi, pool[k0:k0 + 8], 0)))
         del phi
     torch.cuda.synchronize()
-    t["quantize_ms"] = (time.perf_counter() - t0) * 1e3
+    t["quantize_wall_ms"] = (time.perf_counter() - t0) * 1e3
+    _quantize_stats(t, qev, rows * p.planes * p.N, p.K, p.b_phi)
     torch.cuda.empty_cache()
     return pool, c, t, rows, row0
 
@@ -104,12 +128,8 @@ def _build_pool_cols(p, rank, world, dev, dist_on):
     c = float(cmax.item())
     pool = [iht.new_copy(p.M, cols, p.planes, p.b_phi, 0, p.seed, k, c, device=dev, col_offset=col0)
             for k in range(p.K)]
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for k0 in range(0, p.K, 8):
-        iht.quantize_rows(phi, pool[k0:k0 + 8], 0)
-    torch.cuda.synchronize()
-    t["quantize_ms"] = (time.perf_counter() - t0) * 1e3
+    qev = [_timed(lambda: iht.quantize_rows(phi, pool[k0:k0 + 8], 0)) for k0 in range(0, p.K, 8)]
+    _quantize_stats(t, qev, p.M * p.planes * cols, p.K, p.b_phi)
     del phi
     torch.cuda.empty_cache()
     return pool, c, t, p.M, 0

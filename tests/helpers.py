@@ -82,3 +82,31 @@ def dense(idx, val, N):
     x = np.zeros(N)
     x[np.asarray(idx, dtype=np.int64)] = val
     return x
+
+
+def near_tie(rec_a, margin, s, rel=1e-5):
+    """The parity rule's near-tie test: the oracle's gap between the s-th and
+    (s+1)-th largest |a| is at most rel * |a|_(s), so fp32 and fp64 may legitimately pick
+    different supports from here on."""
+    mag = np.sort(np.abs(np.asarray(rec_a)))[::-1]
+    if s <= 0 or mag.size == 0:
+        return False
+    kth = mag[min(s, mag.size) - 1]
+    return not margin > rel * max(kth, 1e-30)
+
+
+def check_trajectory(trace, idx, val, nnz, s, tol):
+    """Free-running comparison of a solver trace with the oracle's records: every iteration
+    before the oracle's first near-tie must have the identical support and x within `tol`
+    relative l2 (no escape).  idx / val: [n_iter][s], nnz: [n_iter] (row n = x after
+    iteration n+1).  Returns the number of compared iterations (len(trace) = no near-tie)."""
+    idx, val, nnz = np.asarray(idx), np.asarray(val), np.asarray(nnz)
+    for n, rec in enumerate(trace):
+        if near_tie(rec.a, rec.margin, s):
+            return n
+        k = int(nnz[n])
+        assert idx[n, :k].tolist() == list(rec.x_idx), \
+            f"iteration {rec.n}: support differs from the oracle (margin {rec.margin:.3e})"
+        err = rel_l2(val[n, :k], rec.x_val, floor=1e-30)
+        assert err <= tol, f"iteration {rec.n}: x relative l2 error {err:.3e} > {tol}"
+    return len(trace)

@@ -73,7 +73,7 @@ def test_adaptive_solver_matches_oracle(case, graph):
     mu, sh = sol.steps()
     checked, clean = _compare(recs, idx.numpy(), val.numpy(), nnz.numpy(), mu.numpy(), sh.numpy(), 1e-4, 1e-4, 1e-5,
                               1e-4)
-    assert checked >= min(3, p.n_iter)
+    assert checked >= min(10, p.n_iter), checked
     if clean:
         assert idx[-1, :int(nnz[-1])].tolist() == xi.tolist()
     sol.close()

@@ -273,7 +273,9 @@ def test_batched_solver_free_running(B, graph):
         if clean:
             clean_snapshots += 1
             assert fi[b, :fn[b]].tolist() == refs[b].x_idx.tolist()
-    assert clean_snapshots >= 1 and checked >= B * p.n_iter // 4, (clean_snapshots, checked)
+    # never vacuous: most snapshots run clean to the end, and at least 3/4 of all
+    # snapshot-iterations are compared
+    assert clean_snapshots >= B // 2 and checked >= 3 * B * p.n_iter // 4, (clean_snapshots, checked)
     # deterministic replay
     gi, gv, gn = sol.run(_to_dev(Y))
     torch.cuda.synchronize()

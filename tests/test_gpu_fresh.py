@@ -107,5 +107,5 @@ def test_fresh_solver_matches_oracle_2n_copies(case):
         assert idx[n, :k].tolist() == rec.x_idx.tolist(), f"iteration {rec.n}"
         assert rel_l2(val[n, :k].numpy(), rec.x_val, floor=1e-30) < TOL
         checked += 1
-    assert checked >= 3
+    assert checked >= min(n_iter, 10), checked
     sol.close()

@@ -1,0 +1,189 @@
+"""Free-running trajectory parity at BASELINE.json's full shapes (Algorithm 1's n* loop,
+P:345-351): the whole solve runs through iht_solver (the CUDA graph bench.py times) and every
+iterate x^[n+1] is compared with the float64 oracle's, up to the oracle's first near-tie:
+
+* config 2 (4096 x 16384 real Gaussian, 2-bit): all 200 iterations with K = 2 copies, and the
+  first 10 iterations with the bench's K = 400 (copies 0..19, i.e. exact Algorithm 1);
+* config 3 (2304 x 65536 complex radio, 2-bit, single observation): 20 iterations, K = 2;
+* config 5 (the radio Phi, batched tcgen05 path): 8 snapshots, 20 iterations, K = 2.
+
+Bar: identical supports and x within 1e-4 relative l2 (1e-3 on the tensor-core path) in
+every compared iteration, no escape; a final support identical to the oracle's whenever no
+near-tie occurred; a minimum number of compared iterations so no case is vacuous.
+The oracle's copies are quantised by oracle.quantize in row blocks on forked worker
+processes (codes depend only on global indices: block/whole equality is pinned in
+tests/test_oracle_quantize.py); everything else is oracle.iht.qniht as it stands.
+"""
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import iht as OI
+from oracle import quantize as OQ
+from paper_1802_04907_b200 import iht
+from paper_1802_04907_b200.problem import build_pool
+from workloads import gen as G
+
+from helpers import check_trajectory
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+TOL_T = 1e-3            # tensor-core (batched) path
+MIN_CHECKED = 10
+
+_PHI = None             # the matrix the forked quantiser workers read (copy-on-write)
+
+
+def _dev():
+    return torch.device("cuda:0")
+
+
+def _to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(_dev())
+
+
+def _quant_job(job):
+    bits, seed, cid, c, r0, r1 = job
+    return OQ.quantize_matrix(_PHI[r0:r1], bits, 0, seed, cid, c=c, row_offset=r0)[0]
+
+
+def oracle_codes(phi, bits, seed, copy_ids, c):
+    """{copy_id: codes (planes, M, N)} from oracle.quantize.quantize_matrix, row blocks in
+    parallel (forked workers; no CUDA in them)."""
+    global _PHI
+    _PHI = phi
+    M = phi.shape[0]
+    workers = max(1, min(16, os.cpu_count() or 1))
+    blk = max(256, -(-M // workers))
+    jobs = [(bits, seed, cid, c, r, min(M, r + blk)) for cid in copy_ids for r in range(0, M, blk)]
+    with mp.get_context("fork").Pool(workers) as pool:
+        parts = pool.map(_quant_job, jobs)
+    out, i = {}, 0
+    nb = len(range(0, M, blk))
+    for cid in copy_ids:
+        out[cid] = np.concatenate(parts[i:i + nb], axis=1)
+        i += nb
+    _PHI = None
+    return out
+
+
+class _CodesPool(OI.CopyPool):
+    """The oracle's CopyPool with its copies' codes computed up front (oracle_codes)."""
+
+    def __init__(self, phi, bits, seed, c, codes):
+        super().__init__(phi, bits, 0, seed, c, cache=2)
+        self._codes = codes
+
+    def codes(self, copy_id):
+        return self._codes[copy_id]
+
+
+def _run_gpu(pool, p, n_iter, y, nrhs=1):
+    sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, nrhs=nrhs)
+    fi, fv, fn = sol.run(_to_dev(y))
+    torch.cuda.synchronize()
+    out = sol.trace_arrays()
+    final = (fi.cpu().numpy(), fv.cpu().numpy(), fn.cpu().numpy())
+    sol.close()
+    return out, final
+
+
+def _check(ref, idx, val, nnz, final, s, tol, min_checked):
+    checked = check_trajectory(ref.trace, idx, val, nnz, s, tol)
+    assert checked >= min(len(ref.trace), min_checked), f"only {checked} iterations before a near-tie"
+    if checked == len(ref.trace):
+        fi, fv, fn = final
+        assert fi[:int(fn)].tolist() == ref.x_idx.tolist(), "final support differs from the oracle"
+    return checked
+
+
+# ------------------------------------------------------------------------------ config 2
+def test_config2_all_200_iterations_K2():
+    p = G.config_problem(2, K=2)
+    pool, c, _, _, _ = build_pool(p, 0, 1, _dev(), False)
+    (idx, val, nnz), final = _run_gpu(pool, p, p.n_iter, p.y)
+    c_ref = OQ.scale_c(p.phi)
+    assert np.float32(c) == c_ref
+    opool = _CodesPool(p.phi, p.b_phi, p.seed, c_ref, oracle_codes(p.phi, p.b_phi, p.seed, [0, 1], c_ref))
+    ref = OI.qniht(p.phi, p.y, p.s, p.n_iter, p.mu, p.b_phi, p.b_y, p.seed, 2, record=True, pool=opool)
+    checked = _check(ref, idx, val, nnz, (final[0], final[1], final[2][0]), p.s, TOL, 100)
+    print(f"config 2, K = 2: {checked}/{p.n_iter} iterations identical")
+
+
+def test_config2_first_10_iterations_K400():
+    p = G.config_problem(2)                     # K = 2 n* = 400, the bench's pool
+    pool, c, _, _, _ = build_pool(p, 0, 1, _dev(), False)
+    n_iter = 10
+    (idx, val, nnz), final = _run_gpu(pool, p, n_iter, p.y)
+    c_ref = OQ.scale_c(p.phi)
+    codes = oracle_codes(p.phi, p.b_phi, p.seed, list(range(2 * n_iter)), c_ref)
+    opool = _CodesPool(p.phi, p.b_phi, p.seed, c_ref, codes)
+    ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, p.K, record=True, pool=opool)
+    assert [r.adj_copy for r in ref.trace] == list(range(0, 2 * n_iter, 2))     # exact Algorithm 1
+    _check(ref, idx, val, nnz, (final[0], final[1], final[2][0]), p.s, TOL, n_iter)
+
+
+# ------------------------------------------------------------------------------ configs 3, 5
+@pytest.fixture(scope="module")
+def radio_oracle():
+    """Config 3's problem (= config 5's Phi and snapshot 0) with the two oracle copies of each
+    config's quantiser seed."""
+    p3 = G.config_problem(3, K=2)
+    p5 = G.config_problem(5, K=2)
+    assert np.array_equal(p3.phi, p5.phi)
+    c_ref = OQ.scale_c(p3.phi)
+    codes3 = oracle_codes(p3.phi, p3.b_phi, p3.seed, [0, 1], c_ref)
+    codes5 = oracle_codes(p5.phi, p5.b_phi, p5.seed, [0, 1], c_ref)
+    return p3, p5, c_ref, codes3, codes5
+
+
+def test_config3_20_iterations(radio_oracle):
+    p3, _, c_ref, codes3, _ = radio_oracle
+    n_iter = 20
+    pool, c, _, _, _ = build_pool(p3, 0, 1, _dev(), False)
+    assert np.float32(c) == c_ref
+    (idx, val, nnz), final = _run_gpu(pool, p3, n_iter, p3.y)
+    del pool
+    torch.cuda.empty_cache()
+    opool = _CodesPool(p3.phi, p3.b_phi, p3.seed, c_ref, codes3)
+    ref = OI.qniht(p3.phi, p3.y, p3.s, n_iter, p3.mu, p3.b_phi, p3.b_y, p3.seed, 2, record=True, pool=opool)
+    checked = _check(ref, idx, val, nnz, (final[0], final[1], final[2][0]), p3.s, TOL, n_iter)
+    print(f"config 3: {checked}/{n_iter} iterations identical")
+
+
+def test_config5_8_snapshots_20_iterations(radio_oracle):
+    _, p5, c_ref, _, codes5 = radio_oracle
+    n_iter, B = 20, 8
+    Y = np.ascontiguousarray(p5.meta["batch_y"][:, :B].T)            # (B, M): snapshots 0..7
+    pool, c, _, _, _ = build_pool(p5, 0, 1, _dev(), False, shard="cols")
+    assert np.float32(c) == c_ref
+    (idx, val, nnz), final = _run_gpu(pool, p5, n_iter, Y, nrhs=B)
+    del pool
+    torch.cuda.empty_cache()
+    idx, val, nnz = np.asarray(idx), np.asarray(val), np.asarray(nnz)
+    opool = _CodesPool(p5.phi, p5.b_phi, p5.seed, c_ref, codes5)
+    clean = total = 0
+    for b in range(B):
+        ref = OI.qniht(p5.phi, Y[b], p5.s, n_iter, p5.mu, p5.b_phi, p5.b_y, p5.seed, 2, record=True, pool=opool,
+                       snapshot=b)
+        # the tensor-core adjoint carries ~1e-4 relative error: a near-tie at the 1e-3 level may
+        # flip, after which the trajectories legitimately part
+        from helpers import near_tie
+        n_ok = 0
+        for n, rec in enumerate(ref.trace):
+            if near_tie(rec.a, rec.margin, p5.s, rel=1e-3):
+                break
+            k = int(nnz[n, b])
+            assert idx[n, b, :k].tolist() == ref.trace[n].x_idx.tolist(), (b, n)
+            err = np.linalg.norm(val[n, b, :k] - rec.x_val) / max(np.linalg.norm(rec.x_val), 1e-30)
+            assert err <= TOL_T, (b, n, err)
+            n_ok += 1
+        total += n_ok
+        if n_ok == n_iter:
+            clean += 1
+            assert final[0][b, :final[2][b]].tolist() == ref.x_idx.tolist(), b
+    print(f"config 5: {clean}/{B} snapshots clean to the end, {total}/{B * n_iter} snapshot-iterations identical")
+    assert clean >= B // 2 and total >= 3 * B * n_iter // 4, (clean, total)

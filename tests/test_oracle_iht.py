@@ -204,3 +204,56 @@ def test_row_sharded_adjoint_sums_to_full():
     r = rng.standard_normal(40) + 1j * rng.standard_normal(40)
     parts = sum(I.adjoint(A[a:b], r[a:b]) for a, b in [(0, 13), (13, 29), (29, 40)])
     np.testing.assert_allclose(parts, I.adjoint(A, r), rtol=1e-12)
+
+
+def _identify_copy(copies, vec_in, out, op):
+    """Which of the candidate dequantised copies reproduces `out` = op(copy, vec_in)?"""
+    hits = [k for k, D in enumerate(copies) if np.allclose(op(D, vec_in), out, rtol=1e-12, atol=1e-12)]
+    return hits
+
+
+@pytest.mark.parametrize("K", [2, 6])
+def test_copy_roles_follow_algorithm1(K):
+    """Pin of the copy-role map (readings c6-c8; Algorithm 1).  With strongly
+    distinct 2-bit copies, each iteration's recorded r and g are matched by brute force
+    against EVERY copy of the pool (each dequantised from oracle.quantize, the pinned
+    quantiser), independently of qniht's own bookkeeping:
+      * iteration 1's gradient is Phi-hat_1^dagger y-hat with Phi-hat_1 = copy 0 -- the
+        vector whose H_s gives Gamma^1 (P:347), since x^[1] = 0 (c8);
+      * the adjoint of iteration n uses the odd-labelled copy Phi-hat_{2n-1} and the forward
+        the even-labelled Phi-hat_{2n} (P:349, c7), i.e. 0-based ids (2n-2, 2n-1) mod K;
+      * forward and adjoint of one iteration never share a copy (the Q_1 / Q_2 independence
+        of the proof), and with K = 2 n* every copy is used exactly once.
+    Swapping the roles, or using one copy for both, fails this test."""
+    rng = np.random.default_rng(11)
+    M, N, s, n_iter = 40, 96, 4, K // 2 if K > 2 else 3
+    phi = rng.standard_normal((M, N)).astype(np.float32)
+    x = np.zeros(N)
+    x[rng.choice(N, s, replace=False)] = rng.standard_normal(s)
+    y = (phi.astype(np.float64) @ x).astype(np.float32)
+    res = I.qniht(phi, y, s, n_iter, 0.5, 2, 8, SEED, K, record=True)
+    c = Q.scale_c(phi)
+    copies = [Q.dequantize(Q.quantize_matrix(phi, 2, 0, SEED, k, c=c)[0], c, 2, 0) for k in range(K)]
+    for a in range(K):                      # the copies really are distinct at 2 bits
+        for b in range(a + 1, K):
+            assert np.abs(copies[a] - copies[b]).max() > 0.5 * c
+    # iteration 1: g = Phi-hat_1^T y-hat (x^[1] = 0, so r = y-hat), Gamma^1 from it (P:347)
+    assert np.array_equal(res.trace[0].r, res.y_hat)
+    assert _identify_copy(copies, res.y_hat, res.trace[0].g, lambda D, v: D.T @ v) == [0]
+    g1_idx, _ = I.hard_threshold(copies[0].T @ res.y_hat, s)
+    assert res.trace[0].x_idx.tolist() == g1_idx.tolist()        # mu > 0 keeps H_s's support
+    used = []
+    x_idx, x_val = np.zeros(0, np.int64), np.zeros(0)
+    for n, rec in enumerate(res.trace, start=1):
+        fwd = _identify_copy(copies, (x_idx, x_val), rec.r,
+                             lambda D, xv: res.y_hat - D[:, xv[0]] @ xv[1] if len(xv[0]) else res.y_hat)
+        adj = _identify_copy(copies, rec.r, rec.g, lambda D, v: D.T @ v)
+        assert adj == [(2 * n - 2) % K], (n, adj)
+        if n > 1:                            # at n = 1 x = 0: every copy gives r = y-hat
+            assert fwd == [(2 * n - 1) % K], (n, fwd)
+            assert fwd != adj
+            used.append(fwd[0])
+        used.append(adj[0])
+        x_idx, x_val = rec.x_idx, rec.x_val
+    if K == 2 * n_iter:                      # Algorithm 1 exactly: each copy once (fwd of n=1 unused)
+        assert sorted(used) == sorted(set(used)) and len(used) == K - 1
