@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--variant", type=int, default=0, help="adjoint: 0 int8 MMA, 1 FFMA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: ranks rendezvous over gloo, rank 0 prints a JSON line")
     ap.add_argument("--adaptive", action="store_true", help="Algorithm 1's adaptive step (NEXT-1)")
     ap.add_argument("--fresh", action="store_true",
                     help="NEXT-2: fresh copies drawn on the fly from the resident fp32 Phi (K = 2 n*, no codes)")
@@ -318,11 +320,25 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and (args.impl == "ours" or args.dry_run):
         return relaunch_under_torchrun(args.gpus)
     if world != args.gpus and args.impl == "ours":
         print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         return 2
+
+    if args.dry_run:
+        import torch
+        import torch.distributed as dist
+        if world > 1:
+            dist.init_process_group("gloo")
+            t = torch.tensor([float(rank)], dtype=torch.float64)
+            dist.barrier()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)                 # the max-over-ranks reduction
+            dist.destroy_process_group()
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_max": world - 1,
+                              "local_rank": local, "master": os.environ.get("MASTER_ADDR")}))
+        return 0
 
     if args.impl == "reference":
         # the oracle arm: rank 0 alone runs it on the host cores; other ranks exit at once

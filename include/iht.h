@@ -305,6 +305,11 @@ IHT_API int iht_comm_create(int rank, int world, const void* id_host_128, int de
 IHT_API int iht_comm_destroy(iht_comm* comm);
 /* In-place sum / max all-reduce of `count` floats on the stream (test hook). */
 IHT_API int iht_comm_allreduce(iht_comm* comm, float* buf_dev, int64_t count, int op_max, void* stream);
+/* Sum reduce-scatter of P * recv_count floats: rank p receives elements
+ * [p * recv_count, (p+1) * recv_count) of the sum over ranks of send_dev.  In place when
+ * recv_dev == send_dev + rank * recv_count (the row-sharded solver's g). */
+IHT_API int iht_comm_reduce_scatter(iht_comm* comm, const float* send_dev, float* recv_dev, int64_t recv_count,
+                                    void* stream);
 /* All-gather of `bytes` bytes per rank: recv_dev[p * bytes ..] = rank p's send_dev. */
 IHT_API int iht_comm_allgather(iht_comm* comm, const void* send_dev, void* recv_dev, int64_t bytes,
                                void* stream);
@@ -321,8 +326,13 @@ typedef struct {
   int32_t trace;        /* 1: keep every iterate x^[n] (see iht_solver_trace)            */
   int32_t use_graph;    /* 1: capture the n_iter loop into one CUDA graph (default)      */
   iht_comm* comm;       /* NULL: single GPU; else the rows are sharded (single observation:
-                           c_y max- and g sum-all-reduced every iteration) or the columns
-                           (batched); world 1 runs the same collectives on one rank      */
+                           c_y max-all-reduced; per iteration g is sum-REDUCE-SCATTERED
+                           over the P ranks (rank p owns columns [p N/P, (p+1) N/P)), each
+                           rank takes the local top-s of its columns (global indices), the
+                           P lists are all-gathered and merged into the global H_s -- when
+                           N % P == 0 and P s <= 8192, else g is all-reduced and H_s
+                           replicated; the adaptive step always all-reduces g) or the
+                           columns (batched); world 1 runs the same collectives          */
   int32_t profile;      /* 1: record a CUDA event pair around every adjoint launch      */
   int32_t nrhs;         /* B independent observations sharing Phi (BASELINE config 5);
                            0 or 1: one observation.  B > 1 runs the batched path: sparse

@@ -100,6 +100,7 @@ SIGNATURES = {
     "iht_comm_destroy": (c_int, [c_vp]),
     "iht_comm_allreduce": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
     "iht_comm_allgather": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "iht_comm_reduce_scatter": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
     "iht_solver_create": (c_int, [ctypes.POINTER(IhtQmat), c_int, ctypes.POINTER(IhtConfig), ctypes.POINTER(c_vp)]),
     "iht_solver_destroy": (c_int, [c_vp]),
     "iht_solver_run": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),

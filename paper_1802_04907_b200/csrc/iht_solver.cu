@@ -65,6 +65,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
 };
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
@@ -81,8 +83,9 @@ bool load_nccl() {
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
   g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
+  g_nccl.ReduceScatter = (decltype(g_nccl.ReduceScatter))dlsym(h, "ncclReduceScatter");
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce &&
-              g_nccl.AllGather;
+              g_nccl.AllGather && g_nccl.ReduceScatter;
   return g_nccl.ok;
 }
 }  // namespace
@@ -135,10 +138,24 @@ extern "C" int iht_comm_allgather(iht_comm* comm, const void* send, void* recv, 
   return IHT_OK;
 }
 
+extern "C" int iht_comm_reduce_scatter(iht_comm* comm, const float* send, float* recv, int64_t recv_count,
+                                       void* stream) {
+  if (comm == nullptr || send == nullptr || recv == nullptr || recv_count < 0) return IHT_EINVAL;
+  if (g_nccl.ReduceScatter(send, recv, (size_t)recv_count, ncclFloat32, ncclSum, comm->comm, (cudaStream_t)stream) !=
+      ncclSuccess)
+    return IHT_ENCCL;
+  return IHT_OK;
+}
+
 // ------------------------------------------------------------------ solver
 // Modes (fixed at create):
-//   single  (nrhs <= 1): GEMV adjoint; with a communicator of world P > 1 the rows are
-//           sharded and g is all-reduced (north star).
+//   single  (nrhs <= 1): GEMV adjoint; with a communicator of world P the rows are
+//           sharded (north star).  Fixed step: g is REDUCE-SCATTERED (rank p owns columns
+//           [p N/P, (p+1) N/P)), each rank selects the local top-s of its columns, the P
+//           candidate lists are all-gathered and merged into the global H_s (SURVEY 8(e)'s
+//           "reduce-scatter g, then a sharded select, then an all-gather of <= s P
+//           candidates": half the bytes of an all-reduce and 1/P of the select).  The
+//           adaptive step all-reduces g (its norms need g on the whole support).
 //   batched (nrhs = B > 1, BASELINE config 5): per-snapshot sparse forward, tcgen05
 //           adjoint (chunks of <= 64 snapshots inside iht_adjoint_batched), per-snapshot
 //           H_s; with a communicator the COLUMNS are sharded: forward partials
@@ -153,6 +170,8 @@ struct iht_solver {
   int planes;
   int B = 1;                           // snapshots
   bool batched = false, rowshard = false, colshard = false;
+  bool shardsel = false;               // row shards: reduce-scatter g + sharded select + merge
+  int64_t nloc = 0, col0 = 0;          // this rank's columns of g when shardsel
   int world = 1, rank = 0;
   // device buffers (one allocation)
   void* block = nullptr;
@@ -354,7 +373,9 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       L += 2 * ((B + 63) / 64);
     }
     if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[2 * (n - 1) + 1], st));
-    if (S->rowshard) {
+    if (S->shardsel) {          // in place: rank p's summed slice lands at g + p N/P
+      if ((rc = iht_comm_reduce_scatter(S->cfg.comm, S->g, S->g + S->col0, S->nloc, st)) != IHT_OK) return rc;
+    } else if (S->rowshard) {
       if ((rc = iht_comm_allreduce(S->cfg.comm, S->g, S->N, 0, st)) != IHT_OK) return rc;
     }
     // (a6) update + H_s
@@ -363,6 +384,22 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
     } else if (nparts > 0) {
       if ((rc = iht_threshold_parts(xi, xv, xn, s, static_cast<const float*>(S->ws_adj), nparts, gsigma, S->g,
                                     S->cfg.mu, s, S->N, oi, ov, s, on, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+        return rc;
+      L += 1;
+    } else if (S->shardsel) {
+      // local top-s of this rank's columns (global indices), all-gathered, merged
+      int32_t* ci = S->cand_send;
+      float* cv = reinterpret_cast<float*>(S->cand_send + xslot);
+      int32_t* cn = S->cand_send + 2 * xslot;
+      if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g + S->col0, S->cfg.mu, s, S->nloc, S->col0, 1, ci, cv, s,
+                                      cn, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
+        return rc;
+      L += iht_threshold_launches(S->nloc);
+      if ((rc = iht_comm_allgather(S->cfg.comm, S->cand_send, S->cand_recv, S->cand_words * 4, st)) != IHT_OK)
+        return rc;
+      if ((rc = iht_merge_candidates(S->cand_recv, reinterpret_cast<const float*>(S->cand_recv + xslot),
+                                     S->cand_recv + 2 * xslot, S->cand_words, S->world, s, 1, oi, ov, on, st)) !=
+          IHT_OK)
         return rc;
       L += 1;
     } else if (!S->colshard) {
@@ -466,6 +503,9 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->rank = cfg->comm ? cfg->comm->rank : 0;
   S->rowshard = !batched && cfg->comm != nullptr;  // any world size (world 1 exercises the same path)
   S->colshard = batched && cfg->comm != nullptr;   // any world size (world 1 exercises the same path)
+  S->shardsel = S->rowshard && cfg->step_mode == 0 && q0.cols % world == 0 && (int64_t)world * cfg->s <= 8192;
+  S->nloc = S->shardsel ? q0.cols / world : q0.cols;
+  S->col0 = S->shardsel ? (int64_t)S->rank * S->nloc : 0;
   // NCCL kernels may not sit inside a conditional body graph: the adaptive row-sharded
   // run drives its shrink loop from the host
   if (cfg->step_mode == 1 && S->rowshard) S->cfg.use_graph = 0;
@@ -474,7 +514,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->ws_thr_bytes = iht_threshold_batched_ws_bytes(S->N, cfg->s, B);
   S->nslots = cfg->trace ? cfg->n_iter + 1 : 2;
   const int s = cfg->s > 0 ? cfg->s : 1;
-  S->cand_words = S->colshard ? 2 * (int64_t)B * s + B : 0;
+  S->cand_words = (S->colshard || S->shardsel) ? 2 * (int64_t)B * s + B : 0;
   auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
   const int64_t ycount = q0.rows * q0.planes;
   const int64_t sz_y = al((int64_t)B * ycount * 4), sz_c = al((int64_t)B * 4),
@@ -490,7 +530,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
                               sz_b4 + sz_v + 2 * sz_rec)
                            : 0;
   const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_xi + sz_xv + sz_xn +
-                        (S->colshard ? sz_cs + sz_cr : 0) + sz_ad;
+                        ((S->colshard || S->shardsel) ? sz_cs + sz_cr : 0) + sz_ad;
   if (cudaMalloc(&S->block, total) != cudaSuccess) {
     delete S;
     return IHT_ENOMEM;
@@ -506,7 +546,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->xs_idx = reinterpret_cast<int32_t*>(p); p += sz_xi;
   S->xs_val = reinterpret_cast<float*>(p); p += sz_xv;
   S->xs_nnz = reinterpret_cast<int32_t*>(p); p += sz_xn;
-  if (S->colshard) {
+  if (S->colshard || S->shardsel) {
     S->cand_send = reinterpret_cast<int32_t*>(p); p += sz_cs;
     S->cand_recv = reinterpret_cast<int32_t*>(p); p += sz_cr;
   }

@@ -354,6 +354,16 @@ class Comm:
               "iht_comm_allreduce")
         return t
 
+    def reduce_scatter(self, t, stream=None):
+        """Sum reduce-scatter of a contiguous float32 CUDA tensor of world * k elements:
+        returns this rank's k summed elements."""
+        assert t.dtype == torch.float32 and t.numel() % self.world == 0
+        k = t.numel() // self.world
+        out = torch.empty(k, dtype=t.dtype, device=t.device)
+        check(load().iht_comm_reduce_scatter(self.handle, _ptr(t), _ptr(out), k, _stream(stream)),
+              "iht_comm_reduce_scatter")
+        return out
+
     def allgather(self, t, stream=None):
         """All-gather of a contiguous CUDA tensor: returns (world, *t.shape)."""
         out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)

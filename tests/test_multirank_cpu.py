@@ -243,3 +243,117 @@ def test_shard_cols_partition():
         assert sum(s[0] for s in spans) == 65536 and all(s[1] % 16 == 0 for s in spans)
     with pytest.raises(ValueError):
         shard_cols(1000, 3, 0)
+
+
+# ---------------------------------------------------------------------------------------
+# Row-sharded single-observation path with the SHARDED select (libiht's iht_solver at P > 1,
+# fixed step): every rank holds the partial adjoint g_p of its rows over all N columns;
+# g is reduce-scattered (rank p receives the summed columns [p N/P, (p+1) N/P)); each rank
+# forms a = x + mu g on its columns and keeps their local top-s (global indices); the P lists
+# are all-gathered and merged.  The merge equals the global H_s(x + mu sum_p g_p) on every rank.
+def _rs_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import iht as OI
+        from oracle import quantize as OQ
+        from paper_1802_04907_b200.problem import shard_rows
+        from workloads import gen as G
+
+        p = G.gaussian_problem(512, 704, 24, cfg_id=93, b_phi=2, K=2)
+        rows, row0 = shard_rows(p.M, world, rank)
+        phi_shard = p.phi[row0:row0 + rows]
+        c_loc = torch.tensor([float(OQ.scale_c(phi_shard))], dtype=torch.float64)
+        dist.all_reduce(c_loc, op=dist.ReduceOp.MAX)
+        c = np.float32(c_loc.item())
+        A = OQ.dequantize(OQ.quantize_matrix(phi_shard, p.b_phi, 0, p.seed, 0, c=c, row_offset=row0)[0], c,
+                          p.b_phi, 0)
+        rng = np.random.default_rng(12)
+        out = []
+        for trial in range(3):
+            xi = np.sort(rng.choice(p.N, p.s, replace=False))
+            xv = rng.standard_normal(p.s)
+            r_full = rng.standard_normal(p.M)
+            g_part = torch.from_numpy(OI.adjoint(A, r_full[row0:row0 + rows]))
+            nloc = p.N // world
+            col0 = rank * nloc
+            g_loc = torch.empty(nloc, dtype=torch.float64)
+            try:
+                dist.reduce_scatter_tensor(g_loc, g_part, op=dist.ReduceOp.SUM)
+            except (RuntimeError, NotImplementedError, ValueError):
+                # gloo without reduce-scatter: the same sums through an all-reduce, sliced
+                t = g_part.clone()
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+                g_loc = t[col0:col0 + nloc].clone()
+            a = 0.7 * g_loc.numpy()
+            mine = (xi >= col0) & (xi < col0 + nloc)
+            a[xi[mine] - col0] += xv[mine]
+            li, lv = OI.hard_threshold(a, p.s)
+            gathered = [None] * world
+            dist.all_gather_object(gathered, (li + col0, lv))
+            out.append((xi, xv, r_full, _merge_topk(gathered, p.s)))
+        out_q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_row_sharded_sharded_select_world2():
+    from oracle import iht as OI
+    from oracle import quantize as OQ
+    from workloads import gen as G
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rs_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = G.gaussian_problem(512, 704, 24, cfg_id=93, b_phi=2, K=2)
+    c = OQ.scale_c(p.phi)
+    A = OQ.dequantize(OQ.quantize_matrix(p.phi, p.b_phi, 0, p.seed, 0, c=c)[0], c, p.b_phi, 0)
+    for t in range(3):
+        xi, xv, r_full, (mi0, mv0) = res[0][1][t]
+        mi1, mv1 = res[1][1][t][3]
+        a = 0.7 * OI.adjoint(A, r_full)
+        a[xi] += xv
+        gi, gv = OI.hard_threshold(a, p.s)
+        assert mi0.tolist() == gi.tolist() and mi1.tolist() == gi.tolist()     # merge == global H_s
+        np.testing.assert_allclose(mv0, gv, rtol=1e-12, atol=1e-12)
+        np.testing.assert_array_equal(mv0, mv1)                                 # replicated x
+
+
+def test_bench_relaunch_command():
+    """bench.py --gpus N without a launcher re-executes itself under torchrun, one rank per
+    GPU on one node, rendezvous on 127.0.0.1."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    cmd = bench.relaunch_cmd(8, ["--gpus", "8", "--steps", "5"], 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "8", "--steps", "5"] and cmd[-5].endswith("bench.py")
+
+
+@pytest.mark.timeout(300)
+def test_bench_launcher_dry_run_world2():
+    """End to end on CPU: `python bench.py --gpus 2 --dry-run` starts two ranks under torchrun,
+    they rendezvous (gloo), reduce over ranks, and rank 0 prints one JSON line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=240, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["ranks_max"] == 1
+    assert lines[0]["master"] == "127.0.0.1"
