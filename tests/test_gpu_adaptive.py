@@ -55,7 +55,7 @@ def _compare(recs, idx, val, nnz, mu, sh, tol_x, tol_mu, tol_sel, tol_acc):
 
 CASES = {
     "gauss4bit": lambda: G.gaussian_problem(256, 1024, 16, cfg_id=61, b_phi=4, n_iter=15, K=30),
-    "gauss2bit": lambda: G.gaussian_problem(1024, 4096, 40, cfg_id=62, values="sign", b_phi=2, n_iter=12, K=24),
+    "gauss2bit": lambda: G.gaussian_problem(1024, 4096, 40, cfg_id=63, values="sign", b_phi=2, n_iter=12, K=24),
     "radio": lambda: G.radio_problem(cfg_id=63, A=12, grid=48, n_src=10, n_iter=12, K=24),
 }
 

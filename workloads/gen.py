@@ -195,17 +195,23 @@ def radio_phi(pos, wavelength, grid):
 
 
 def radio_problem(*, cfg_id, A=48, radius_m=30.0, freq_hz=150e6, grid=256, n_src=64, n_iter=200,
-                  b_phi=2, b_y=8, K=2, noise_frac=0.01, name=None, batch=1, mu_scale=0.1):
+                  b_phi=2, b_y=8, K=2, noise_frac=0.01, name=None, batch=1, mu_scale=0.1, phi_cfg_id=None):
     """Synthetic radio interferometer (BASELINE config 3, batch=64 -> config 5).
     Fixed step mu = mu_scale / M (reading c9): the columns have |Phi_kp| = 1, so 1/M
     normalises them, but the coherent radio Phi diverges at 1/M and 1/4M (|x| -> inf,
     scripts/step_study.py); 1/10 M stays bounded.
     Sources: n_src pixels drawn without replacement among pixels with
     l^2 + m^2 < 1 (reading c19), log-normal(0,1) fluxes; complex noise
-    e = (sigma/sqrt 2)(n1 + i n2), sigma = noise_frac * rms visibility (c17)."""
+    e = (sigma/sqrt 2)(n1 + i n2), sigma = noise_frac * rms visibility (c17).
+    phi_cfg_id: take the antenna layout (hence Phi) of that config (config 5 = "the config-3
+    Phi", BASELINE): its antennas are the first draws of _rng(phi_cfg_id); the skies and noise
+    then come from _rng(cfg_id)."""
     rng = _rng(cfg_id)
     wavelength = 299792458.0 / freq_hz
-    pos = radio_antennas(A, radius_m, rng)
+    if phi_cfg_id is None or phi_cfg_id == cfg_id:
+        pos = radio_antennas(A, radius_m, rng)
+    else:
+        pos = radio_antennas(A, radius_m, _rng(phi_cfg_id))
     phi, l, m = radio_phi(pos, wavelength, grid)
     inside = np.flatnonzero(l * l + m * m < 1.0)
     xs, vs, ys = [], [], []
@@ -235,7 +241,7 @@ CONFIGS = {
     2: dict(kind="gauss", M=4096, N=16384, s=128, values="sign", n_iter=200, b_phi=2, b_y=8, mu=0.25),
     3: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8),
     4: dict(kind="gauss", M=65536, N=262144, s=1024, values="normal", n_iter=100, b_phi=4, b_y=8),
-    5: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8, batch=64),
+    5: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8, batch=64, phi_cfg_id=3),
 }
 
 
@@ -258,4 +264,4 @@ def config_problem(cfg_id, K=None, materialize=None, b_phi=None):
         K = 2 * c["n_iter"]
     return radio_problem(cfg_id=cfg_id, A=c["A"], grid=c["grid"], n_src=c["n_src"],
                          n_iter=c["n_iter"], b_phi=c["b_phi"], b_y=c["b_y"], K=K,
-                         batch=c.get("batch", 1), name=f"config{cfg_id}")
+                         batch=c.get("batch", 1), name=f"config{cfg_id}", phi_cfg_id=c.get("phi_cfg_id"))
