@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define IHT_ABI_VERSION 2
+#define IHT_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define IHT_API __attribute__((visibility("default")))
@@ -352,6 +352,14 @@ typedef struct {
   float step_c;         /* c of the acceptance test (0 < c < 1; SPEC default 1e-3)       */
   float step_k;         /* k of the shrink mu / (k (1 - c)), k > 1 / (1 - c) (default 2) */
   int32_t max_shrink;   /* bound on proposals per iteration; the last is kept    */
+  int32_t fused;        /* 1: when the problem fits (single observation, fixed step, no
+                           communicator, stored copies, variant 0, stacked rows small enough
+                           for r limbs in one CTA's shared memory: configs 1-3), the WHOLE
+                           n-iteration loop runs as ONE persistent cooperative kernel (one
+                           CTA per SM, three grid barriers per iteration, the next
+                           iteration's adjoint codes prefetched into shared memory under the
+                           select and the forward; same arithmetic as the per-step kernels
+                           up to fp32 summation order).  0: per-step kernels always.         */
 } iht_config;
 
 /* Stateful solver over a pool of K quantised copies pool[0..K) (all with the
@@ -402,6 +410,10 @@ IHT_API int iht_solver_adjoint_times(iht_solver* solver, float* ms_host);
 /* Adaptive step (cfg.step_mode = 1): the accepted mu and the number of shrinks of every
  * iteration of the LAST run, [n_iter][B] each (host arrays).  Synchronises the stream. */
 IHT_API int iht_solver_steps(iht_solver* solver, float* mu_host, int32_t* shrinks_host, void* stream);
+/* 1 if the solver runs the fused persistent kernel (cfg.fused and the problem fits), else 0;
+ * negative on a NULL solver.  With cfg.profile, iht_solver_adjoint_times then reports the
+ * fused kernel's duration divided evenly over the n_iter iterations. */
+IHT_API int iht_solver_fused(const iht_solver* solver);
 /* Number of kernel launches one iht_solver_run enqueues (for gpu_launches); with the
  * adaptive step it counts one pass of the shrink loop per iteration. */
 IHT_API int64_t iht_solver_launches_per_run(const iht_solver* solver);

@@ -57,6 +57,7 @@ class IhtConfig(ctypes.Structure):
         ("adjoint_variant", c_i32), ("seed", c_u64), ("trace", c_i32), ("use_graph", c_i32),
         ("comm", c_vp), ("profile", c_i32), ("nrhs", c_i32),
         ("step_mode", c_i32), ("step_c", c_f32), ("step_k", c_f32), ("max_shrink", c_i32),
+        ("fused", c_i32),
     ]
 
 
@@ -108,6 +109,7 @@ SIGNATURES = {
     "iht_solver_buffers": (c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     "iht_solver_adjoint_times": (c_int, [c_vp, c_vp]),
     "iht_solver_launches_per_run": (c_i64, [c_vp]),
+    "iht_solver_fused": (c_int, [c_vp]),
     "iht_solver_steps": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "iht_solve": (c_int, [ctypes.POINTER(IhtQmat), c_int, ctypes.POINTER(IhtConfig), c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
 }

@@ -40,6 +40,15 @@ int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t*
                         int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
                         void* stream);
 
+// Fused small-problem solver (iht_fused.cu): the whole fixed-step Algorithm 1 loop as one
+// persistent cooperative kernel.  create returns IHT_EUNSUPPORTED when the problem does not
+// fit (then the solver keeps its per-step kernels).
+struct iht_fused_state;
+int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, int trace, const float* yhat,
+                     float* r, float* g, int32_t* xs_idx, float* xs_val, int32_t* xs_nnz, iht_fused_state** out);
+int iht_fused_enqueue(iht_fused_state* S, void* stream);
+void iht_fused_destroy(iht_fused_state* S);
+
 namespace iht {
 
 constexpr int kNumSMs = 148;  // B200; launch code queries the device, this is a default

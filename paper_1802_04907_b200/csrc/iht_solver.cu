@@ -7,6 +7,7 @@
 #include <math.h>
 #include <nccl.h>   // types and enum values only: NCCL itself is loaded with dlopen
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -199,6 +200,7 @@ struct iht_solver {
   std::vector<cudaEvent_t> ev;   // profile: [2 * n_iter] start/stop of each adjoint
   int64_t launches = 0;
   int final_slot = 0;
+  iht_fused_state* fused = nullptr;    // the whole loop as one persistent kernel (iht_fused.cu)
 };
 
 // Event record that survives stream capture: inside a capture it becomes an event-record
@@ -323,6 +325,15 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
   L += 1;
   // x^[1] = 0 (reading c8): slot 0 holds x^[1]
   IHT_CUDA_CHECK(cudaMemsetAsync(S->xs_nnz, 0, sizeof(int32_t) * B, st));
+  if (S->fused && S->cfg.n_iter > 0) {   // the n* iterations in one persistent kernel
+    if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[0], st));
+    if ((rc = iht_fused_enqueue(S->fused, st)) != IHT_OK) return rc;
+    if (!S->ev.empty()) IHT_CUDA_CHECK(record_event(S->ev[1], st));
+    L += 1;
+    S->final_slot = S->cfg.trace ? S->cfg.n_iter : (S->cfg.n_iter & 1);
+    if (launches) *launches = L;
+    return IHT_OK;
+  }
   const int K = (int)S->pool.size();
   const int64_t xslot = (int64_t)B * s;
   // single observation, fixed step, int8-MMA adjoint, no g all-reduce, fused threshold:
@@ -432,6 +443,12 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
 
 static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg, const iht_fmat* fm,
                               iht_solver** out);
+
+static bool fused_disabled_by_env() {   // profiling switch: IHT_FUSED=0 keeps the per-step kernels
+  static int v = -1;
+  if (v < 0) v = (getenv("IHT_FUSED") && atoi(getenv("IHT_FUSED")) == 0) ? 1 : 0;
+  return v == 1;
+}
 
 extern "C" int iht_solver_create(const iht_qmat* pool, int K, const iht_config* cfg, iht_solver** out) {
   return solver_create_impl(pool, K, cfg, nullptr, out);
@@ -579,6 +596,15 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
     delete S;
     return IHT_ECUDA;
   }
+  if (cfg->fused && !batched && !fm && !S->rowshard && cfg->step_mode == 0 && cfg->adjoint_variant == 0 &&
+      cfg->n_iter > 0 && !fused_disabled_by_env()) {
+    const int frc = iht_fused_create(pool, K, cfg->s, cfg->n_iter, cfg->mu, cfg->trace, S->yhat, S->r, S->g,
+                                     S->xs_idx, S->xs_val, S->xs_nnz, &S->fused);
+    if (frc != IHT_OK && frc != IHT_EUNSUPPORTED) {
+      iht_solver_destroy(S);
+      return frc;
+    }
+  }
   if (cfg->profile) {
     S->ev.resize(2 * (size_t)cfg->n_iter);
     for (auto& e : S->ev) {
@@ -594,6 +620,13 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
 
 extern "C" int iht_solver_adjoint_times(iht_solver* S, float* ms) {
   if (S == nullptr || ms == nullptr || S->ev.empty()) return IHT_EINVAL;
+  if (S->fused) {                      // one event pair around the fused kernel
+    float t = 0.0f;
+    IHT_CUDA_CHECK(cudaEventSynchronize(S->ev[1]));
+    IHT_CUDA_CHECK(cudaEventElapsedTime(&t, S->ev[0], S->ev[1]));
+    for (int n = 0; n < S->cfg.n_iter; ++n) ms[n] = t / (float)S->cfg.n_iter;
+    return IHT_OK;
+  }
   IHT_CUDA_CHECK(cudaEventSynchronize(S->ev.back()));
   for (int n = 0; n < S->cfg.n_iter; ++n) IHT_CUDA_CHECK(cudaEventElapsedTime(&ms[n], S->ev[2 * n], S->ev[2 * n + 1]));
   return IHT_OK;
@@ -604,6 +637,7 @@ extern "C" int iht_solver_destroy(iht_solver* S) {
   for (auto& e : S->ev)
     if (e) cudaEventDestroy(e);
   if (S->exec) cudaGraphExecDestroy(S->exec);
+  iht_fused_destroy(S->fused);
   if (S->cap_stream) cudaStreamDestroy(S->cap_stream);
   if (S->body_stream) cudaStreamDestroy(S->body_stream);
   if (S->block) cudaFree(S->block);
@@ -692,6 +726,8 @@ extern "C" int iht_solver_buffers(iht_solver* S, const float** yhat, const float
 }
 
 extern "C" int64_t iht_solver_launches_per_run(const iht_solver* S) { return S ? S->launches : -1; }
+
+extern "C" int iht_solver_fused(const iht_solver* S) { return S ? (S->fused != nullptr) : -1; }
 
 extern "C" int iht_solver_steps(iht_solver* S, float* mu_host, int32_t* shrinks_host, void* stream) {
   if (S == nullptr || mu_host == nullptr || shrinks_host == nullptr || S->cfg.step_mode != 1) return IHT_EINVAL;

@@ -383,9 +383,11 @@ class Solver:
     and the outputs are (B, s) / (B,)."""
 
     def __init__(self, pool, s, n_iter, mu, b_y, seed, level_mode=0, adjoint_variant=0, trace=False,
-                 use_graph=True, comm=None, profile=False, nrhs=1, adaptive=False, c=1e-3, k=2.0, max_shrink=60):
+                 use_graph=True, comm=None, profile=False, nrhs=1, adaptive=False, c=1e-3, k=2.0, max_shrink=60,
+                 fused=True):
         """pool: list of QCopy (stored copies), or a FreshPhi (NEXT-2: copies drawn on the fly,
-        K = 2 n*)."""
+        K = 2 n*).  fused: run the whole loop as one persistent kernel when the problem fits
+        (iht_config.fused); False keeps the per-step kernels."""
         lib = load()
         self.pool = pool                     # keep the code / Phi tensors alive
         self.s, self.n_iter = s, n_iter
@@ -394,7 +396,8 @@ class Solver:
         cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
                         adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
                         comm=comm.handle if comm is not None else None, profile=int(profile), nrhs=self.nrhs,
-                        step_mode=int(adaptive), step_c=float(c), step_k=float(k), max_shrink=int(max_shrink))
+                        step_mode=int(adaptive), step_c=float(c), step_k=float(k), max_shrink=int(max_shrink),
+                        fused=int(fused))
         h = ctypes.c_void_p()
         if isinstance(pool, FreshPhi):
             check(lib.iht_solver_create_fresh(ctypes.byref(pool.desc), ctypes.byref(cfg), ctypes.byref(h)),
@@ -462,6 +465,11 @@ class Solver:
 
     def launches_per_run(self):
         return int(load().iht_solver_launches_per_run(self.handle))
+
+    @property
+    def fused(self):
+        """True when the solve runs as the single fused persistent kernel."""
+        return bool(load().iht_solver_fused(self.handle))
 
     def close(self):
         if self.handle:

@@ -1,0 +1,3 @@
+#!/bin/bash
+OUT=gpurun_out/r02g02; mkdir -p $OUT
+timeout 600 python scripts/r02/fused_check.py > $OUT/fused_check.log 2>&1; echo "rc=$?" >> $OUT/fused_check.log

@@ -44,7 +44,7 @@ def test_no_undeclared_signature():
 
 
 def test_sizes_and_strings(lib):
-    assert lib.iht_abi_version() == 2
+    assert lib.iht_abi_version() == 3
     assert lib.iht_rows_pad(1) == 256 and lib.iht_rows_pad(256) == 256 and lib.iht_rows_pad(257) == 512
     assert lib.iht_strip_bytes(65536, 1, 4) == 32768            # config 4: 32 KiB strips
     assert lib.iht_strip_bytes(4096, 1, 2) == 1024              # config 2

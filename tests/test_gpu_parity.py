@@ -299,8 +299,8 @@ def test_teacher_forced_iterations(case):
 
 
 @pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("graph", [True, False])
-def test_free_running_solver(case, graph):
+@pytest.mark.parametrize("graph,fused", [(True, True), (True, False), (False, False)])
+def test_free_running_solver(case, graph, fused):
     """Whole solve through iht_solver (CUDA graph) vs the oracle trajectory: identical
     supports and x within 1e-4 up to the first near-tie; final support identical
     when no near-tie occurred."""
@@ -309,7 +309,8 @@ def test_free_running_solver(case, graph):
     ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, p.K)
     c = OQ.scale_c(p.phi)
     pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c, p.seed)
-    sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, use_graph=graph)
+    sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, use_graph=graph, fused=fused)
+    assert sol.fused == fused                 # every case fits the fused persistent kernel
     sol.run(_to_dev(p.y))
     idx, val, nnz = sol.trace_arrays()
     checked = check_trajectory(ref.trace, idx, val, nnz, p.s, TOL)
@@ -354,7 +355,7 @@ def test_solver_world1_row_shard_path():
     comm = iht.Comm(0, 1, 0)
     try:
         for adaptive in (False, True):
-            ref = iht.Solver(pool, p.s, 12, p.mu, p.b_y, p.seed, adaptive=adaptive)
+            ref = iht.Solver(pool, p.s, 12, p.mu, p.b_y, p.seed, adaptive=adaptive, fused=False)
             ri, rv, rn = [t.cpu().clone() for t in ref.run(_to_dev(p.y))]
             sol = iht.Solver(pool, p.s, 12, p.mu, p.b_y, p.seed, comm=comm, adaptive=adaptive)
             gi, gv, gn = sol.run(_to_dev(p.y))
