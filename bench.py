@@ -531,6 +531,17 @@ def main():
                 "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside a "
                        "profiled copy of the solver graph (run after the timed region); ops = 2 R N B useful (x2 executed: two int8 limbs of r)"}
 
+    fused = sol.fused
+    fused_roof = None
+    if fused:   # the whole loop is one persistent kernel: its roofline is the iteration's bytes
+        fused_roof = {"bound": "hbm", "kernel": "fused_iht_kernel (all n* iterations in one persistent launch)",
+                      "achieved": iter_bytes / (adj_avg / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                      "frac": iter_bytes / (adj_avg / 1e3) / 1e9 / peak, "peak_kind": peak_kind, "traffic": traffic,
+                      "algorithmic_bytes_per_launch": iter_bytes * p.n_iter, "avg_launch_ms": adj_avg * p.n_iter,
+                      "launches_timed": len(adj_ms) // max(p.n_iter, 1),
+                      "how": "CUDA event pair around the fused kernel inside a profiled copy of the solver graph "
+                             "(run after the timed region); achieved = algorithmic bytes of one iteration (adjoint "
+                             "copy + forward columns + vectors) / per-iteration time"}
     if rank != 0:
         return 0
     cb = None
@@ -559,7 +570,7 @@ def main():
                       f"on both sides, max over ranks); median region reported"}),
         "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
                 "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},
-        "roofline": roof if B > 1 else
+        "roofline": roof if B > 1 else fused_roof if fused else
                     {"bound": "hbm", "kernel": "adjoint_fresh_kernel (fp32 Phi + Philox, NEXT-2)" if args.fresh else
                                "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
                      "achieved": adj_gbs, "peak": peak, "unit": "GB/s", "frac": adj_gbs / peak,
@@ -570,6 +581,7 @@ def main():
         "cpu_baseline": cb,
         "e2e": e2e,
         "gpu_launches": int(launches_per_run * args.steps),
+        "fused_solver": fused,
         "clocks": clocks,
         "preprocess": {**prep, "c_phi": c_phi, "setup_s": setup_s,
                        "quantize_frac_of_hbm": (prep["quantize_GBps"] / peak) if prep.get("quantize_GBps") else None,

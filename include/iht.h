@@ -352,14 +352,16 @@ typedef struct {
   float step_c;         /* c of the acceptance test (0 < c < 1; SPEC default 1e-3)       */
   float step_k;         /* k of the shrink mu / (k (1 - c)), k > 1 / (1 - c) (default 2) */
   int32_t max_shrink;   /* bound on proposals per iteration; the last is kept    */
-  int32_t fused;        /* 1: when the problem fits (single observation, fixed step, no
+  int32_t fused;        /* 1 (auto): when the problem fits (single observation, fixed step, no
                            communicator, stored copies, variant 0, stacked rows small enough
                            for r limbs in one CTA's shared memory: configs 1-3), the WHOLE
                            n-iteration loop runs as ONE persistent cooperative kernel (one
                            CTA per SM, three grid barriers per iteration, the next
                            iteration's adjoint codes prefetched into shared memory under the
                            select and the forward; same arithmetic as the per-step kernels
-                           up to fp32 summation order).  0: per-step kernels always.         */
+                           up to fp32 summation order) and a copy is >= 2 MiB (smaller
+                           problems run faster as per-step kernels); 2: whenever it fits;
+                           0: per-step kernels always.                                      */
 } iht_config;
 
 /* Stateful solver over a pool of K quantised copies pool[0..K) (all with the

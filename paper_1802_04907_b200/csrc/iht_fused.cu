@@ -51,7 +51,9 @@ struct FusedArgs {
   int L;
   float sigma, mu;
   int s, n_iter;
-  int ntiles, nslot, tile_bytes, nchunks, wpc, words_total, cap_c, s_cap;
+  int ntiles, tile_bytes, nchunks, wpc, words_total, cap_c, s_cap;
+  int nsub, block_bytes, mslot;        // ring: a tile = nsub blocks; each warp owns mslot block slots
+  int limb_stride;                     // bytes between the 3 limb planes (Rpad + 64: bank spread)
   const float* yhat;                   // [Rpad] stacked, pads 0
   float* r;                            // [Rpad] scratch (and the last r)
   float* g;                            // [N] the last g
@@ -67,7 +69,10 @@ struct FusedArgs {
   float* cand_val;
   int* cand_cnt;                       // [G]
   // dynamic shared memory offsets (bytes)
-  int off_bars, off_limbs, off_fc, off_as, off_x, off_u;
+  int off_bars, off_limbs, off_fc, off_as, off_x, off_u, off_tab, off_h;
+  long long* tl;                       // profiling (IHT_FUSED_TL): [64][16] globaltimer stamps of CTA tl_cta
+  int tl_cta;
+  int probe;                           // profiling (IHT_FUSED_PROBE): 1 no MMA work, 2 no refills inside A, 4 no flush
 };
 
 __device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t parity) {
@@ -106,18 +111,19 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t ring_u = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t full_u = (uint32_t)__cvta_generic_to_shared(smem + a.off_bars);
-  const uint32_t empty_u = full_u + 8 * a.nslot;
   uint8_t* limbs = smem + a.off_limbs;
   int* Fc = reinterpret_cast<int*>(smem + a.off_fc);
   int* Sl = Fc + a.nchunks;                                       // [chunk][3]
   float* as = reinterpret_cast<float*>(smem + a.off_as);         // [cap_c] a of this CTA's columns
   int32_t* xi_s = reinterpret_cast<int32_t*>(smem + a.off_x);    // the current x (support)
   float* xv_s = reinterpret_cast<float*>(xi_s + a.s_cap);
-  long long* Vs = reinterpret_cast<long long*>(smem + a.off_u);  // A: exact chunk sums [tile][chunk][16]
-  int* hist_s = reinterpret_cast<int*>(smem + a.off_u);          // S1: the global histogram
+  int* Vs = reinterpret_cast<int*>(smem + a.off_u);              // A: exact limb sums [tile][chunk][16][3]
+  int* hist_s = reinterpret_cast<int*>(smem + a.off_h);          // A: the CTA's histogram; S1: the global one
   int32_t* ci_s = reinterpret_cast<int32_t*>(smem + a.off_u);    // S2: staged candidates
   float* cv_s = reinterpret_cast<float*>(ci_s + kFuCandCap);
-  int* sel_hist = reinterpret_cast<int*>(cv_s + kFuCandCap);     // S2: offsets + select histogram
+  int* sel_hist = reinterpret_cast<int*>(cv_s + kFuCandCap);     // S2: offsets | histogram / keys | positions | flags
+  const uint8_t** ctab = reinterpret_cast<const uint8_t**>(smem + a.off_tab);   // the pool's code pointers
+  for (int k = tid; k < a.K; k += kFuThreads) ctab[k] = a.copies[k];
 
   // ---- work assignment -------------------------------------------------------------------
   const int t0 = (int)((int64_t)cta * a.ntiles / G), t1 = (int)((int64_t)(cta + 1) * a.ntiles / G);
@@ -125,63 +131,83 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
   const int col_lo = 16 * t0;
   const int ncol = max(0, min(16 * t1, a.N) - col_lo);
   const int KS = a.Rpad / KSTEP;                                  // k-steps per tile
-  const long long total_blocks = (long long)a.n_iter * T;
+  const int total_blocks = a.n_iter * T;                          // <= 2^31 (eligibility)
   const int g8 = lane >> 2, t = lane & 3;
 
-  // ---- ring producer (thread 0): block b = (n - 1) T + j is tile j of iteration n's adjoint
-  // copy, in slot b % nslot; a slot is refilled once all warps released its previous block
-  long long nb = 0;                                               // next block to request
-  auto request = [&](bool blocking, long long limit) {
-    while (nb < limit) {
-      const int slot = (int)(nb % a.nslot);
-      const long long use = nb / a.nslot;
-      if (use > 0) {
-        const uint32_t par = (uint32_t)((use - 1) & 1);
-        if (blocking) mbar_wait(empty_u + 8 * slot, par);
-        else if (!mbar_test(empty_u + 8 * slot, par)) return;
-      }
-      const int n = (int)(nb / T) + 1, j = (int)(nb % T);
-      const uint8_t* src = a.copies[(2 * n - 2) % a.K] + (int64_t)(t0 + j) * a.tile_bytes;
-      mbar_expect_tx(full_u + 8 * slot, (uint32_t)a.tile_bytes);
-      bulk_g2s(ring_u + (uint32_t)slot * a.tile_bytes, src, (uint32_t)a.tile_bytes, full_u + 8 * slot);
+  // ---- per-warp rings: warp w owns the tiles j = w, w + 8, ... of this CTA and streams them
+  // itself through its own mslot slots (lane 0 issues the bulk copies, full mbarriers only):
+  // its q-th block is sub-block h of its k-th tile of iteration n, q = ((n-1) Tw + k) nsub + h.
+  // A slot is refilled by the warp as soon as it has consumed it, so the NEXT iteration's
+  // tiles stream in while the CTA is in the barriers, the select and the forward.
+  const int Tw = T > warp ? (T - warp + kFuWarps - 1) / kFuWarps : 0;   // tiles of this warp
+  const int Bw = Tw * a.nsub;                                     // its blocks per iteration
+  const int total_w = a.n_iter * Bw;
+  const uint32_t wfull = full_u + 8 * (warp * a.mslot);
+  const uint32_t wring = ring_u + (uint32_t)(warp * a.mslot) * a.block_bytes;
+  int nb = 0;                                                     // lane 0: next block to request
+  int rq_slot = 0, rq_k = 0, rq_h = 0, rq_n = 1;
+  const uint8_t* rq_src = nullptr;                                // the copy of iteration rq_n
+  auto request = [&](int limit) {                                 // lane 0 only
+    while (nb < limit && nb < total_w) {
+      if (rq_k == 0 && rq_h == 0) rq_src = ctab[(2 * rq_n - 2) % a.K];
+      const uint8_t* src = rq_src + (int64_t)(t0 + warp + kFuWarps * rq_k) * a.tile_bytes +
+                           (int64_t)rq_h * a.block_bytes;
+      mbar_expect_tx(wfull + 8 * rq_slot, (uint32_t)a.block_bytes);
+      bulk_g2s(wring + (uint32_t)rq_slot * a.block_bytes, src, (uint32_t)a.block_bytes, wfull + 8 * rq_slot);
       ++nb;
+      if (++rq_h == a.nsub) {
+        rq_h = 0;
+        if (++rq_k == Tw) {
+          rq_k = 0;
+          ++rq_n;
+        }
+      }
+      if (++rq_slot == a.mslot) rq_slot = 0;
     }
   };
   if (tid == 0) {
-    for (int j = 0; j < a.nslot; ++j) {
-      mbar_init(full_u + 8 * j, 1);
-      mbar_init(empty_u + 8 * j, kFuWarps);
-    }
+    for (int j = 0; j < kFuWarps * a.mslot; ++j) mbar_init(full_u + 8 * j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_nnz = 0;                                                    // x^[1] = 0 (reading c8)
   }
   __syncthreads();
-  if (tid == 0 && T > 0) request(true, total_blocks < a.nslot ? total_blocks : a.nslot);
+  if (lane == 0 && !(a.probe & 8)) request(a.mslot);
 
   unsigned int bar_target = 0;
   auto grid_sync = [&]() {
     __syncthreads();
     if (tid == 0) {
       bar_target += (unsigned int)G;
-      __threadfence();
-      atomicAdd(a.bar, 1u);
+      // release: the CTA's writes (ordered before by bar.sync) become visible with the arrival
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
       while (ld_acquire_u32(a.bar) < bar_target) {
       }
     }
     __syncthreads();
   };
 
-  const uint32_t limb_n = (uint32_t)__cvta_generic_to_shared(limbs + (g8 < 3 ? g8 : 0) * a.Rpad);
+  const uint32_t limb_n = (uint32_t)__cvta_generic_to_shared(limbs + (g8 < 3 ? g8 : 0) * a.limb_stride);
   const bool bload = g8 < 3;
   uint32_t bw[4 * P];
 #pragma unroll
   for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
   const unsigned int lt = (1u << lane) - 1u;
-  long long consumed = 0;                                         // blocks consumed (all warps)
+  int consumed = 0;                                               // blocks this warp consumed
+  int c_slot = 0;                                                 // consumer cursor: slot, use parity
+  uint32_t c_par = 0;
   int n_done = 0;
 
+  auto stamp = [&](int n, int k) {      // profiling timeline (IHT_FUSED_TL)
+    if (a.tl && tid == 0) {
+      long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      if (a.tl_cta >= 0 && cta == a.tl_cta && n <= 64) a.tl[(n - 1) * 16 + k] = tt;
+      if (a.tl_cta < 0 && n == 3) a.tl[cta * 16 + k] = tt;     // every CTA, iteration 3
+    }
+  };
   for (int n = 1; n <= a.n_iter; ++n) {
     const int par = n & 1;
+    stamp(n, 0);
     // ================================================================ F: forward
     {
       const int w0 = cta * a.wpc;
@@ -192,9 +218,12 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         const int wi = tid % wpc, cl = tid / wpc;
         const int64_t word = (int64_t)w0 + wi;
         const bool live = word < a.words_total;
-        const uint8_t* cf = a.copies[(2 * n - 1) % a.K];            // Phi-hat_{2n}, forward
+        const uint8_t* cf = ctab[(2 * n - 1) % a.K];                // Phi-hat_{2n}, forward
         const int64_t kofs = (word >> 4) * 1024 + (word & 15) * 4;  // tiled byte 4 word, sans column
         const int nnz = s_nnz;
+        // y-hat of this CTA's output rows, requested before the code loads
+        const float ypre = tid < wpc * CPW && (int64_t)w0 * CPW + tid < (int64_t)a.words_total * CPW
+                               ? __ldg(a.yhat + (int64_t)w0 * CPW + tid) : 0.0f;
         float acc[CPW];
 #pragma unroll
         for (int i = 0; i < CPW; ++i) acc[i] = 0.0f;
@@ -227,9 +256,10 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         // column lanes of the warp (xor shuffles), then the 8 warps in order
         const float xl = __fmul_rn((float)(a.L - 1), xs);
 #pragma unroll
-        for (int i = 0; i < CPW; ++i) {
-          acc[i] = __fsub_rn(__fmul_rn(2.0f, acc[i]), xl);
-          for (int o = wpc; o < 32; o <<= 1) acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], o));
+        for (int i = 0; i < CPW; ++i) acc[i] = __fsub_rn(__fmul_rn(2.0f, acc[i]), xl);
+        for (int o = wpc; o < 32; o <<= 1) {                      // CPW independent shuffles per level
+#pragma unroll
+          for (int i = 0; i < CPW; ++i) acc[i] = __fadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], o));
         }
         if (lane < wpc) {
 #pragma unroll
@@ -244,7 +274,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
             float sum = part[0][ww][i];
 #pragma unroll
             for (int w2 = 1; w2 < kFuWarps; ++w2) sum = __fadd_rn(sum, part[w2][ww][i]);
-            const float rv = (int)(m % a.rpad) < a.rows ? __fsub_rn(__ldg(a.yhat + m), __fmul_rn(a.sigma, sum)) : 0.0f;
+            const float rv = (int)(m % a.rpad) < a.rows ? __fsub_rn(ypre, __fmul_rn(a.sigma, sum)) : 0.0f;
             a.r[m] = rv;
             mymax = __float_as_uint(rv) & 0x7FFFFFFFu;               // NaN / inf caught by bit pattern
           }
@@ -255,13 +285,34 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         if (tid == 0 && s_cmax) atomicMax(&a.cmax[par * a.nchunks + (w0 * CPW) / kFuKC], s_cmax);
       }
     }
+    stamp(n, 1);
     grid_sync();                                                  // ---- barrier 1: r complete
+    stamp(n, 2);
     // ================================================================ limbs of r
     if (T > 0) {
+      // r -> three balanced signed 8-bit limbs, permuted per lane chunk (iht_adjoint.cu layout).
+      // A thread converts whole groups of CPW consecutive rows (the rows of one 32-bit code
+      // word = P limb items): its loads are P contiguous float4 (coalesced; r is read once per
+      // CTA from L2), all requested together with the chunk maxima before anything waits
+      const int ngroups = a.Rpad / CPW;
+      const int rounds = (ngroups + kFuThreads - 1) / kFuThreads;
+      constexpr int kMaxRounds = 16384 / CPW / kFuThreads;       // Rpad <= 16384 rows
+      float4 rv[kMaxRounds][P];
+#pragma unroll
+      for (int rd = 0; rd < kMaxRounds; ++rd) {
+        const int gw = tid + rd * kFuThreads;
+#pragma unroll
+        for (int e = 0; e < P; ++e)
+          rv[rd][e] = (rd < rounds && gw < ngroups) ? __ldcg(reinterpret_cast<const float4*>(a.r + gw * CPW) + e)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       if (tid == 0) s_nonfinite = 0;
+      unsigned int mb = tid < a.nchunks ? __ldcg(&a.cmax[par * a.nchunks + tid]) : 0u;
+      for (int q = tid; q < T * a.nchunks * 48; q += kFuThreads) Vs[q] = 0;
+      for (int q = tid; q < 2048; q += kFuThreads) hist_s[q] = 0;  // the A-phase histogram (off the critical path)
       __syncthreads();
-      for (int c = tid; c < a.nchunks; c += kFuThreads) {
-        unsigned int mb = __ldcg(&a.cmax[par * a.nchunks + c]);
+      if (tid < a.nchunks) {
+        const int c = tid;
         if (mb >= 0x7F800000u) {
           s_nonfinite = 1;
           mb = 0;
@@ -272,33 +323,23 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         Fc[c] = (m > 0.0f) ? min(22 - e, 126) : 0;                // |r| 2^F < 2^22
         Sl[3 * c] = Sl[3 * c + 1] = Sl[3 * c + 2] = 0;
       }
-      for (int q = tid; q < T * a.nchunks * 16; q += kFuThreads) Vs[q] = 0;
       __syncthreads();
-      // r -> three balanced signed 8-bit limbs, permuted per lane chunk (iht_adjoint.cu layout)
-      constexpr int kIt = 4;
-      const int items = a.Rpad / RPC * (4 * P);
-      for (int it0 = tid; it0 < items; it0 += kIt * kFuThreads) {
-        float rvs[kIt][4];
 #pragma unroll
-        for (int q = 0; q < kIt; ++q) {
-          const int it = it0 + q * kFuThreads;
-          const int ch = it / (4 * P), rho = it % (4 * P);
-          const int base = ch * RPC + (rho / P) * (32 / B) + (rho % P);
+      for (int rd = 0; rd < kMaxRounds; ++rd) {
+        if (rd >= rounds) break;
+        const int gw = tid + rd * kFuThreads;
+        const bool ok = gw < ngroups;
+        const int c = ok ? (gw * CPW) / kFuKC : 0;
+        const float scale = ldexpf(1.0f, Fc[c]);
+        const int ch = gw >> 2, h = gw & 3;                       // lane chunk, word within it
+        const float* rr = reinterpret_cast<const float*>(&rv[rd][0]);   // CPW rows of this group
+        int s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) rvs[q][i] = it < items ? __ldcg(a.r + base + P * i) : 0.0f;
-        }
-#pragma unroll
-        for (int q = 0; q < kIt; ++q) {
-          const int it = it0 + q * kFuThreads;
-          if (it >= items) break;
-          const int ch = it / (4 * P), rho = it % (4 * P);
-          const int c = (ch * RPC) / kFuKC;
-          const float scale = ldexpf(1.0f, Fc[c]);
+        for (int e = 0; e < P; ++e) {                             // item rho = h P + e: rows e + P i
           uint32_t l0w = 0, l1w = 0, l2w = 0;
-          int s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int ri = __float2int_rn(rvs[q][i] * scale);
+            const int ri = __float2int_rn(rr[e + P * i] * scale);
             const int l0 = ((ri + 128) & 255) - 128;
             const int tt = (ri - l0) >> 8;
             const int l1 = ((tt + 128) & 255) - 128;
@@ -308,28 +349,32 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
             l1w |= (uint32_t)(l1 & 255) << (8 * i);
             l2w |= (uint32_t)(l2 & 255) << (8 * i);
           }
-          const int off = ch * (16 * P) + (4 * (rho % P) + rho / P) * 4;
-          *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
-          *reinterpret_cast<uint32_t*>(limbs + a.Rpad + off) = l1w;
-          *reinterpret_cast<uint32_t*>(limbs + 2 * a.Rpad + off) = l2w;
-          s0 = __reduce_add_sync(0xffffffffu, s0);
-          s1 = __reduce_add_sync(0xffffffffu, s1);
-          s2 = __reduce_add_sync(0xffffffffu, s2);
-          if (lane == 0) {
-            atomicAdd(&Sl[3 * c], s0);
-            atomicAdd(&Sl[3 * c + 1], s1);
-            atomicAdd(&Sl[3 * c + 2], s2);
+          if (ok) {
+            const int off = ch * (16 * P) + (4 * e + h) * 4;
+            *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
+            *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
+            *reinterpret_cast<uint32_t*>(limbs + 2 * a.limb_stride + off) = l2w;
           }
+        }
+        // the 32 groups of a warp lie in one chunk (32 CPW = 512 / B rows, aligned)
+        s0 = __reduce_add_sync(0xffffffffu, s0);
+        s1 = __reduce_add_sync(0xffffffffu, s1);
+        s2 = __reduce_add_sync(0xffffffffu, s2);
+        if (lane == 0) {
+          atomicAdd(&Sl[3 * c], s0);
+          atomicAdd(&Sl[3 * c + 1], s1);
+          atomicAdd(&Sl[3 * c + 2], s2);
         }
       }
       __syncthreads();
+      stamp(n, 3);
       // ============================================================== A: adjoint
       int cur_seg = -1;
       int acc[P][4];
 #pragma unroll
       for (int j = 0; j < P; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
       auto flush = [&]() {
-        if (cur_seg < 0) return;
+        if (cur_seg < 0 || (a.probe & 4)) return;
         int v00 = 0, v01 = 0, v10 = 0, v11 = 0;
 #pragma unroll
         for (int j = 0; j < P; ++j) {
@@ -341,63 +386,78 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         }
         const int l2r0 = __shfl_down_sync(0xffffffffu, v00, 1);
         const int l2r1 = __shfl_down_sync(0xffffffffu, v10, 1);
-        if (t == 0) {                 // exact int64 sums of warps sharing the (tile, chunk)
-          const long long V0 = (long long)v00 + 256ll * v01 + 65536ll * l2r0;
-          const long long V1 = (long long)v10 + 256ll * v11 + 65536ll * l2r1;
-          atomicAdd(reinterpret_cast<unsigned long long*>(&Vs[cur_seg * 16 + g8]), (unsigned long long)V0);
-          atomicAdd(reinterpret_cast<unsigned long long*>(&Vs[cur_seg * 16 + g8 + 8]), (unsigned long long)V1);
+        if (t == 0) {                 // exact per-limb int32 sums of the warps sharing (tile, chunk)
+          int* v = Vs + (cur_seg * 16 + g8) * 3;
+          atomicAdd(v, v00);
+          atomicAdd(v + 1, v01);
+          atomicAdd(v + 2, l2r0);
+          atomicAdd(v + 24, v10);
+          atomicAdd(v + 25, v11);
+          atomicAdd(v + 26, l2r1);
         }
       };
-      for (int j = 0; j < T; ++j) {
-        const long long b = (long long)(n - 1) * T + j;
-        const int slot = (int)(b % a.nslot);
-        if (tid == 0) request(true, b + 1);                       // block b is in flight
-        mbar_wait(full_u + 8 * slot, (uint32_t)((b / a.nslot) & 1));
-        const int r0 = (j * KS) % kFuWarps;
-        for (int ks = (warp - r0 + kFuWarps) % kFuWarps; ks < KS; ks += kFuWarps) {
-          const int seg = j * a.nchunks + (ks * KSTEP) / kFuKC;
-          if (seg != cur_seg) {
-            flush();
-            cur_seg = seg;
-          }
-          const uint32_t src = ring_u + (uint32_t)slot * a.tile_bytes + ks * 1024 + g8 * 64 + t * 16;
-          const uint4 s0 = lds128(src), s1 = lds128(src + 512);
-          if (bload) {
-            const uint32_t bp = limb_n + (uint32_t)(ks * 4 + t) * (16 * P);
-#pragma unroll
-            for (int q = 0; q < P; ++q) {
-              const uint4 v = lds128(bp + 16 * q);
-              bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
+      const int KSB = KS / a.nsub;                                // k-steps per block
+      // probe 8: no cross-iteration prefetch (each warp streams its tiles during its own A)
+      const int rq_cap = (a.probe & 8) ? n * Bw : total_w;
+      if (lane == 0) request(min(consumed + a.mslot, rq_cap));
+      for (int k = 0; k < Tw; ++k) {
+        const int j = warp + kFuWarps * k;                        // tile (CTA-local)
+        for (int h = 0; h < a.nsub; ++h) {
+          if (k == 0 && h == 0) stamp(n, 10);
+          mbar_wait(wfull + 8 * c_slot, c_par);
+          if (k == 0 && h == 0) stamp(n, 11);
+          const uint32_t sbase = wring + (uint32_t)c_slot * a.block_bytes;
+          for (int kk = 0; kk < KSB && !(a.probe & 1); ++kk) {
+            const int ks = h * KSB + kk;
+            const int seg = j * a.nchunks + (ks * KSTEP) / kFuKC;
+            if (seg != cur_seg) {
+              flush();
+              cur_seg = seg;
             }
-          }
-          uint32_t af[NMMA][4];
+            const uint32_t src = sbase + kk * 1024 + g8 * 64 + t * 16;
+            const uint4 s0 = lds128(src), s1 = lds128(src + 512);
+            if (bload) {
+              const uint32_t bp = limb_n + (uint32_t)(ks * 4 + t) * (16 * P);
 #pragma unroll
-          for (int jj = 0; jj < P; ++jj)
-#pragma unroll
-            for (int m = 0; m < 2; ++m) {
-              af[2 * jj + m][0] = frag_reg<B>(s0, 2 * m, jj);
-              af[2 * jj + m][1] = frag_reg<B>(s1, 2 * m, jj);
-              af[2 * jj + m][2] = frag_reg<B>(s0, 2 * m + 1, jj);
-              af[2 * jj + m][3] = frag_reg<B>(s1, 2 * m + 1, jj);
+              for (int q = 0; q < P; ++q) {
+                const uint4 v = lds128(bp + 16 * q);
+                bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
+              }
             }
+            uint32_t af[NMMA][4];
 #pragma unroll
-          for (int u = 0; u < NMMA; ++u) mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
+            for (int jj = 0; jj < P; ++jj)
+#pragma unroll
+              for (int m = 0; m < 2; ++m) {
+                af[2 * jj + m][0] = frag_reg<B>(s0, 2 * m, jj);
+                af[2 * jj + m][1] = frag_reg<B>(s1, 2 * m, jj);
+                af[2 * jj + m][2] = frag_reg<B>(s0, 2 * m + 1, jj);
+                af[2 * jj + m][3] = frag_reg<B>(s1, 2 * m + 1, jj);
+              }
+#pragma unroll
+            for (int u = 0; u < NMMA; ++u) mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
+          }
+          __syncwarp();                                           // every lane has read the slot
+          ++consumed;
+          if (lane == 0 && !(a.probe & 2)) request(min(consumed + a.mslot, rq_cap));   // refill (maybe next iteration)
+          if (++c_slot == a.mslot) {
+            c_slot = 0;
+            c_par ^= 1u;
+          }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty_u + 8 * slot);          // this warp is done with block b
-        if (tid == 0) request(false, total_blocks);               // refill whatever is free
       }
       flush();
-      consumed = (long long)n * T;
-      __syncthreads();                                            // every block of iteration n consumed
-      if (tid == 0) request(true, consumed + a.nslot < total_blocks ? consumed + a.nslot : total_blocks);
+      stamp(n, 4);
+      __syncthreads();                                            // every tile of iteration n consumed
+      if (lane == 0 && (a.probe & 2)) request(consumed + a.mslot);
       // g = sigma sum_c 2^{-F_c} (2 V_c - (L-1) S_c) (iht_adjoint.cu's combination), a = mu g
       for (int q = tid; q < ncol; q += kFuThreads) {
         const int jl = q >> 4, cc = q & 15;
         float accf = 0.0f;
         for (int c = 0; c < a.nchunks; ++c) {
           const long long S = (long long)Sl[3 * c] + 256ll * Sl[3 * c + 1] + 65536ll * Sl[3 * c + 2];
-          const long long V = Vs[(jl * a.nchunks + c) * 16 + cc];
+          const int* v = Vs + ((jl * a.nchunks + c) * 16 + cc) * 3;
+          const long long V = (long long)v[0] + 256ll * v[1] + 65536ll * v[2];
           accf += (float)((double)(2 * V - (long long)(a.L - 1) * S) * ldexp(1.0, -Fc[c]));
         }
         const float gv = s_nonfinite ? __int_as_float(0x7FC00000) : a.sigma * accf;
@@ -411,16 +471,25 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         if (c >= 0 && c < ncol) as[c] = __fadd_rn(xv_s[j], as[c]);
       }
       __syncthreads();
+      // the CTA's histogram in shared memory first (the union region: V sums are consumed),
+      // then one global atomic per nonzero bin -- the keys crowd a few dozen 1/8-octave bins,
+      // and per-element global atomics on them serialised at L2 (and delayed the barrier)
       int nan = 0;
       for (int q = tid; q < ncol; q += kFuThreads) {
         const unsigned int key = __float_as_uint(as[q]) & 0x7FFFFFFFu;
         nan |= key > 0x7F800000u;
-        atomicAdd(&a.hist[par * 2048 + (key >> 20)], 1);
+        atomicAdd(&hist_s[key >> 20], 1);
       }
       nan = __syncthreads_or(nan);
+      for (int q = tid; q < 2048; q += kFuThreads) {
+        const int v = hist_s[q];
+        if (v) atomicAdd(&a.hist[par * 2048 + q], v);
+      }
       if (tid == 0 && nan) atomicOr(&a.flags[par], 1);
     }
+    stamp(n, 5);
     grid_sync();                                                  // ---- barrier 2: histogram complete
+    stamp(n, 6);
     // ================================================================ S1: candidates
     if (cta == 0) {                                               // parity par^1 is idle now
       for (int q = tid; q < 2048; q += kFuThreads) a.hist[(par ^ 1) * 2048 + q] = 0;
@@ -428,7 +497,13 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       if (tid == 0) a.flags[par ^ 1] = 0;
     }
     if (tid == 0) s_flag = __ldcg(&a.flags[par]);
-    for (int q = tid; q < 2048; q += kFuThreads) hist_s[q] = __ldcg(&a.hist[par * 2048 + q]);
+    {
+      int hv[2048 / kFuThreads];                                  // every load in flight at once
+#pragma unroll
+      for (int u = 0; u < 2048 / kFuThreads; ++u) hv[u] = __ldcg(&a.hist[par * 2048 + tid + u * kFuThreads]);
+#pragma unroll
+      for (int u = 0; u < 2048 / kFuThreads; ++u) hist_s[tid + u * kFuThreads] = hv[u];
+    }
     __syncthreads();
     const bool all = a.s >= a.N;
     unsigned int d1 = 0;
@@ -464,7 +539,9 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       if (tid == 0) a.cand_cnt[cta] = base;
     }
     (void)above;
+    stamp(n, 7);
     grid_sync();                                                  // ---- barrier 3: candidates complete
+    stamp(n, 8);
     // ================================================================ S2: exact top-s
     const int slot_out = a.trace ? n : (n & 1);
     if (s_flag) {                                                 // non-finite a: domain error
@@ -493,16 +570,119 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
     if (a.s == 0) {                                               // H_0 keeps nothing
       if (tid == 0) s_nnz = 0;
     } else if (C <= kFuCandCap) {
-      for (int c = warp; c < G; c += kFuWarps) {
-        const int o = cnt_s[c], k = cnt_s[c + 1] - o;
-        for (int i = lane; i < k; i += 32) {
-          ci_s[o + i] = __ldcg(&a.cand_idx[(int64_t)c * a.cap_c + i]);
-          cv_s[o + i] = __ldcg(&a.cand_val[(int64_t)c * a.cap_c + i]);
+      // one candidate per thread and round, its CTA found by binary search over the offsets:
+      // every L2 load of a round is in flight at once
+      for (int i0 = 0; i0 < C; i0 += 4 * kFuThreads) {
+        int32_t ci[4];
+        float cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kFuThreads + tid;
+          if (i < C) {
+            int lo = 0, hi = G;                                   // cnt_s[lo] <= i < cnt_s[hi]
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (cnt_s[mid] <= i) lo = mid; else hi = mid;
+            }
+            const int64_t src = (int64_t)lo * a.cap_c + (i - cnt_s[lo]);
+            ci[u] = __ldcg(&a.cand_idx[src]);
+            cv[u] = __ldcg(&a.cand_val[src]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kFuThreads + tid;
+          if (i < C) {
+            ci_s[i] = ci[u];
+            cv_s[i] = cv[u];
+          }
         }
       }
       __syncthreads();
-      select_ordered<kFuThreads>(C, a.s, [&](int i) { return cv_s[i]; }, [&](int i) { return ci_s[i]; }, xi_s, xv_s,
-                                 &s_nnz, 0, hsel, scratch, wgt, weq, wtake, wbase, sh);
+      // ordered block compaction of the staged candidates whose flag is set -> (dst_i, dst_v)
+      auto compact = [&](auto flag, int32_t* di, float* dv) {
+        int base = 0;
+        for (int q0 = 0; q0 < C; q0 += kFuThreads) {
+          const int q = q0 + tid;
+          const bool f = q < C && flag(q);
+          const unsigned int bal = __ballot_sync(0xffffffffu, f);
+          if (lane == 0) wgt[warp] = __popc(bal);
+          __syncthreads();
+          int off = base, tot = 0;
+          for (int w = 0; w < kFuWarps; ++w) {
+            if (w < warp) off += wgt[w];
+            tot += wgt[w];
+          }
+          if (f) {
+            di[off + __popc(bal & lt)] = ci_s[q];
+            dv[off + __popc(bal & lt)] = cv_s[q];
+          }
+          base += tot;
+          __syncthreads();
+        }
+        return base;
+      };
+      if (all || C <= a.s) {
+        // every candidate is kept: the nonzero keys number at most s (or s >= N)
+        const int k = compact([&](int) { return true; }, xi_s, xv_s);
+        if (tid == 0) s_nnz = k;
+      } else {
+        // bins above d1 hold `above` < s keys, all kept; the remaining need = s - above come
+        // from bin d1: rank each bin-d1 key among them (greater key, or equal key at a lower
+        // index -- the list is in index order) and keep ranks < need (ties to the lowest index)
+        const int need = a.s - above;
+        unsigned int* Dk = reinterpret_cast<unsigned int*>(hsel);   // bin-d1 keys, index order
+        int* Dp = hsel + 2048;                                       // their list positions
+        uint8_t* keep = reinterpret_cast<uint8_t*>(hsel + 4096);
+        int C1 = 0;
+        for (int q0 = 0; q0 < C; q0 += kFuThreads) {
+          const int q = q0 + tid;
+          const unsigned int key = q < C ? (__float_as_uint(cv_s[q]) & 0x7FFFFFFFu) : 0u;
+          const bool f = q < C && (key >> 20) == d1;
+          if (q < C) keep[q] = (key >> 20) > d1;
+          const unsigned int bal = __ballot_sync(0xffffffffu, f);
+          if (lane == 0) wgt[warp] = __popc(bal);
+          __syncthreads();
+          int off = C1, tot = 0;
+          for (int w = 0; w < kFuWarps; ++w) {
+            if (w < warp) off += wgt[w];
+            tot += wgt[w];
+          }
+          if (f && off + __popc(bal & lt) < 2048) {
+            Dk[off + __popc(bal & lt)] = key;
+            Dp[off + __popc(bal & lt)] = q;
+          }
+          C1 += tot;
+          __syncthreads();
+        }
+        if (C1 <= 1024) {
+          for (int e0 = 0; e0 < C1; e0 += kFuThreads) {
+            const int e = e0 + tid;
+            const bool have = e < C1;
+            const unsigned int ke = have ? Dk[e] : 0u;
+            int rk = 0;
+            if (__any_sync(0xffffffffu, have)) {
+              int f = 0;
+              for (; f + 4 <= C1; f += 4) {                       // broadcast reads, 4 in flight
+                const unsigned int k0 = Dk[f], k1 = Dk[f + 1], k2 = Dk[f + 2], k3 = Dk[f + 3];
+                rk += (k0 > ke || (k0 == ke && f < e)) + (k1 > ke || (k1 == ke && f + 1 < e)) +
+                      (k2 > ke || (k2 == ke && f + 2 < e)) + (k3 > ke || (k3 == ke && f + 3 < e));
+              }
+              for (; f < C1; ++f) {
+                const unsigned int kf = Dk[f];
+                rk += kf > ke || (kf == ke && f < e);
+              }
+            }
+            if (have && rk < need) keep[Dp[e]] = 1;
+          }
+          __syncthreads();
+          const int k = compact([&](int q) { return keep[q] != 0; }, xi_s, xv_s);
+          if (tid == 0) s_nnz = k;
+        } else {                                                  // a crowded bin: radix passes
+          select_ordered<kFuThreads>(C, a.s, [&](int i) { return cv_s[i]; }, [&](int i) { return ci_s[i]; }, xi_s,
+                                     xv_s, &s_nnz, 0, hsel, scratch, wgt, weq, wtake, wbase, sh);
+        }
+      }
     } else {
       // many candidates (massive ties): select over the global lists, element i found by
       // binary search over the CTA offsets
@@ -519,6 +699,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
                                  scratch, wgt, weq, wtake, wbase, sh);
     }
     __syncthreads();
+    stamp(n, 9);
     if (cta == 0) {                                               // the iterate x^[n+1]
       const int k = s_nnz;
       for (int j = tid; j < k; j += kFuThreads) {
@@ -531,8 +712,14 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
   }
   (void)n_done;
   // drain: bulk copies still in flight (prefetch past an aborted run) must land before exit
-  if (tid == 0) {
-    for (long long b = consumed; b < nb; ++b) mbar_wait(full_u + 8 * (int)(b % a.nslot), (uint32_t)((b / a.nslot) & 1));
+  if (lane == 0) {
+    for (int b = consumed; b < nb; ++b) {
+      mbar_wait(wfull + 8 * c_slot, c_par);
+      if (++c_slot == a.mslot) {
+        c_slot = 0;
+        c_par ^= 1u;
+      }
+    }
   }
   __syncthreads();
 }
@@ -546,6 +733,7 @@ using namespace iht;
 
 struct iht_fused_state {
   FusedArgs args{};
+  long long* tl = nullptr;
   int G = 0, bits = 0;
   size_t smem = 0;
   void* block = nullptr;               // copies table | bar | hist | cmax | flags | candidates
@@ -559,7 +747,8 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   *out = nullptr;
   const iht_qmat& q = pool[0];
   if (q.bits != 2 && q.bits != 4 && q.bits != 8) return IHT_EUNSUPPORTED;
-  if (q.cols > 0x7FFFFFFF || q.rows > 0x7FFFFFFF || s < 0) return IHT_EUNSUPPORTED;
+  if (q.cols > 0x7FFFFFFF || q.rows > 0x7FFFFFFF || s < 0 || K > 2048) return IHT_EUNSUPPORTED;
+  if ((int64_t)n_iter * ((q.cols + 15) / 16) > 0x7FFFFFFF) return IHT_EUNSUPPORTED;
   int dev = 0, G = 0, coop = 0, optin = 0;
   IHT_CUDA_CHECK(cudaGetDevice(&dev));
   IHT_CUDA_CHECK(cudaDeviceGetAttribute(&G, cudaDevAttrMultiProcessorCount, dev));
@@ -581,14 +770,15 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   const int s_cap = s > 0 ? s : 1;
   // shared memory: ring | bars | limbs | Fc, Sl | a | x | union(V sums, histogram, candidates)
   size_t o = 0;
-  const size_t u_bytes = std::max({(size_t)tmax * nchunks * 16 * 8, (size_t)2048 * 4,
-                                   (size_t)kFuCandCap * 8 + (size_t)(((G + 4) & ~3) + 2048) * 4});
-  auto layout = [&](int nslot, FusedArgs* A) {
-    o = (size_t)nslot * tile_bytes;
+  const size_t u_bytes = std::max({(size_t)tmax * nchunks * 16 * 12, (size_t)2048 * 4,
+                                   (size_t)kFuCandCap * 8 + (size_t)(((G + 4) & ~3) + 2048 + 2048) * 4 +
+                                       (size_t)kFuCandCap});
+  auto layout = [&](int nring, int block_bytes, FusedArgs* A) {   // nring = 8 warps x mslot slots
+    o = (size_t)nring * block_bytes;
     const size_t bars = o;
-    o = al16(o + 16 * (size_t)nslot);
+    o = al16(o + 8 * (size_t)nring);
     const size_t limbs = o;
-    o = al16(o + 3 * (size_t)Rpad);
+    o = al16(o + 3 * (size_t)(Rpad + 64));
     const size_t fc = o;
     o = al16(o + 16 * (size_t)nchunks);
     const size_t as = o;
@@ -596,7 +786,11 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
     const size_t xo = o;
     o = al16(o + 8 * (size_t)s_cap);
     const size_t uo = o;
-    o += u_bytes;
+    o = al16(o + u_bytes);
+    const size_t tb = o;
+    o = al16(o + 8 * (size_t)K);
+    const size_t ho = o;
+    o += 2048 * 4;
     if (A) {
       A->off_bars = (int)bars;
       A->off_limbs = (int)limbs;
@@ -604,17 +798,33 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
       A->off_as = (int)as;
       A->off_x = (int)xo;
       A->off_u = (int)uo;
+      A->off_tab = (int)tb;
+      A->off_h = (int)ho;
     }
     return o;
   };
   const size_t limit = (size_t)optin - 8192;          // static shared memory and margin
-  const size_t rest = layout(0, nullptr);
-  if (rest + tile_bytes > limit) return IHT_EUNSUPPORTED;
-  int nslot = (int)((limit - rest) / (tile_bytes + 16));
-  nslot = std::max(1, std::min(nslot, tmax));
+  const size_t rest = layout(0, 0, nullptr);
+  // ring: each warp owns mslot >= 2 blocks (double buffering); a block is a whole number of
+  // 1 KiB k-steps, the largest divisor nsub of the tile's KS k-steps that fits
+  const int KSTEP = 512 / B, KS = Rpad / KSTEP;
+  const int tw_max = (tmax + kFuWarps - 1) / kFuWarps;          // tiles per warp
+  int nsub = 0, mslot = 0;
+  for (int d = 1; d <= KS; ++d) {
+    if (KS % d) continue;
+    const size_t blk = (size_t)tile_bytes / d;
+    if (rest + (size_t)kFuWarps * 2 * (blk + 8) <= limit) {
+      nsub = d;
+      mslot = (int)((limit - rest) / ((size_t)kFuWarps * (blk + 8)));
+      mslot = std::max(2, std::min(mslot, std::max(2, tw_max * d)));
+      break;
+    }
+  }
+  if (nsub == 0) return IHT_EUNSUPPORTED;
+  const int block_bytes = tile_bytes / nsub;
   iht_fused_state* S = new iht_fused_state();
   FusedArgs& A = S->args;
-  S->smem = layout(nslot, &A);
+  S->smem = layout(kFuWarps * mslot, block_bytes, &A);
   S->G = G;
   S->bits = B;
   // device workspace
@@ -657,12 +867,15 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   A.s = s;
   A.n_iter = n_iter;
   A.ntiles = ntiles;
-  A.nslot = nslot;
+  A.nsub = nsub;
+  A.block_bytes = block_bytes;
+  A.mslot = mslot;
   A.tile_bytes = tile_bytes;
   A.nchunks = nchunks;
   A.wpc = wpc;
   A.words_total = words_total;
   A.cap_c = cap_c;
+  A.limb_stride = Rpad + 64;
   A.s_cap = s_cap;
   A.yhat = yhat;
   A.r = r;
@@ -671,6 +884,16 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   A.xs_val = xs_val;
   A.xs_nnz = xs_nnz;
   A.trace = trace;
+  A.probe = getenv("IHT_FUSED_PROBE") ? atoi(getenv("IHT_FUSED_PROBE")) : 0;   // profiling only
+  if (getenv("IHT_FUSED_TL")) {        // profiling only: per-phase globaltimer stamps of one CTA
+    A.tl_cta = atoi(getenv("IHT_FUSED_TL"));
+    if (A.tl_cta >= G) A.tl_cta = 0;
+    const size_t nt = (size_t)std::max(64, G) * 16;
+    if (cudaMalloc(&S->tl, nt * sizeof(long long)) == cudaSuccess) {
+      cudaMemset(S->tl, 0, nt * sizeof(long long));
+      A.tl = S->tl;
+    }
+  }
   auto kern = B == 2 ? fused_iht_kernel<2> : B == 4 ? fused_iht_kernel<4> : fused_iht_kernel<8>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem);
   int nblk = 0;
@@ -705,6 +928,51 @@ int iht_fused_enqueue(iht_fused_state* S, void* stream) {
 
 void iht_fused_destroy(iht_fused_state* S) {
   if (S == nullptr) return;
+  if (S->tl && S->args.tl_cta < 0) {   // profiling: per-CTA phase durations of iteration 3
+    std::vector<long long> h((size_t)S->G * 16);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), S->tl, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    const char* names[9] = {"F", "B1", "limbs", "A", "hist", "B2", "S1", "B3", "S2"};
+    fprintf(stderr, "fused per-CTA (iteration 3, ns): ");
+    for (int k = 0; k < 9; ++k) {
+      std::vector<std::pair<long long, int>> d;
+      for (int c = 0; c < S->G; ++c) d.push_back({h[c * 16 + k + 1] - h[c * 16 + k], c});
+      std::sort(d.begin(), d.end());
+      fprintf(stderr, " %s min %lld med %lld max %lld (cta %d)", names[k], d[0].first, d[d.size() / 2].first,
+              d.back().first, d.back().second);
+    }
+    long long t0 = h[1 * 16 + 4];                    // A end of CTA 1 as reference
+    fprintf(stderr, "\n  A-end offsets vs CTA 1 (ns):");
+    for (int c = 0; c < S->G; ++c) fprintf(stderr, " %lld", h[c * 16 + 4] - t0);
+    fprintf(stderr, "\n");
+    cudaFree(S->tl);
+    S->tl = nullptr;
+  }
+  if (S->tl) {                         // profiling: median phase durations (ns) over the recorded iterations
+    long long h[64 * 16];
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, S->tl, sizeof(h), cudaMemcpyDeviceToHost);
+    const int nit = S->args.n_iter < 64 ? S->args.n_iter : 64;
+    const char* names[9] = {"F", "B1", "limbs", "A", "hist", "B2", "S1", "B3", "S2"};
+    fprintf(stderr, "fused timeline (CTA %d, ns, median of %d iterations):", S->args.tl_cta, nit > 1 ? nit - 1 : nit);
+    for (int k = 0; k < 9; ++k) {
+      std::vector<long long> d;
+      for (int n = (nit > 1 ? 1 : 0); n < nit; ++n) d.push_back(h[n * 16 + k + 1] - h[n * 16 + k]);
+      std::sort(d.begin(), d.end());
+      fprintf(stderr, " %s %lld", names[k], d.empty() ? -1 : d[d.size() / 2]);
+    }
+    for (int k = 10; k < 15; ++k) {                  // A: tile 0..2 wait start / wait end
+      std::vector<long long> d;
+      for (int n = (nit > 1 ? 1 : 0); n < nit; ++n) d.push_back(h[n * 16 + k + 1] - h[n * 16 + k]);
+      std::sort(d.begin(), d.end());
+      fprintf(stderr, " a%d %lld", k - 10, d.empty() ? -1 : d[d.size() / 2]);
+    }
+    std::vector<long long> it;
+    for (int n = 1; n < nit; ++n) it.push_back(h[n * 16] - h[(n - 1) * 16]);
+    std::sort(it.begin(), it.end());
+    fprintf(stderr, " | iteration %lld\n", it.empty() ? -1 : it[it.size() / 2]);
+    cudaFree(S->tl);
+  }
   if (S->block) cudaFree(S->block);
   delete S;
 }

@@ -596,8 +596,12 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
     delete S;
     return IHT_ECUDA;
   }
-  if (cfg->fused && !batched && !fm && !S->rowshard && cfg->step_mode == 0 && cfg->adjoint_variant == 0 &&
-      cfg->n_iter > 0 && !fused_disabled_by_env()) {
+  // fused = 1 (auto): when the adjoint copy is large enough for the persistent kernel to pay
+  // (>= 2 MiB: measured, config 1's 128 KiB copies run faster as per-step kernels); 2: whenever
+  // it fits
+  const bool fuse_size = cfg->fused == 2 || iht_qmat_bytes(q0.rows, q0.cols, q0.planes, q0.bits) >= (2ll << 20);
+  if (cfg->fused && fuse_size && !batched && !fm && !S->rowshard && cfg->step_mode == 0 &&
+      cfg->adjoint_variant == 0 && cfg->n_iter > 0 && !fused_disabled_by_env()) {
     const int frc = iht_fused_create(pool, K, cfg->s, cfg->n_iter, cfg->mu, cfg->trace, S->yhat, S->r, S->g,
                                      S->xs_idx, S->xs_val, S->xs_nnz, &S->fused);
     if (frc != IHT_OK && frc != IHT_EUNSUPPORTED) {

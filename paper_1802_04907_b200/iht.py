@@ -386,8 +386,9 @@ class Solver:
                  use_graph=True, comm=None, profile=False, nrhs=1, adaptive=False, c=1e-3, k=2.0, max_shrink=60,
                  fused=True):
         """pool: list of QCopy (stored copies), or a FreshPhi (NEXT-2: copies drawn on the fly,
-        K = 2 n*).  fused: run the whole loop as one persistent kernel when the problem fits
-        (iht_config.fused); False keeps the per-step kernels."""
+        K = 2 n*).  fused: True = run the whole loop as one persistent kernel when the problem
+        fits and is large enough to pay (iht_config.fused = 1), "force" = whenever it fits (2),
+        False = per-step kernels (0)."""
         lib = load()
         self.pool = pool                     # keep the code / Phi tensors alive
         self.s, self.n_iter = s, n_iter
@@ -397,7 +398,7 @@ class Solver:
                         adjoint_variant=adjoint_variant, seed=seed, trace=int(trace), use_graph=int(use_graph),
                         comm=comm.handle if comm is not None else None, profile=int(profile), nrhs=self.nrhs,
                         step_mode=int(adaptive), step_c=float(c), step_k=float(k), max_shrink=int(max_shrink),
-                        fused=int(fused))
+                        fused=2 if fused == "force" else int(bool(fused)))
         h = ctypes.c_void_p()
         if isinstance(pool, FreshPhi):
             check(lib.iht_solver_create_fresh(ctypes.byref(pool.desc), ctypes.byref(cfg), ctypes.byref(h)),

@@ -36,7 +36,7 @@ for name, p in cases.items():
     ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, K)
     y = torch.from_numpy(p.y).to(dev)
     for fused in (True, False):
-        sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, fused=fused)
+        sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, fused="force" if fused else False)
         sol.run(y)
         torch.cuda.synchronize()
         idx, val, nnz = sol.trace_arrays()
@@ -53,7 +53,7 @@ for cfg in (1, 2, 3):
     pool, c, _, rows, row0 = build_pool(p, 0, 1, dev, False)
     y = torch.from_numpy(p.y).to(dev)
     for fused in (True, False):
-        sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, fused=fused)
+        sol = iht.Solver(pool, p.s, p.n_iter, p.mu, p.b_y, p.seed, fused="force" if fused else False)
         for _ in range(3):
             sol.run(y)
         torch.cuda.synchronize()

@@ -309,7 +309,8 @@ def test_free_running_solver(case, graph, fused):
     ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, p.K)
     c = OQ.scale_c(p.phi)
     pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c, p.seed)
-    sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, use_graph=graph, fused=fused)
+    sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, use_graph=graph,
+                     fused="force" if fused else False)
     assert sol.fused == fused                 # every case fits the fused persistent kernel
     sol.run(_to_dev(p.y))
     idx, val, nnz = sol.trace_arrays()
