@@ -132,6 +132,8 @@ def load(path=None):
     global _lib
     if _lib is not None:
         return _lib
+    if path is None and os.environ.get("IHT_LIB") == "checked":      # bounds-checked build (debug)
+        path = os.path.join(os.path.dirname(LIB_PATH), "libiht_checked.so")
     path = path or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libiht.so not built at {path}; run `python -m paper_1802_04907_b200.build` "

@@ -19,6 +19,11 @@ INCLUDE = os.path.join(ROOT, "include")
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libiht.so")
+# checked variant (-DIHT_CHECKS): device-side bounds checks on every hand-rolled pipeline's
+# indices and bounded mbarrier / grid-barrier waits that trap instead of hanging -- the
+# stand-in for compute-sanitizer, which is closed on this GPU pool.  Loaded with IHT_LIB=checked.
+LIB_CHECKED = os.path.join(HERE, "libiht_checked.so")
+BUILD_CHECKED = os.path.join(HERE, "_build_checked")
 GEN_SRC = os.path.join(ROOT, "workloads", "csrc", "gen.cu")
 GEN_LIB = os.path.join(ROOT, "workloads", "libihtgen.so")
 
@@ -51,8 +56,8 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, obj, verbose):
-    cmd = [nvcc(), *ARCH, *FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
+def _compile(src, obj, verbose, extra=()):
+    cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")
@@ -64,26 +69,32 @@ def _compile(src, obj, verbose):
     return obj
 
 
-def build(force=False, verbose=True):
-    """Compile libiht.so and libihtgen.so if any source is newer than the library."""
-    os.makedirs(BUILD, exist_ok=True)
+def _build_lib(lib, bdir, extra, force, verbose):
+    os.makedirs(bdir, exist_ok=True)
     srcs = _sources()
     hdrs = _headers()
     objs = []
     jobs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         for s in srcs:
-            o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
+            o = os.path.join(bdir, os.path.basename(s)[:-3] + ".o")
             objs.append(o)
             if force or _stale(o, [s, *hdrs]):
-                jobs.append(ex.submit(_compile, s, o, verbose))
+                jobs.append(ex.submit(_compile, s, o, verbose, extra))
         for j in jobs:
             j.result()
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-ldl"]
         subprocess.run(cmd, check=True, capture_output=True, text=True)
         if verbose:
-            print(f"[build] linked {LIB}", file=sys.stderr)
+            print(f"[build] linked {lib}", file=sys.stderr)
+
+
+def build(force=False, verbose=True, checked=True):
+    """Compile libiht.so (and libiht_checked.so) and libihtgen.so if any source is newer."""
+    _build_lib(LIB, BUILD, (), force, verbose)
+    if checked:
+        _build_lib(LIB_CHECKED, BUILD_CHECKED, ("-DIHT_CHECKS",), force, verbose)
     if force or _stale(GEN_LIB, [GEN_SRC]):
         cmd = [nvcc(), *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", GEN_SRC, "-o", GEN_LIB]
         res = subprocess.run(cmd, capture_output=True, text=True)

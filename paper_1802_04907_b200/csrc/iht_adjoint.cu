@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)min(kReq, nsteps - rq_ks) * 1024;
         const uint32_t bar = bar_w + 8 * slot;
+        IHT_DCHECK(slot < kRing && rq >= a.codes && rq + bytes <= a.codes + ntask * 16 * a.strip_bytes,
+                   "adjoint: bulk request inside the copy");
         mbar_expect_tx(bar, bytes);
         bulk_g2s(ring_w + slot * kSlot, rq, bytes, bar);
       }
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         l2w |= (uint32_t)(l2 & 255) << (8 * i);
       }
       const int off = ch * (16 * P) + (4 * (rho % P) + rho / P) * 4;   // slot 4 j + v
+      IHT_DCHECK(off + 4 <= a.limb_stride, "adjoint: limb word inside its plane");
       *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
       *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
       *reinterpret_cast<uint32_t*>(limbs + 2 * a.limb_stride + off) = l2w;

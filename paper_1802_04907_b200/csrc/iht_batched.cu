@@ -29,6 +29,7 @@
 #include <stdlib.h>
 
 #include "iht_internal.cuh"
+#include "iht_mma.cuh"
 
 namespace iht {
 
@@ -65,6 +66,9 @@ __device__ __forceinline__ void mbar_expect_tx2(uint32_t mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait2(uint32_t mbar, uint32_t parity) {
+#ifdef IHT_CHECKS
+  mbar_wait(mbar, parity);             // bounded (iht_mma.cuh)
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
@@ -72,6 +76,7 @@ __device__ __forceinline__ void mbar_wait2(uint32_t mbar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(mbar),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s2(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -258,6 +263,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           }
         };
         const uint32_t ta = tmem + a_col0 + (uint32_t)(ss * ACOLS) + ((uint32_t)(warp * 32) << 16);
+        IHT_DCHECK(((a_col0 + (uint32_t)((ss + 1) * ACOLS)) & 0xFFFFu) <= 512u, "batched: A stage inside TMEM");
         auto store = [&](int ts, const uint32_t* out) {
           if (!(a.probe & 4)) {
 #pragma unroll
@@ -373,6 +379,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
         if (lane < 8) {
           int64_t col_tile = (int64_t)tile * 8 + lane;                // 16-column tile index
           if (col_tile > last_tile) col_tile = last_tile;              // past N: any valid data
+          IHT_DCHECK(ps < PKS && (int64_t)kb * TS * 1024 + bytes <= 16 * a.strip_bytes && col_tile >= 0 &&
+                         col_tile <= last_tile, "batched: packed-code bulk copy inside the copy");
           bulk_g2s2(smem_u32(sP + ps * PK + lane * (TS * 1024)),
                     a.codes + col_tile * 16 * a.strip_bytes + (int64_t)kb * TS * 1024, bytes,
                     smem_u32(&pk_full[ps]));
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           if ((a.probe & 1) && wrapped) {
             mbar_arrive2(smem_u32(&st_full[ss]));                 // probe: reuse the stale stage
           } else {
+            IHT_DCHECK(ss < ST && kb < a.nkb, "batched: limb-image stage index");
             mbar_expect_tx2(smem_u32(&st_full[ss]), (uint32_t)BSZ);
             bulk_g2s2(smem_u32(sB + ss * BSZ), a.bimg + (int64_t)kb * BSZ, (uint32_t)BSZ, smem_u32(&st_full[ss]));
           }

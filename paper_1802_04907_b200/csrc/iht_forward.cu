@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
       const int j = j0 + 8 * CS * u;
       const bool ok = j < nst && live;
       xv[u] = j < nst ? sval[j] : 0.0f;
+      IHT_DCHECK(!ok || sidx[j] + kofs + 4 <= (ncols + 15) / 16 * 16 * strip_bytes, "forward: code word inside the copy");
       w[u] = ok ? __ldg(reinterpret_cast<const uint32_t*>(codes + sidx[j] + kofs)) : 0u;
     }
 #pragma unroll

@@ -152,6 +152,9 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       if (rq_k == 0 && rq_h == 0) rq_src = ctab[(2 * rq_n - 2) % a.K];
       const uint8_t* src = rq_src + (int64_t)(t0 + warp + kFuWarps * rq_k) * a.tile_bytes +
                            (int64_t)rq_h * a.block_bytes;
+      IHT_DCHECK(rq_slot < a.mslot && t0 + warp + kFuWarps * rq_k < t1 && rq_h < a.nsub &&
+                     (int64_t)(t0 + warp + kFuWarps * rq_k + 1) * a.tile_bytes <= (int64_t)a.ntiles * a.tile_bytes,
+                 "fused: ring request inside this CTA's tiles of the copy");
       mbar_expect_tx(wfull + 8 * rq_slot, (uint32_t)a.block_bytes);
       bulk_g2s(wring + (uint32_t)rq_slot * a.block_bytes, src, (uint32_t)a.block_bytes, wfull + 8 * rq_slot);
       ++nb;
@@ -180,7 +183,16 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       bar_target += (unsigned int)G;
       // release: the CTA's writes (ordered before by bar.sync) become visible with the arrival
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+#ifdef IHT_CHECKS
+      long long spins = 0;
+#endif
       while (ld_acquire_u32(a.bar) < bar_target) {
+#ifdef IHT_CHECKS
+        if (++spins > IHT_SPIN_LIMIT) {
+          printf("IHT_DCHECK: fused grid barrier did not complete (block %d, target %u)\n", cta, bar_target);
+          __trap();
+        }
+#endif
       }
     }
     __syncthreads();
@@ -388,6 +400,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         const int l2r1 = __shfl_down_sync(0xffffffffu, v10, 1);
         if (t == 0) {                 // exact per-limb int32 sums of the warps sharing (tile, chunk)
           int* v = Vs + (cur_seg * 16 + g8) * 3;
+          IHT_DCHECK((cur_seg * 16 + g8 + 8) * 3 + 3 <= T * a.nchunks * 48, "fused: limb-sum slot inside V");
           atomicAdd(v, v00);
           atomicAdd(v + 1, v01);
           atomicAdd(v + 2, l2r0);
@@ -468,6 +481,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       // x's entries on this CTA's columns: a_n = x_n + mu g_n
       for (int j = tid; j < s_nnz; j += kFuThreads) {
         const int c = xi_s[j] - col_lo;
+        IHT_DCHECK(j < a.s_cap && xi_s[j] >= 0 && xi_s[j] < a.N, "fused: support index");
         if (c >= 0 && c < ncol) as[c] = __fadd_rn(xv_s[j], as[c]);
       }
       __syncthreads();
@@ -530,6 +544,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         }
         if (f) {
           const int pos = off + __popc(bal & lt);
+          IHT_DCHECK(pos < a.cap_c, "fused: candidate inside the CTA's slot");
           a.cand_idx[(int64_t)cta * a.cap_c + pos] = col_lo + q;
           a.cand_val[(int64_t)cta * a.cap_c + pos] = v;
         }
@@ -585,6 +600,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
               if (cnt_s[mid] <= i) lo = mid; else hi = mid;
             }
             const int64_t src = (int64_t)lo * a.cap_c + (i - cnt_s[lo]);
+            IHT_DCHECK(i - cnt_s[lo] >= 0 && i - cnt_s[lo] < a.cap_c && i < kFuCandCap, "fused: staged candidate");
             ci[u] = __ldcg(&a.cand_idx[src]);
             cv[u] = __ldcg(&a.cand_val[src]);
           }
@@ -614,6 +630,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
             tot += wgt[w];
           }
           if (f) {
+            IHT_DCHECK(off + __popc(bal & lt) < a.s_cap, "fused: kept entry inside x");
             di[off + __popc(bal & lt)] = ci_s[q];
             dv[off + __popc(bal & lt)] = cv_s[q];
           }

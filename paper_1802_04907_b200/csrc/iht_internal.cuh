@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "iht.h"
 
@@ -15,6 +16,25 @@
   } while (0)
 
 #define IHT_LAUNCH_CHECK() IHT_CUDA_CHECK(cudaGetLastError())
+
+// Checked build (-DIHT_CHECKS, libiht_checked.so): device-side bounds checks on the indices of
+// the hand-rolled pipelines and bounded spin waits (mbarriers, grid barrier) that trap with a
+// message instead of hanging -- the stand-in for compute-sanitizer (closed on this GPU pool).
+#ifdef IHT_CHECKS
+#define IHT_DCHECK(cond, what)                                                                       \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("IHT_DCHECK failed: %s at %s:%d (block %d,%d thread %d)\n", what, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                                    \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#define IHT_SPIN_LIMIT (1ll << 27)
+#else
+#define IHT_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
 
 void iht_set_last_cuda_error(cudaError_t e, const char* expr, const char* file, int line);
 

@@ -38,12 +38,34 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint32_t mbar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(mbar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+#ifdef IHT_CHECKS
+  long long spins = 0;
+  while (!mbar_try(mbar, parity)) {
+    if (++spins > IHT_SPIN_LIMIT) {
+      printf("IHT_DCHECK: mbarrier wait did not complete (smem 0x%x parity %u, block %d thread %d)\n", mbar, parity,
+             (int)blockIdx.x, (int)threadIdx.x);
+      __trap();
+    }
+  }
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(mbar), "r"(parity) : "memory");
+#endif
 }
 
 // cp.async (LDGSTS) 16 bytes global -> shared, L2 only; one commit group per k-step

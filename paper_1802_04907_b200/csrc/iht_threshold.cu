@@ -682,6 +682,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     int off = base;
     for (int w = 0; w < warp; ++w) off += min(wgt[w], kWarpCand);
     for (int j = lane; j < min(wgt[warp], kWarpCand); j += 32) {
+      IHT_DCHECK(off + j < kClWarps * kWarpCand, "threshold: gathered candidate inside rank 0's list");
       gidx[off + j] = cidx[warp * kWarpCand + j];
       gval[off + j] = cval[warp * kWarpCand + j];
     }

@@ -53,4 +53,4 @@ if which in ("all", "fused", "solver"):
         torch.cuda.synchronize()
         sol.close()
 torch.cuda.synchronize()
-print("sanitize cases done:", which)
+print("sanitize cases done:", which, "library:", iht._lib.load()._name)
