@@ -308,7 +308,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         l1w |= (uint32_t)(l1 & 255) << (8 * i);
         l2w |= (uint32_t)(l2 & 255) << (8 * i);
       }
-      const int off = ch * (16 * P) + (4 * (rho % P) + rho / P) * 4;   // slot 4 j + v
+      // bank-spread layout: k-step ch / 4 holds 64 P bytes per plane; the 16-byte chunk of
+      // (bit position j = rho % P, lane t = ch % 4) sits at (4 j + t) 16, word v = rho / P in it
+      const int off = (ch >> 2) * (64 * P) + (4 * (rho % P) + (ch & 3)) * 16 + (rho / P) * 4;
       IHT_DCHECK(off + 4 <= a.limb_stride, "adjoint: limb word inside its plane");
       *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
       *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
@@ -357,10 +359,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
           const uint32_t src = ring_w + slot * kSlot + h * 1024 + g8 * 64 + t * 16;
           const uint4 s0 = lds128(src), s1 = lds128(src + 512);
           if (bload) {                           // other lanes keep the zeros set once below
-            const uint32_t bp = limb_n + (uint32_t)(ks * 4 + t) * (16 * P);
+            const uint32_t bp = limb_n + (uint32_t)ks * (64 * P) + t * 16;   // 12 lanes: 3 x 4 bank quads
 #pragma unroll
             for (int q = 0; q < P; ++q) {
-              const uint4 v = lds128(bp + 16 * q);
+              const uint4 v = lds128(bp + 64 * q);
               bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
             }
           }
@@ -477,7 +479,7 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   while ((p.KRp / 1024) % d) --d;
   p.KC = 1024 * d;
   p.nK = (int)((Rpad + KR - 1) / KR);
-  p.limb_stride = p.KRp + 64;
+  p.limb_stride = p.KRp + 32;                          // limb planes 2 bank quads apart
   const int nchunks = p.KRp / p.KC;
   p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
            sizeof(float) * nchunks * kMmaWarps + 16;

@@ -12,6 +12,8 @@
 // fixed order (shuffles, then shared memory), so r is deterministic.
 // Batched (config 5): grid row blockIdx.y = snapshot b, with its own x_b, y-hat_b, r_b.
 // Column shards: x holds GLOBAL indices; only [col_offset, col_offset + cols) are local.
+#include <stdlib.h>
+
 #include "iht_internal.cuh"
 
 namespace iht {
@@ -174,6 +176,12 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
   const unsigned blocks32 = (unsigned)ceil_div<int64_t>(words_total, 32);
   // many CTAs of tiny work (batched, small support): 4x wider CTAs, about one wave
   const bool wide = nrhs > 1 && (int64_t)blocks8 * nrhs > 4 * (int64_t)kNumSMs;
+  // a single observation over many rows (config 4: 8192 words): 16 words = one whole 64-byte
+  // piece of each support column per CTA (a full DRAM burst instead of half of one)
+  const unsigned blocks16 = (unsigned)ceil_div<int64_t>(words_total, 16);
+  static int ww_env = -1;                        // profiling override (IHT_FWD_WORDS = 8, 16, 32)
+  if (ww_env < 0) ww_env = getenv("IHT_FWD_WORDS") ? atoi(getenv("IHT_FWD_WORDS")) : 0;
+  const bool mid = ww_env == 16 || (ww_env == 0 && nrhs == 1 && blocks16 >= 2u * kNumSMs);
   const int64_t vlen = iht_vec_len(F->rows, F->planes);
   if (F->rows > 0x7FFFFFFF) return IHT_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -182,10 +190,14 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
   IHT_CUDA_CHECK(launch_pdl(forward_kernel<BB, WW>, dim3(NBLK, nrhs), dim3(kFwdThreads), 0, st, codes,    \
                             F->strip_bytes, words_total, (int)F->rows, (int)iht_rows_pad(F->rows), L, sigma, \
                             x_idx, x_val, x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen))
-  if (wide) {
+  if ((wide && ww_env == 0) || ww_env == 32) {
     if (F->bits == 2) IHT_FWD(2, 32, blocks32);
     else if (F->bits == 4) IHT_FWD(4, 32, blocks32);
     else IHT_FWD(8, 32, blocks32);
+  } else if (mid) {
+    if (F->bits == 2) IHT_FWD(2, 16, blocks16);
+    else if (F->bits == 4) IHT_FWD(4, 16, blocks16);
+    else IHT_FWD(8, 16, blocks16);
   } else {
     if (F->bits == 2) IHT_FWD(2, 8, blocks8);
     else if (F->bits == 4) IHT_FWD(4, 8, blocks8);

@@ -53,7 +53,7 @@ struct FusedArgs {
   int s, n_iter;
   int ntiles, tile_bytes, nchunks, wpc, words_total, cap_c, s_cap;
   int nsub, block_bytes, mslot;        // ring: a tile = nsub blocks; each warp owns mslot block slots
-  int limb_stride;                     // bytes between the 3 limb planes (Rpad + 64: bank spread)
+  int limb_stride;                     // bytes between the 3 limb planes (Rpad + 32: bank spread)
   const float* yhat;                   // [Rpad] stacked, pads 0
   float* r;                            // [Rpad] scratch (and the last r)
   float* g;                            // [N] the last g
@@ -362,7 +362,9 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
             l2w |= (uint32_t)(l2 & 255) << (8 * i);
           }
           if (ok) {
-            const int off = ch * (16 * P) + (4 * e + h) * 4;
+            // bank-spread limb layout: k-step ks = ch / 4 holds 64 P bytes per plane, the 16-byte
+            // chunk of (bit position j = e, lane t = ch % 4) at (4 j + t) 16, word v = h inside it
+            const int off = (ch >> 2) * (64 * P) + (4 * e + (ch & 3)) * 16 + h * 4;
             *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
             *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
             *reinterpret_cast<uint32_t*>(limbs + 2 * a.limb_stride + off) = l2w;
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       stamp(n, 3);
       // ============================================================== A: adjoint
       int cur_seg = -1;
-      int acc[P][4];
+      int acc[P][4];                                              // one accumulator per bit position
 #pragma unroll
       for (int j = 0; j < P; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0;
       auto flush = [&]() {
@@ -430,10 +432,10 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
             const uint32_t src = sbase + kk * 1024 + g8 * 64 + t * 16;
             const uint4 s0 = lds128(src), s1 = lds128(src + 512);
             if (bload) {
-              const uint32_t bp = limb_n + (uint32_t)(ks * 4 + t) * (16 * P);
+              const uint32_t bp = limb_n + (uint32_t)ks * (64 * P) + t * 16;
 #pragma unroll
-              for (int q = 0; q < P; ++q) {
-                const uint4 v = lds128(bp + 16 * q);
+              for (int q = 0; q < P; ++q) {                       // 12 lanes hit 3 x 4 distinct bank quads
+                const uint4 v = lds128(bp + 64 * q);
                 bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
               }
             }
@@ -795,7 +797,7 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
     const size_t bars = o;
     o = al16(o + 8 * (size_t)nring);
     const size_t limbs = o;
-    o = al16(o + 3 * (size_t)(Rpad + 64));
+    o = al16(o + 3 * (size_t)(Rpad + 32));
     const size_t fc = o;
     o = al16(o + 16 * (size_t)nchunks);
     const size_t as = o;
@@ -892,7 +894,7 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   A.wpc = wpc;
   A.words_total = words_total;
   A.cap_c = cap_c;
-  A.limb_stride = Rpad + 64;
+  A.limb_stride = Rpad + 32;                          // planes 2 bank quads apart
   A.s_cap = s_cap;
   A.yhat = yhat;
   A.r = r;

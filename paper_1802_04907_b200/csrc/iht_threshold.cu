@@ -893,7 +893,9 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
   cudaStream_t st = (cudaStream_t)stream;
   // max_nnz: the caller's x arrays hold at most min(ldx, s) entries (x is an H_s output)
   const int32_t max_nnz = ldx < s ? ldx : s;
-  if (N <= kClusterMaxN && nrhs <= 65535) {
+  static int multi_env = -1;                         // profiling override: IHT_THR_MULTI=1 forces T1-T3
+  if (multi_env < 0) multi_env = getenv("IHT_THR_MULTI") ? atoi(getenv("IHT_THR_MULTI")) : 0;
+  if (N <= kClusterMaxN && nrhs <= 65535 && !(multi_env && nparts == 0)) {
     int CL = 1;
     while ((int64_t)CL * kClusterSlice < N) CL *= 2;
     // spread small problems too: up to ~2 CTAs per SM while slices stay >= 4096 a-values
