@@ -253,7 +253,7 @@ static int enqueue_adaptive(iht_solver* S, cudaStream_t st, int n, const iht_qma
   const int B = S->B, s = S->cfg.s;
   const int32_t *gi = xi, *gn = xn;
   if (n == 1) {   // Gamma^[1] = supp(H_s(Phi-hat_1^H y-hat)): x^[1] = 0, so H_s(g^[1])
-    if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, 1.0f, s, S->N, 0, B, S->ad_gi, S->ad_gv, s, S->ad_gn,
+    if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g, 1.0f, nullptr, s, S->N, 0, B, S->ad_gi, S->ad_gv, s, S->ad_gn,
                                     S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
       return rc;
     gi = S->ad_gi;
@@ -339,7 +339,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
   // single observation, fixed step, int8-MMA adjoint, no g all-reduce, fused threshold:
   // the adjoint's split-K partials go straight to the threshold (one launch fewer)
   const bool fuse_parts = !S->fresh && !S->batched && !S->rowshard && S->cfg.step_mode == 0 &&
-                          S->cfg.adjoint_variant == 0 && iht_threshold_launches(S->N) == 1;
+                          S->cfg.adjoint_variant == 0;
   int nparts = 0;
   float gsigma = 1.0f;
   for (int n = 1; n <= S->cfg.n_iter; ++n) {
@@ -402,7 +402,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       int32_t* ci = S->cand_send;
       float* cv = reinterpret_cast<float*>(S->cand_send + xslot);
       int32_t* cn = S->cand_send + 2 * xslot;
-      if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g + S->col0, S->cfg.mu, s, S->nloc, S->col0, 1, ci, cv, s,
+      if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g + S->col0, S->cfg.mu, nullptr, s, S->nloc, S->col0, 1, ci, cv, s,
                                       cn, S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
       L += iht_threshold_launches(S->nloc);
@@ -414,7 +414,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
         return rc;
       L += 1;
     } else if (!S->colshard) {
-      if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
+      if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g, S->cfg.mu, nullptr, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
       L += iht_threshold_launches(S->N);
@@ -422,7 +422,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       int32_t* ci = S->cand_send;
       float* cv = reinterpret_cast<float*>(S->cand_send + xslot);
       int32_t* cn = S->cand_send + 2 * xslot;
-      if ((rc = iht_threshold_batched(xi, xv, xn, s, S->g, S->cfg.mu, s, S->N, q0.col_offset, B, ci, cv, s, cn,
+      if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g, S->cfg.mu, nullptr, s, S->N, q0.col_offset, B, ci, cv, s, cn,
                                       S->ws_thr, S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
       L += iht_threshold_launches(S->N);

@@ -94,12 +94,20 @@ __device__ __forceinline__ ThrWs thr_at(const ThrWs& w, int b) {
   return o;
 }
 
-// T1: a = x + mu g, global histogram of key >> 20
+// T1: a = x + mu g (g possibly the sum of split-K partials), the CTA's 2048-bin histogram of
+// the top 11 key bits in shared memory, then one global atomic per nonzero bin.  The global
+// histogram is zero on entry (zeroed by T3 of the previous call, or by the memset of a cold
+// workspace).
 __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev,
-    int64_t N, int64_t col_offset, ThrWs w0) {
+    int64_t N, int64_t col_offset, ThrWs w0, int nparts, float gsigma, float* __restrict__ gout) {
   __shared__ float as[kTile];
+  __shared__ int hist[kHistBins];
+  pdl_launch_dependents();
+  const int tid = threadIdx.x;
+  for (int b = tid; b < kHistBins; b += kTileThreads) hist[b] = 0;
+  pdl_wait();                                   // g (adjoint) and x (previous H_s)
   const int bq = blockIdx.y;
   if (mu_dev) mu = mu_dev[bq];
   const ThrWs w = thr_at(w0, bq);
@@ -107,12 +115,29 @@ __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
   x_val += (int64_t)bq * ldx;
   x_nnz += bq;
   g += (int64_t)bq * N;
-  __shared__ int hist[kHistBins];
-  const int tid = threadIdx.x;
   const int64_t start = (int64_t)blockIdx.x * kTile;
   const int cnt = (int)min64(kTile, N - start);
-  for (int b = tid; b < kHistBins; b += kTileThreads) hist[b] = 0;
-  for (int i = tid; i < cnt; i += kTileThreads) as[i] = __fmul_rn(mu, g[start + i]);
+  constexpr int PER = kTile / kTileThreads;     // 8 entries per thread, all loads in flight
+  float gv[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kTileThreads;
+    float v = 0.0f;
+    if (i < cnt) {
+      v = __ldg(g + start + i);
+      for (int k = 1; k < nparts; ++k) v = __fadd_rn(v, __ldg(g + (int64_t)k * N + start + i));
+      if (nparts > 0) v = __fmul_rn(gsigma, v);   // adjoint_reduce_kernel's order and rounding
+    }
+    gv[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kTileThreads;
+    if (i < cnt) {
+      if (gout && nparts > 0) gout[start + i] = gv[u];
+      as[i] = __fmul_rn(mu, gv[u]);
+    }
+  }
   int nnz = *x_nnz;
   nnz = nnz < 0 ? 0 : min(nnz, max_nnz);
   __syncthreads();
@@ -129,51 +154,53 @@ __global__ void __launch_bounds__(kTileThreads) thr_update_hist(
     nan |= key > 0x7F800000u;
     atomicAdd(&hist[key >> 20], 1);
   }
-  if (nan) atomicOr(&w.flags[0], 1);
-  __syncthreads();
+  nan = __syncthreads_or(nan);
+  if (tid == 0 && nan) atomicOr(&w.flags[0], 1);
   for (int b = tid; b < kHistBins; b += kTileThreads)
     if (hist[b]) atomicAdd(&w.hist[b], hist[b]);
 }
 
-// T2: bin d1 of the s-th largest key (same in every CTA), ordered per-tile compaction
-// of the entries with digit >= d1 (key > 0).
+// T2: every CTA finds the bin d1 holding the s-th largest key in the global histogram (the
+// same in all CTAs; CTA 0 records d1 and the count above it for T3) and writes its entries
+// with digit >= d1 (key > 0) to its candidate slot in index order.
 __global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N, int64_t col_offset, ThrWs w0) {
+  __shared__ int hist[kHistBins];
+  __shared__ int scratch[kTileThreads / 32], wcnt[kTileThreads / 32], sh[2];
+  pdl_launch_dependents();
+  pdl_wait();                                   // T1's histogram and a
   const ThrWs w = thr_at(w0, blockIdx.y);
-  __shared__ int sfx[kTileThreads];
-  __shared__ int d1s;
-  __shared__ int wcnt[kTileThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // thread t owns bins [8t, 8t+8); suffix sums over threads (descending bins)
-  int local = 0;
-  for (int b = tid * 8; b < tid * 8 + 8; ++b) local += w.hist[b];
-  sfx[tid] = local;
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0, d = 0;
-    const int target = s < 1 ? 1 : s;
-    for (int t = kTileThreads - 1; t >= 0 && d == 0; --t) {
-      if (acc + sfx[t] >= target) {
-        for (int b = t * 8 + 7; b >= t * 8; --b) {
-          acc += w.hist[b];
-          if (acc >= target) { d = b; break; }
-        }
-        break;
-      }
-      acc += sfx[t];
-    }
-    d1s = d;
+  {
+    int hv[kHistBins / kTileThreads];
+#pragma unroll
+    for (int u = 0; u < kHistBins / kTileThreads; ++u) hv[u] = __ldcg(&w.hist[tid + u * kTileThreads]);
+#pragma unroll
+    for (int u = 0; u < kHistBins / kTileThreads; ++u) hist[tid + u * kTileThreads] = hv[u];
   }
+  if (tid == 0) sh[0] = sh[1] = 0;
   __syncthreads();
-  const unsigned int d1 = (unsigned int)d1s;
+  const bool all = (int64_t)s >= N;
+  if (!all && s > 0) find_bin<kTileThreads>(hist, kHistBins, s, &sh[0], &sh[1], scratch);
+  const unsigned int d1 = all ? 0u : (unsigned int)sh[0];
+  if (blockIdx.x == 0 && tid == 0) {
+    w.flags[1] = (int)d1;
+    w.flags[2] = all ? 0 : sh[1];
+  }
   const int64_t start = (int64_t)blockIdx.x * kTile;
   const int cnt = (int)min64(kTile, N - start);
-  // two passes over the tile (L1/L2 resident): count per warp, then write in order
   const int per_warp = kTile / (kTileThreads / 32);       // 256 contiguous entries per warp
   const int lo = warp * per_warp, hi = min(cnt, lo + per_warp);
+  float v8[per_warp / 32];
+#pragma unroll
+  for (int u = 0; u < per_warp / 32; ++u) {
+    const int i = lo + u * 32 + lane;
+    v8[u] = i < hi ? __ldcg(&w.a[start + i]) : 0.0f;
+  }
   int c = 0;
-  for (int i0 = lo; i0 < hi; i0 += 32) {
-    const int i = i0 + lane;
-    const unsigned int key = i < hi ? (__float_as_uint(w.a[start + i]) & 0x7FFFFFFFu) : 0u;
+#pragma unroll
+  for (int u = 0; u < per_warp / 32; ++u) {
+    const int i = lo + u * 32 + lane;
+    const unsigned int key = __float_as_uint(v8[u]) & 0x7FFFFFFFu;
     c += __popc(__ballot_sync(0xffffffffu, i < hi && key > 0u && (key >> 20) >= d1));
   }
   if (lane == 0) wcnt[warp] = c;
@@ -181,9 +208,10 @@ __global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N,
   int base = 0;
   for (int q = 0; q < warp; ++q) base += wcnt[q];
   const unsigned int lt = (1u << lane) - 1u;
-  for (int i0 = lo; i0 < hi; i0 += 32) {
-    const int i = i0 + lane;
-    const float v = i < hi ? w.a[start + i] : 0.0f;
+#pragma unroll
+  for (int u = 0; u < per_warp / 32; ++u) {
+    const int i = lo + u * 32 + lane;
+    const float v = v8[u];
     const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
     const bool sel = i < hi && key > 0u && (key >> 20) >= d1;
     const unsigned int b = __ballot_sync(0xffffffffu, sel);
@@ -201,7 +229,12 @@ __global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N,
   }
 }
 
-// T3: gather candidates (index order) and finish the selection in one CTA.
+// T3 (one CTA per snapshot): gather the candidates (index order), then the exact top-s.  Keys
+// in bins above d1 (`above` < s of them) are all kept; the need = s - above remaining come from
+// bin d1: a second 11-bit histogram over the bin-d1 keys finds the sub-bin d2 of the need-th
+// largest, keys above it are kept, and the few keys of sub-bin d2 are ranked (greater key, or
+// equal key at a lower index).  Ordered compaction writes the support.  Finally the global
+// histogram and flags are zeroed for the next call.
 __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
     const int32_t* __restrict__ x_nnz, int s, int64_t N, int64_t col_offset, ThrWs w0,
     int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz) {
@@ -217,53 +250,169 @@ __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
   __shared__ int hist[2048];
   __shared__ int scratch[kThrWarps];
   __shared__ int wgt[kThrWarps], weq[kThrWarps], wtake[kThrWarps], wbase[kThrWarps];
-  __shared__ int sh[4];
+  __shared__ int sh[8];
   __shared__ int tile_base[1025];
-  const int tid = threadIdx.x;
-  if (*x_nnz < 0) {                 // poisoned input (earlier non-finite a) stays poisoned
-    if (tid == 0) *out_nnz = -1;
-    return;
-  }
-  const int nan = w.flags[0];
-  if (s == 0 || nan) {              // H_0 keeps nothing; NaN -> domain error
-    if (tid == 0) *out_nnz = nan ? -1 : 0;
-    return;
-  }
+  __shared__ int grp_k[1024];                   // keys of sub-bin d2 (index order)
+  __shared__ unsigned char keep[kCandCap];
+  pdl_launch_dependents();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  pdl_wait();                                   // T2's candidates
   const int ntiles = (int)((N + kTile - 1) / kTile);
-  // total candidates
-  int total = 0;
+  auto finish = [&]() {                         // zero the histogram + flags for the next call
+    __syncthreads();
+    for (int b = tid; b < kHistBins; b += kThrThreads) w.hist[b] = 0;
+    if (tid < 4) w.flags[tid] = 0;
+  };
+  const int poisoned = *x_nnz < 0, nan = __ldcg(&w.flags[0]);
+  if (poisoned || nan || s == 0) {              // poisoned input / NaN -> domain error; H_0 keeps nothing
+    if (tid == 0) *out_nnz = (poisoned || nan) ? -1 : 0;
+    finish();
+    return;
+  }
+  // tile offsets: block-wide exclusive scan of the per-tile counts (ntiles <= 1024)
+  const int myc = tid < ntiles ? __ldcg(&w.ccount[tid]) : 0;
+  int incl = myc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) scratch[warp] = incl;
+  __syncthreads();
   if (tid == 0) {
     int acc = 0;
-    for (int t = 0; t < ntiles; ++t) acc += w.ccount[t];
+    for (int q = 0; q < kThrWarps; ++q) {
+      const int v = scratch[q];
+      scratch[q] = acc;
+      acc += v;
+    }
     sh[3] = acc;
   }
   __syncthreads();
-  total = sh[3];
-  const bool fits = total <= kCandCap && ntiles <= 1024 && (int64_t)s < N;
-  if (fits) {
-    if (tid == 0) {
-      int acc = 0;
-      for (int t = 0; t < ntiles; ++t) { tile_base[t] = acc; acc += w.ccount[t]; }
-    }
-    __syncthreads();
-    // gather: warp per tile, in order
-    for (int t = tid >> 5; t < ntiles; t += kThrWarps) {
-      const int c = w.ccount[t], b = tile_base[t];
-      const int64_t src = (int64_t)t * kTile;
-      for (int i = tid & 31; i < c; i += 32) {
-        cidx[b + i] = w.cidx[src + i];
-        cval[b + i] = w.cval[src + i];
-      }
-    }
-    __syncthreads();
-    select_ordered(total, s, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, out_idx, out_val,
-                   out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
-  } else {
+  if (tid < ntiles) tile_base[tid] = scratch[warp] + incl - myc;
+  if (tid == 0) tile_base[ntiles] = sh[3];
+  __syncthreads();
+  const int total = sh[3];
+  const unsigned int d1 = (unsigned int)__ldcg(&w.flags[1]);
+  const int above = __ldcg(&w.flags[2]);
+  const bool all = (int64_t)s >= N;
+  if (total > kCandCap || ntiles > 1024) {      // massive ties: radix passes over a itself
     const float* a = w.a;
     const int c0 = (int)col_offset;
-    select_ordered((int)N, s, [&](int i) { return a[i]; }, [&](int i) { return c0 + i; }, out_idx, out_val,
+    select_ordered((int)N, s, [&](int i) { return __ldcg(&a[i]); }, [&](int i) { return c0 + i; }, out_idx, out_val,
                    out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
+    finish();
+    return;
   }
+  // gather: candidate i of tile t at tile_base[t] + j (one per thread per round, tile by binary search)
+  for (int i0 = 0; i0 < total; i0 += 2 * kThrThreads) {
+    int32_t ci[2];
+    float cv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * kThrThreads + tid;
+      if (i < total) {
+        int lo = 0, hi = ntiles;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (tile_base[mid] <= i) lo = mid; else hi = mid;
+        }
+        const int64_t src = (int64_t)lo * kTile + (i - tile_base[lo]);
+        ci[u] = __ldcg(&w.cidx[src]);
+        cv[u] = __ldcg(&w.cval[src]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * kThrThreads + tid;
+      if (i < total) {
+        cidx[i] = ci[u];
+        cval[i] = cv[u];
+      }
+    }
+  }
+  for (int b = tid; b < 2048; b += kThrThreads) hist[b] = 0;
+  __syncthreads();
+  auto key_of = [&](int i) { return __float_as_uint(cval[i]) & 0x7FFFFFFFu; };
+  if (all || total <= s) {
+    for (int i = tid; i < total; i += kThrThreads) keep[i] = 1;
+  } else {
+    const int need = s - above;                 // >= 1
+    // second level: 11-bit histogram of the bin-d1 keys (bits 19..9)
+    for (int i = tid; i < total; i += kThrThreads) {
+      const unsigned int k = key_of(i);
+      keep[i] = (k >> 20) > d1;
+      if ((k >> 20) == d1) atomicAdd(&hist[(k >> 9) & 2047], 1);
+    }
+    __syncthreads();
+    find_bin<kThrThreads>(hist, 2048, need, &sh[0], &sh[1], scratch);
+    const unsigned int d2 = (unsigned int)sh[0];
+    const int need2 = need - sh[1];             // >= 1 keys to take from sub-bin d2
+    const unsigned int pre = (d1 << 11) | d2;   // 22-bit prefix of the sub-bin
+    // compact sub-bin d2 (index order); keep the keys above it
+    int ng = 0;
+    for (int i0 = 0; i0 < total; i0 += kThrThreads) {
+      const int i = i0 + tid;
+      const unsigned int k = i < total ? key_of(i) : 0u;
+      const bool f = i < total && (k >> 9) == pre;
+      if (i < total && (k >> 20) == d1 && ((k >> 9) & 2047) > d2) keep[i] = 1;
+      const unsigned int bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wgt[warp] = __popc(bal);
+      __syncthreads();
+      int off = ng, tot = 0;
+      for (int q = 0; q < kThrWarps; ++q) {
+        if (q < warp) off += wgt[q];
+        tot += wgt[q];
+      }
+      if (f && off + __popc(bal & lt) < 1024) {
+        grp_k[off + __popc(bal & lt)] = (int)k;
+        tile_base[off + __popc(bal & lt)] = i;  // reuse: list position of the group member
+      }
+      ng += tot;
+      __syncthreads();
+    }
+    if (ng <= 1024) {
+      for (int e = tid; e < ng; e += kThrThreads) {
+        const unsigned int ke = (unsigned int)grp_k[e];
+        int rk = 0;
+        for (int f = 0; f < ng; ++f) {
+          const unsigned int kf = (unsigned int)grp_k[f];
+          rk += kf > ke || (kf == ke && f < e);
+        }
+        if (rk < need2) keep[tile_base[e]] = 1;
+      }
+    } else {                                    // a crowded sub-bin: radix passes over the candidates
+      __syncthreads();
+      select_ordered(total, s, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, out_idx, out_val,
+                     out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
+      finish();
+      return;
+    }
+  }
+  __syncthreads();
+  // ordered compaction of the kept candidates
+  int base = 0;
+  for (int i0 = 0; i0 < total; i0 += kThrThreads) {
+    const int i = i0 + tid;
+    const bool f = i < total && keep[i];
+    const unsigned int bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wgt[warp] = __popc(bal);
+    __syncthreads();
+    int off = base, tot = 0;
+    for (int q = 0; q < kThrWarps; ++q) {
+      if (q < warp) off += wgt[q];
+      tot += wgt[q];
+    }
+    if (f) {
+      out_idx[off + __popc(bal & lt)] = cidx[i];
+      out_val[off + __popc(bal & lt)] = cval[i];
+    }
+    base += tot;
+    __syncthreads();
+  }
+  if (tid == 0) *out_nnz = base;
+  finish();
 }
 
 // ---------------------------------------------------------------------------- fused (cluster)
@@ -855,32 +1004,47 @@ static int thr_attrs() {
   return IHT_OK;
 }
 
+// Grid path (T1 - T3 over every SM) or one cluster launch: the cluster holds at most
+// kClusterMaxN a-values; a single large problem (N >= kGridSelMinN) spreads over all SMs
+// instead of CL <= 8 (config 4, N = 262144: 22.5 us in the cluster).  IHT_THR_MULTI=1 forces
+// the grid path, =2 the cluster path where it fits (profiling).
+constexpr int64_t kGridSelMinN = 131072;
+static bool thr_grid_path(int64_t N, int nrhs) {
+  static int env = -1;
+  if (env < 0) env = getenv("IHT_THR_MULTI") ? atoi(getenv("IHT_THR_MULTI")) : 0;
+  if (N > kClusterMaxN || env == 1) return true;
+  if (env == 2) return false;
+  return nrhs == 1 && N >= kGridSelMinN;
+}
+
 static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                           const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
                           int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
-                          int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream);
+                          int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream,
+                          bool ws_prezeroed);
 
 int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                              const float* g, float mu, const float* mu_dev, int32_t s, int64_t N, int64_t col_offset,
                              int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws,
                              int64_t ws_bytes, void* stream) {
   return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, mu_dev, s, N, col_offset, nrhs, out_idx,
-                        out_val, ldo, out_nnz, ws, ws_bytes, stream);
+                        out_val, ldo, out_nnz, ws, ws_bytes, stream, true);   // the solver's workspace
 }
 
 int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                         const float* g, int nparts, float gsigma, float* gout, float mu, int32_t s, int64_t N,
                         int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
                         void* stream) {
-  if (nparts < 0 || (nparts > 0 && iht_threshold_launches(N) != 1)) return IHT_EUNSUPPORTED;
+  if (nparts < 0) return IHT_EUNSUPPORTED;
   return threshold_impl(x_idx, x_val, x_nnz, ldx, g, nparts, gsigma, gout, mu, nullptr, s, N, 0, 1, out_idx, out_val,
-                        ldo, out_nnz, ws, ws_bytes, stream);
+                        ldo, out_nnz, ws, ws_bytes, stream, true);
 }
 
 static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                           const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
                           int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
-                          int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream) {
+                          int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream,
+                          bool ws_prezeroed) {
   if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr ||
       s < 0 || N <= 0 || N > 0x7FFFFFFFll || nrhs <= 0 || nrhs > 65535 || ldo < s || ldx < 0 ||
       col_offset < 0 || col_offset + N > 0x7FFFFFFFll)
@@ -893,9 +1057,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
   cudaStream_t st = (cudaStream_t)stream;
   // max_nnz: the caller's x arrays hold at most min(ldx, s) entries (x is an H_s output)
   const int32_t max_nnz = ldx < s ? ldx : s;
-  static int multi_env = -1;                         // profiling override: IHT_THR_MULTI=1 forces T1-T3
-  if (multi_env < 0) multi_env = getenv("IHT_THR_MULTI") ? atoi(getenv("IHT_THR_MULTI")) : 0;
-  if (N <= kClusterMaxN && nrhs <= 65535 && !(multi_env && nparts == 0)) {
+  if (!thr_grid_path(N, nrhs)) {
     int CL = 1;
     while ((int64_t)CL * kClusterSlice < N) CL *= 2;
     // spread small problems too: up to ~2 CTAs per SM while slices stay >= 4096 a-values
@@ -940,15 +1102,15 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
   }
   ThrWs w{};
   thr_ws_layout(N, nrhs, static_cast<char*>(ws), &w);
-  IHT_CUDA_CHECK(cudaMemsetAsync(ws, 0, nrhs * thr_hdr_bytes(), st));
+  // the histogram + flags header is zero on entry: T3 zeroes it for the next call; a cold
+  // workspace (standalone calls) is zeroed here
+  if (!ws_prezeroed) IHT_CUDA_CHECK(cudaMemsetAsync(ws, 0, nrhs * thr_hdr_bytes(), st));
   const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
-  thr_update_hist<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev,
-                                                              N, col_offset, w);
-  IHT_LAUNCH_CHECK();
-  thr_candidates<<<dim3(tiles, nrhs), kTileThreads, 0, st>>>(s, N, col_offset, w);
-  IHT_LAUNCH_CHECK();
-  thr_select<<<nrhs, kThrThreads, kCandCap * 8, st>>>(x_nnz, s, N, col_offset, w, out_idx, out_val, ldo, out_nnz);
-  IHT_LAUNCH_CHECK();
+  IHT_CUDA_CHECK(launch_pdl(thr_update_hist, dim3(tiles, nrhs), dim3(kTileThreads), 0, st, x_idx, x_val, x_nnz,
+                            max_nnz, ldx, g, mu, mu_dev, N, col_offset, w, nparts, gsigma, gout));
+  IHT_CUDA_CHECK(launch_pdl(thr_candidates, dim3(tiles, nrhs), dim3(kTileThreads), 0, st, s, N, col_offset, w));
+  IHT_CUDA_CHECK(launch_pdl(thr_select, dim3(nrhs), dim3(kThrThreads), (size_t)kCandCap * 8, st, x_nnz, s, N,
+                            col_offset, w, out_idx, out_val, ldo, out_nnz));
   return IHT_OK;
 }
 
@@ -956,11 +1118,11 @@ extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, c
                                      const float* g, float mu, int32_t s, int64_t N, int64_t col_offset,
                                      int32_t nrhs, int32_t* out_idx, float* out_val, int32_t ldo,
                                      int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream) {
-  return iht_threshold_batched_mu(x_idx, x_val, x_nnz, ldx, g, mu, nullptr, s, N, col_offset, nrhs, out_idx, out_val,
-                                  ldo, out_nnz, ws, ws_bytes, stream);
+  return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, nullptr, s, N, col_offset, nrhs, out_idx,
+                        out_val, ldo, out_nnz, ws, ws_bytes, stream, false);   // caller's (cold) workspace
 }
 
-int iht_threshold_launches(int64_t N) { return N <= kClusterMaxN ? 1 : 3; }
+int iht_threshold_launches(int64_t N) { return thr_grid_path(N, 1) ? 3 : 1; }
 
 extern "C" int iht_threshold(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz,
                              const float* g, float mu, int32_t s, int64_t N, int32_t* out_idx,

@@ -183,7 +183,8 @@ def _a32(x_idx, x_val, g, mu):
 @pytest.mark.parametrize("N,s", [(1024, 16), (16384, 128), (262144, 1024), (1001, 37), (5, 3), (1, 1),
                                  (100, 100), (100, 150), (3000, 0), (131073, 64), (262145, 1024),   # fused cluster
                                  (262144, 5000), (20000, 4500),        # fused, > 4096 candidates: per-pass path
-                                 (300000, 100), (300000, 7000)])                                   # multi-kernel
+                                 (300000, 100), (300000, 7000),                                    # grid path
+                                 (131072, 1024), (200000, 3000), (262144, 1)])                     # grid path
 def test_threshold_exact_selection(N, s):
     """Selection on identical fp32 a is exact: GPU H_s = oracle H_s of the same a."""
     rng = np.random.default_rng(N + s)
@@ -210,6 +211,15 @@ def test_threshold_ties_and_zeros():
     many = np.full(70000, 0.5, np.float32)                           # massive tie
     idx, _ = _thr([], [], many, 1.0, 1000)
     assert idx.tolist() == list(range(1000))
+    many = np.full(262144, 0.5, np.float32)                          # massive tie on the grid path
+    idx, _ = _thr([], [], many, 1.0, 1000)
+    assert idx.tolist() == list(range(1000))
+    crowd = np.full(262144, 0.01, np.float32)                        # a crowded bin just below the top
+    crowd[::3] = 0.75
+    crowd[::3000] = 1.0
+    idx, _ = _thr([], [], crowd, 1.0, 500)
+    ri, _ = OI.hard_threshold(crowd.astype(np.float64), 500)
+    assert idx.tolist() == ri.tolist()
 
 
 @pytest.mark.parametrize("N", [16384, 65536, 262144])
@@ -229,8 +239,9 @@ def test_threshold_ties_across_cluster(N):
     assert sorted(big.tolist() + rest) == idx.tolist()
 
 
-def test_threshold_nan_domain_error():
-    g = np.ones(1000, np.float32)
+@pytest.mark.parametrize("N", [1000, 262144])
+def test_threshold_nan_domain_error(N):
+    g = np.ones(N, np.float32)
     g[10] = np.nan
     idx, _ = _thr([], [], g, 1.0, 4)
     assert idx is None
@@ -259,6 +270,8 @@ CASES = {
     # 3 K-ranges of the int8-MMA adjoint: the solver sums the split-K partials inside the
     # fused threshold (no reduce kernel)
     "splitk": lambda: G.gaussian_problem(2100, 4096, 20, cfg_id=24, b_phi=4, n_iter=15, mu=0.6, K=30),
+    # N >= 131072: H_s on the grid path (T1 - T3 over every SM) inside the solver graph
+    "gridsel": lambda: G.gaussian_problem(512, 140000, 24, cfg_id=25, b_phi=4, n_iter=10, mu=0.5, K=20),
 }
 
 
