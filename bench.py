@@ -77,6 +77,14 @@ def measured_tensor_peak_int8():
         return 4500.0, "nominal"
 
 
+# NEXT-2 ALU roofline constants: thread-instructions
+# per real component in adjoint_fresh_kernel's main-loop body (SASS: 594 per 4 rows x 4
+# columns at P = 1, 1155 per 4 x 4 x 2 at P = 2; checked against the built object by
+# tests/test_abi.py), and the issue width: 148 SMs x 4 schedulers x 32 lanes per clock.
+FRESH_INST_PER_COMPONENT = {1: 594 / 16, 2: 1155 / 32}
+ALU_ISSUE_LANES = 148 * 4 * 32
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -531,6 +539,23 @@ def main():
                 "how": "CUDA event pair around every batched adjoint (limb prep + tcgen05 GEMM) inside a "
                        "profiled copy of the solver graph (run after the timed region); ops = 2 R N B useful (x2 executed: two int8 limbs of r)"}
 
+    fresh_roof = None
+    if args.fresh:  # NEXT-2: Philox + Q-contract per component: bound by instruction issue, not HBM
+        comps = rows * ncols * p.planes
+        ipc = FRESH_INST_PER_COMPONENT[p.planes]
+        fmax = (clocks or {}).get("sm_max_mhz") or 1965.0
+        ipeak = ALU_ISSUE_LANES * fmax * 1e6 / 1e12                  # thread-instructions / s, in T
+        ach = comps * ipc / (adj_avg / 1e3) / 1e12
+        fresh_roof = {"bound": "alu", "kernel": "adjoint_fresh_kernel (fp32 Phi + Philox4x32-10 + Q-contract, NEXT-2)",
+                      "achieved": ach, "peak": ipeak, "unit": "Tinst/s", "frac": ach / ipeak,
+                      "peak_kind": f"derived: 148 SMs x 4 schedulers x 32 lanes x {fmax:.0f} MHz (sm_max)",
+                      "instructions_per_component": ipc, "components_per_launch": comps,
+                      "hbm_GBps": adj_gbs, "hbm_frac": adj_gbs / peak,
+                      "traffic": traffic, "avg_launch_ms": adj_avg, "launches_timed": len(adj_ms),
+                      "how": "CUDA event pair around every fresh adjoint (kernel + fixed-order split reduce) inside a "
+                             "profiled copy of the solver graph; achieved = components x SASS instructions per "
+                             "component (main-loop body, DESIGN.md) / launch time"}
+
     fused = sol.fused
     fused_roof = None
     if fused:   # the whole loop is one persistent kernel: its roofline is the iteration's bytes
@@ -570,7 +595,7 @@ def main():
                       f"on both sides, max over ranks); median region reported"}),
         "hbm": {"phi_stream_GBps_per_gpu": stream_gbs, "frac_of_measured": stream_gbs / peak,
                 "frac_of_8TBps": stream_gbs / 8000.0, "bytes_per_iter_per_gpu": iter_bytes},
-        "roofline": roof if B > 1 else fused_roof if fused else
+        "roofline": roof if B > 1 else fused_roof if fused else fresh_roof if args.fresh else
                     {"bound": "hbm", "kernel": "adjoint_fresh_kernel (fp32 Phi + Philox, NEXT-2)" if args.fresh else
                                "adjoint_mma_kernel" if args.variant == 0 else "adjoint_ffma_kernel",
                      "achieved": adj_gbs, "peak": peak, "unit": "GB/s", "frac": adj_gbs / peak,

@@ -137,11 +137,42 @@ __global__ void __launch_bounds__(kFrThreads) forward_fresh_kernel(
   }
 }
 
-static int fresh_splits(int64_t rows, int64_t cols, int sms) {
+// Row splits: the grid is colblocks x splits CTAs of equal work, so it runs in
+// ceil(CTAs / resident) waves; pick the fewest splits whose last wave is >= 97 % full
+// (config 4: 256 column blocks x 3 splits had been 1.04 waves of 740 resident CTAs, i.e.
+// the time of two), at least 64 rows per split.  Deterministic for a given device.
+template <int P>
+static int fresh_resident(int sms) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, adjoint_fresh_kernel<P>, kFrThreads, 0) != cudaSuccess ||
+        nb < 1) {
+      (void)cudaGetLastError();
+      nb = 1;
+    }
+    per_sm = nb;
+  }
+  return per_sm * sms;
+}
+
+static int fresh_splits(int64_t rows, int64_t cols, int planes, int sms) {
   const int64_t colblocks = (cols + 4 * kFrThreads - 1) / (4 * kFrThreads);
-  int64_t splits = (4 * (int64_t)sms + colblocks - 1) / colblocks;   // >= ~4 CTAs per SM
-  splits = max64(1, min64(splits, (rows + 255) / 256));
-  return (int)min64(splits, 1024);
+  const int64_t cap = planes == 1 ? fresh_resident<1>(sms) : fresh_resident<2>(sms);
+  const int64_t smax = max64(1, min64(1024, rows / 64));
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t total = colblocks * sp;
+    const int64_t waves = (total + cap - 1) / cap;
+    const double eff = (double)total / (double)(waves * cap);
+    if (eff >= 0.97) return (int)sp;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return (int)best;
 }
 
 static bool fmat_valid(const iht_fmat* F) {
@@ -159,7 +190,7 @@ extern "C" int64_t iht_adjoint_fresh_ws_bytes(const iht_fmat* F) {
   if (!fmat_valid(F)) return -1;
   int dev = 0, sms = kNumSMs;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return (int64_t)fresh_splits(F->rows, F->cols, sms) * F->cols * 4;
+  return (int64_t)fresh_splits(F->rows, F->cols, F->planes, sms) * F->cols * 4;
 }
 
 extern "C" int iht_adjoint_fresh(const iht_fmat* F, int32_t copy_id, const float* r, float* g, void* ws,
@@ -168,7 +199,7 @@ extern "C" int iht_adjoint_fresh(const iht_fmat* F, int32_t copy_id, const float
   int dev = 0, sms = kNumSMs;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int splits = fresh_splits(F->rows, F->cols, sms);
+  const int splits = fresh_splits(F->rows, F->cols, F->planes, sms);
   if (ws == nullptr || ws_bytes < (int64_t)splits * F->cols * 4) return IHT_EINVAL;
   const int L = num_levels(F->bits, F->level_mode);
   FreshArgs a{};

@@ -79,3 +79,43 @@ def test_host_side_validation_without_gpu(lib):
     big = _lib.IhtQmat(rows=1 << 20, cols=64, planes=2, bits=8, strip_bytes=2 * (1 << 20), codes=16)
     assert lib.iht_adjoint_batched(ctypes.byref(big), c(16), 8, c(16), c(16), 1 << 40, c(0)) == \
         _lib.IHT_EUNSUPPORTED                                                          # int32 accumulator bound
+
+
+def _loop_bodies(obj, kernel_substr):
+    """Instruction counts of the backward-branch loop bodies of the kernels whose mangled name
+    contains kernel_substr, from cuobjdump -sass of the built object."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-sass", obj], capture_output=True, text=True).stdout
+    res = {}
+    for f in re.split(r"\n\s*Function : ", out)[1:]:
+        name = f.split("\n")[0].strip()
+        if kernel_substr not in name:
+            continue
+        ins = [(int(m.group(1), 16), m.group(2)) for m in
+               (re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", l) for l in f.split("\n")) if m]
+        for a, t in ins:
+            tgt = re.search(r"BRA(?:\.\w+)?\s.*?0x([0-9a-f]+)", t)
+            if tgt and int(tgt.group(1), 16) < a:
+                res.setdefault(name, []).append(sum(1 for x, _ in ins if int(tgt.group(1), 16) <= x <= a))
+    return res
+
+
+def test_fresh_alu_roofline_constants_match_sass():
+    """bench.py's NEXT-2 ALU roofline uses the SASS instruction count of adjoint_fresh_kernel's
+    main loop per component; it must describe the library as built."""
+    import importlib.util
+    obj = os.path.join(ROOT, "paper_1802_04907_b200", "_build", "iht_fresh.o")
+    if not os.path.exists(obj):
+        from paper_1802_04907_b200 import build
+        build.build(verbose=False)
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    bodies = _loop_bodies(obj, "adjoint_fresh_kernel")
+    for planes, comps in ((1, 16), (2, 32)):
+        name = [n for n in bodies if f"adjoint_fresh_kernelILi{planes}E" in n]
+        assert name, bodies.keys()
+        body = max(bodies[name[0]])                     # the unrolled 4-row main loop
+        assert abs(body / comps - bench.FRESH_INST_PER_COMPONENT[planes]) <= 0.03 * body / comps, (planes, body)
