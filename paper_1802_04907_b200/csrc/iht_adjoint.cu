@@ -381,7 +381,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
             request(slot);                       // refill it with the request kRing later
           }
 #pragma unroll
-          for (int u = 0; u < NMMA; ++u) mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
+          for (int i = 0; i < NMMA; ++i) {   // consecutive MMAs update different accumulators
+            const int u = (i % P) * 2 + i / P;
+            mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
+          }
         };
         if (ks0 + kReq <= nsteps) {              // whole request (all but a task's last, or all)
 #pragma unroll

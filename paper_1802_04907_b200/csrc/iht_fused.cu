@@ -73,6 +73,8 @@ struct FusedArgs {
   long long* tl;                       // profiling (IHT_FUSED_TL): [64][16] globaltimer stamps of CTA tl_cta
   int tl_cta;
   int probe;                           // profiling (IHT_FUSED_PROBE): 1 no MMA work, 2 no refills inside A, 4 no flush
+  int nobound;                         // IHT_FUSED_NOBOUND=1: never take the bounded-candidate path (same results)
+  float bound_frac;                    // bound = bound_frac x the previous threshold (IHT_FUSED_BOUND, default 0.9)
 };
 
 __device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t parity) {
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
   __shared__ float part[kFuWarps][kFuMaxWpc][CPW];
   __shared__ int s_nnz, s_flag, s_nonfinite, s_total, s_base[2];
   __shared__ unsigned int s_cmax;
+  __shared__ float s_min[kFuWarps];
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t ring_u = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t full_u = (uint32_t)__cvta_generic_to_shared(smem + a.off_bars);
@@ -200,9 +203,9 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
 
   const uint32_t limb_n = (uint32_t)__cvta_generic_to_shared(limbs + (g8 < 3 ? g8 : 0) * a.limb_stride);
   const bool bload = g8 < 3;
-  uint32_t bw[4 * P];
+  uint32_t bw[4 * P], bw2[4 * P];      // B fragments (two sets: the A phase's ping-pong); zero on lanes g8 >= 3
 #pragma unroll
-  for (int q = 0; q < 4 * P; ++q) bw[q] = 0u;
+  for (int q = 0; q < 4 * P; ++q) bw[q] = bw2[q] = 0u;
   const unsigned int lt = (1u << lane) - 1u;
   int consumed = 0;                                               // blocks this warp consumed
   int c_slot = 0;                                                 // consumer cursor: slot, use parity
@@ -217,9 +220,57 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       if (a.tl_cta < 0 && n == 3) a.tl[cta * 16 + k] = tt;     // every CTA, iteration 3
     }
   };
+  // ordered compaction of this CTA's columns whose key passes `pred` into its candidate slot
+  // (index order), count to cand_cnt[cta]
+  auto write_cands = [&](auto pred) {
+    int base = 0;
+    for (int q0 = 0; q0 < ncol; q0 += kFuThreads) {
+      const int q = q0 + tid;
+      const float v = q < ncol ? as[q] : 0.0f;
+      const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
+      const bool f = q < ncol && key > 0u && pred(key);
+      const unsigned int bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wgt[warp] = __popc(bal);
+      __syncthreads();
+      int off = base, tot = 0;
+      for (int w = 0; w < kFuWarps; ++w) {
+        if (w < warp) off += wgt[w];
+        tot += wgt[w];
+      }
+      if (f) {
+        const int pos = off + __popc(bal & lt);
+        IHT_DCHECK(pos < a.cap_c, "fused: candidate inside the CTA's slot");
+        a.cand_idx[(int64_t)cta * a.cap_c + pos] = col_lo + q;
+        a.cand_val[(int64_t)cta * a.cap_c + pos] = v;
+      }
+      base += tot;
+      __syncthreads();
+    }
+    if (tid == 0) a.cand_cnt[cta] = base;
+  };
   for (int n = 1; n <= a.n_iter; ++n) {
     const int par = n & 1;
     stamp(n, 0);
+    // Bounded candidates: bkey = the key of half the smallest kept |x^[n]| (the previous
+    // threshold), or 0.  Before barrier 2 every CTA writes its keys >= bkey as candidates;
+    // after it, if bin d1 (the s-th largest key's) lies at or above bkey, the candidates hold
+    // every key with digit >= d1 -- a superset of the top s -- and S1 with its barrier is
+    // skipped (exact: S2 keeps digits > d1, ranks digit d1, drops the rest).  Otherwise S1
+    // rewrites the candidates as before.  Same decision on every CTA (same x, same histogram).
+    unsigned int bkey = 0u;
+    {
+      float mn = __int_as_float(0x7F800000);
+      for (int j = tid; j < s_nnz; j += kFuThreads) mn = fminf(mn, fabsf(xv_s[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      if (lane == 0) s_min[warp] = mn;
+      __syncthreads();
+      mn = s_min[0];
+#pragma unroll
+      for (int w = 1; w < kFuWarps; ++w) mn = fminf(mn, s_min[w]);
+      if (!a.nobound && n >= 2 && a.s > 0 && a.s < a.N && s_nnz == a.s && mn > 0.0f && mn < 3.0e38f)
+        bkey = __float_as_uint(__fmul_rn(a.bound_frac, mn)) & 0x7FFFFFFFu;
+    }
     // ================================================================ F: forward
     {
       const int w0 = cta * a.wpc;
@@ -412,6 +463,34 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         }
       };
       const int KSB = KS / a.nsub;                                // k-steps per block
+      constexpr int KPC = kFuKC / KSTEP;                          // k-steps per fixed-point chunk
+      const bool probe_nomma = (a.probe & 1) != 0;
+      const uint32_t lane_off = g8 * 64 + t * 16;
+      auto kstep_mma = [&](const uint4& w0, const uint4& w1, const uint32_t* b) {
+        uint32_t af[NMMA][4];
+#pragma unroll
+        for (int jj = 0; jj < P; ++jj)
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            af[2 * jj + m][0] = frag_reg<B>(w0, 2 * m, jj);
+            af[2 * jj + m][1] = frag_reg<B>(w1, 2 * m, jj);
+            af[2 * jj + m][2] = frag_reg<B>(w0, 2 * m + 1, jj);
+            af[2 * jj + m][3] = frag_reg<B>(w1, 2 * m + 1, jj);
+          }
+#pragma unroll
+        for (int i = 0; i < NMMA; ++i) {   // consecutive MMAs update different accumulators
+          const int u = (i % P) * 2 + i / P;
+          mma_u8s8(acc[u >> 1], af[u], b[2 * u], b[2 * u + 1]);
+        }
+      };
+      auto load_b = [&](int ks, uint32_t* dst) {                  // r limbs of k-step ks (lanes g8 < 3)
+        const uint32_t bp = limb_n + (uint32_t)ks * (64 * P) + t * 16;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {                             // 12 lanes hit 3 x 4 distinct bank quads
+          const uint4 v = lds128(bp + 64 * q);
+          dst[4 * q + 0] = v.x; dst[4 * q + 1] = v.y; dst[4 * q + 2] = v.z; dst[4 * q + 3] = v.w;
+        }
+      };
       // probe 8: no cross-iteration prefetch (each warp streams its tiles during its own A)
       const int rq_cap = (a.probe & 8) ? n * Bw : total_w;
       if (lane == 0) request(min(consumed + a.mslot, rq_cap));
@@ -422,35 +501,39 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
           mbar_wait(wfull + 8 * c_slot, c_par);
           if (k == 0 && h == 0) stamp(n, 11);
           const uint32_t sbase = wring + (uint32_t)c_slot * a.block_bytes;
-          for (int kk = 0; kk < KSB && !(a.probe & 1); ++kk) {
-            const int ks = h * KSB + kk;
-            const int seg = j * a.nchunks + (ks * KSTEP) / kFuKC;
+          // the block's k-steps in runs that stay inside one fixed-point chunk (the flush
+          // decision is taken once per run, not per k-step), each run software-pipelined:
+          // the shared loads of k-step r+1 are issued before the MMAs of k-step r (the asm
+          // statements keep source order, so the order here is the issue order)
+          int kk = probe_nomma ? KSB : 0;
+          while (kk < KSB) {
+            const int ks0 = h * KSB + kk;
+            const int seg = j * a.nchunks + ks0 / KPC;
             if (seg != cur_seg) {
               flush();
               cur_seg = seg;
             }
-            const uint32_t src = sbase + kk * 1024 + g8 * 64 + t * 16;
-            const uint4 s0 = lds128(src), s1 = lds128(src + 512);
-            if (bload) {
-              const uint32_t bp = limb_n + (uint32_t)ks * (64 * P) + t * 16;
-#pragma unroll
-              for (int q = 0; q < P; ++q) {                       // 12 lanes hit 3 x 4 distinct bank quads
-                const uint4 v = lds128(bp + 64 * q);
-                bw[4 * q + 0] = v.x; bw[4 * q + 1] = v.y; bw[4 * q + 2] = v.z; bw[4 * q + 3] = v.w;
+            const int run = min(KSB - kk, KPC - ks0 % KPC);
+            // two register sets (ping-pong, no copies): set A = (c0, c1, bw), set B = (n0, n1, bw2)
+            uint4 c0 = lds128(sbase + kk * 1024 + lane_off), c1 = lds128(sbase + kk * 1024 + lane_off + 512);
+            uint4 n0 = c0, n1 = c1;
+            if (bload) load_b(ks0, bw);
+            for (int r = 0; r < run; r += 2) {
+              if (r + 1 < run) {
+                n0 = lds128(sbase + (kk + r + 1) * 1024 + lane_off);
+                n1 = lds128(sbase + (kk + r + 1) * 1024 + lane_off + 512);
+                if (bload) load_b(ks0 + r + 1, bw2);
               }
+              kstep_mma(c0, c1, bw);
+              if (r + 1 >= run) break;
+              if (r + 2 < run) {
+                c0 = lds128(sbase + (kk + r + 2) * 1024 + lane_off);
+                c1 = lds128(sbase + (kk + r + 2) * 1024 + lane_off + 512);
+                if (bload) load_b(ks0 + r + 2, bw);
+              }
+              kstep_mma(n0, n1, bw2);
             }
-            uint32_t af[NMMA][4];
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj)
-#pragma unroll
-              for (int m = 0; m < 2; ++m) {
-                af[2 * jj + m][0] = frag_reg<B>(s0, 2 * m, jj);
-                af[2 * jj + m][1] = frag_reg<B>(s1, 2 * m, jj);
-                af[2 * jj + m][2] = frag_reg<B>(s0, 2 * m + 1, jj);
-                af[2 * jj + m][3] = frag_reg<B>(s1, 2 * m + 1, jj);
-              }
-#pragma unroll
-            for (int u = 0; u < NMMA; ++u) mma_u8s8(acc[u >> 1], af[u], bw[2 * u], bw[2 * u + 1]);
+            kk += run;
           }
           __syncwarp();                                           // every lane has read the slot
           ++consumed;
@@ -503,6 +586,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       }
       if (tid == 0 && nan) atomicOr(&a.flags[par], 1);
     }
+    if (bkey) write_cands([&](unsigned int key) { return key >= bkey; });
     stamp(n, 5);
     grid_sync();                                                  // ---- barrier 2: histogram complete
     stamp(n, 6);
@@ -529,35 +613,21 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       d1 = (unsigned int)sh[0];
       above = sh[1];
     }
-    {
-      int base = 0;
-      for (int q0 = 0; q0 < ncol; q0 += kFuThreads) {
-        const int q = q0 + tid;
-        const float v = q < ncol ? as[q] : 0.0f;
-        const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
-        const bool f = q < ncol && key > 0u && (all || (key >> 20) >= d1);
-        const unsigned int bal = __ballot_sync(0xffffffffu, f);
-        if (lane == 0) wgt[warp] = __popc(bal);
-        __syncthreads();
-        int off = base, tot = 0;
-        for (int w = 0; w < kFuWarps; ++w) {
-          if (w < warp) off += wgt[w];
-          tot += wgt[w];
-        }
-        if (f) {
-          const int pos = off + __popc(bal & lt);
-          IHT_DCHECK(pos < a.cap_c, "fused: candidate inside the CTA's slot");
-          a.cand_idx[(int64_t)cta * a.cap_c + pos] = col_lo + q;
-          a.cand_val[(int64_t)cta * a.cap_c + pos] = v;
-        }
-        base += tot;
-        __syncthreads();
-      }
-      if (tid == 0) a.cand_cnt[cta] = base;
+    int* cnt_s = sel_hist;                                        // [G + 1] candidate offsets (S2)
+    bool fast = false;
+    if (bkey && !all && !s_flag && a.s > 0 && bkey <= (d1 << 20)) {
+      for (int c = tid; c < G; c += kFuThreads) cnt_s[c] = __ldcg(&a.cand_cnt[c]);
+      __syncthreads();
+      int tot = 0;
+      for (int c = lane; c < G; c += 32) tot += cnt_s[c];
+      tot = __reduce_add_sync(0xffffffffu, tot);
+      fast = tot <= kFuCandCap;                                   // same on every CTA
+      __syncthreads();
     }
+    if (!fast) write_cands([&](unsigned int key) { return all || (key >> 20) >= d1; });
     (void)above;
     stamp(n, 7);
-    grid_sync();                                                  // ---- barrier 3: candidates complete
+    if (!fast) grid_sync();                                       // ---- barrier 3: candidates complete
     stamp(n, 8);
     // ================================================================ S2: exact top-s
     const int slot_out = a.trace ? n : (n & 1);
@@ -568,19 +638,28 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       break;
     }
     // candidate counts -> offsets (CTA order = increasing column index)
-    int* cnt_s = sel_hist;                                        // [G + 1] candidate offsets
     int* hsel = sel_hist + ((G + 4) & ~3);                        // [2048] select_ordered's histogram
-    for (int c = tid; c < G; c += kFuThreads) cnt_s[c] = __ldcg(&a.cand_cnt[c]);
-    __syncthreads();
-    if (tid == 0) {
-      int acc2 = 0;
-      for (int c = 0; c < G; ++c) {
-        const int v = cnt_s[c];
-        cnt_s[c] = acc2;
-        acc2 += v;
+    if (!fast) {                                                  // (the fast path loaded them above)
+      for (int c = tid; c < G; c += kFuThreads) cnt_s[c] = __ldcg(&a.cand_cnt[c]);
+      __syncthreads();
+    }
+    if (warp == 0) {                                              // exclusive scan, 32 CTAs per step
+      int carry = 0;
+      for (int c0 = 0; c0 < G; c0 += 32) {
+        const int v = c0 + lane < G ? cnt_s[c0 + lane] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (c0 + lane < G) cnt_s[c0 + lane] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
       }
-      cnt_s[G] = acc2;
-      s_total = acc2;
+      if (lane == 0) {
+        cnt_s[G] = carry;
+        s_total = carry;
+      }
     }
     __syncthreads();
     const int C = s_total;
@@ -904,6 +983,8 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   A.xs_nnz = xs_nnz;
   A.trace = trace;
   A.probe = getenv("IHT_FUSED_PROBE") ? atoi(getenv("IHT_FUSED_PROBE")) : 0;   // profiling only
+  A.nobound = getenv("IHT_FUSED_NOBOUND") ? atoi(getenv("IHT_FUSED_NOBOUND")) : 0;
+  A.bound_frac = getenv("IHT_FUSED_BOUND") ? (float)atof(getenv("IHT_FUSED_BOUND")) : 0.9f;
   if (getenv("IHT_FUSED_TL")) {        // profiling only: per-phase globaltimer stamps of one CTA
     A.tl_cta = atoi(getenv("IHT_FUSED_TL"));
     if (A.tl_cta >= G) A.tl_cta = 0;
@@ -986,6 +1067,9 @@ void iht_fused_destroy(iht_fused_state* S) {
       std::sort(d.begin(), d.end());
       fprintf(stderr, " a%d %lld", k - 10, d.empty() ? -1 : d[d.size() / 2]);
     }
+    int skipped = 0;                                 // bounded-candidate iterations (no S1 / barrier 3)
+    for (int n = 0; n < nit; ++n) skipped += h[n * 16 + 8] - h[n * 16 + 7] < 300;
+    fprintf(stderr, " | B3 skipped %d/%d", skipped, nit);
     std::vector<long long> it;
     for (int n = 1; n < nit; ++n) it.push_back(h[n * 16] - h[(n - 1) * 16]);
     std::sort(it.begin(), it.end());

@@ -2,7 +2,8 @@
 // 2 LDS.128 of codes, 4 LDS.128 of r limbs (3 of 8 lane groups), 32 in-place mask LOP3s,
 // 8 IMMA.16832.U8.S8 -- per warp, 8 warps per SM, operands in shared memory.  Variants isolate
 // the parts: 0 full k-step; 1 no LDS (masks of loop-carried registers); 2 no LOP (IMMA on the
-// loaded words directly); 3 IMMA only on constant operands (the peak); 4 full, 8 accumulators.
+// loaded words directly); 3 IMMA only on constant operands (the peak); 4 full, 8 accumulators;
+// 5 full, MMAs ordered so that consecutive ones update different accumulators.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o kstep_bench kstep_bench.cu
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -74,7 +75,10 @@ __global__ void __launch_bounds__(256, 1) kstep(int iters, long long* cyc, int* 
         }
       }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) mma_u8s8(acc[NACC == 8 ? u : (u >> 1)], af[u], bw[2 * u], bw[2 * u + 1]);
+    for (int i = 0; i < 8; ++i) {
+      const int u = VAR == 5 ? (i % 4) * 2 + i / 4 : i;   // 5: consecutive MMAs on different accumulators
+      mma_u8s8(acc[NACC == 8 ? u : (u >> 1)], af[u], bw[2 * u], bw[2 * u + 1]);
+    }
   }
   const long long t1 = clock64();
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
@@ -110,5 +114,6 @@ int main() {
   run<2>("no LOP (IMMA on loaded words)");
   run<3>("IMMA only, constant operands");
   run<4>("full k-step, 8 accumulators");
+  run<5>("full k-step, MMA order interleaving the 4 accumulators");
   return 0;
 }

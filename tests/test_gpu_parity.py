@@ -5,6 +5,8 @@ per iteration; supports identical whenever the oracle's margin at the s-th
 position exceeds 1e-5 |a|_(s) (otherwise logged as a near-tie).  Shapes span
 several tiles with ragged tails; edge cases cover empty/degenerate inputs.
 """
+import re
+
 import numpy as np
 import pytest
 import torch
@@ -338,6 +340,37 @@ def test_free_running_solver(case, graph, fused):
         assert fi[:k].cpu().numpy().tolist() == ref.x_idx.tolist()
         assert rel_l2(fv[:k].cpu().numpy(), ref.x_val, floor=1e-30) < TOL
     sol.close()
+
+
+@pytest.mark.parametrize("case", ["config1", "gauss2bit", "radio", "gauss8bit", "splitk"])
+def test_fused_bounded_candidates_bit_identical(case, capfd, monkeypatch):
+    """The fused solver's bounded-candidate select (candidates = keys >= half the previous
+    threshold, written before barrier 2; S1 and barrier 3 skipped when bin d1 lies above the
+    bound) is exact: every iterate is bit-identical to the unbounded path (IHT_FUSED_NOBOUND=1),
+    and the bounded path is actually taken (phase timeline: barrier 3 skipped)."""
+    p = CASES[case]()
+    n_iter = min(p.n_iter, 40)
+    c = OQ.scale_c(p.phi)
+    pool = _pool(p.phi, p.b_phi, min(p.K, 2 * n_iter), c, p.seed)
+    y = _to_dev(p.y)
+    runs = []
+    for env in ({"IHT_FUSED_NOBOUND": "1"}, {"IHT_FUSED_TL": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, fused="force")
+        assert sol.fused
+        sol.run(y)
+        torch.cuda.synchronize()
+        runs.append(tuple(t.clone() for t in sol.trace_arrays()))
+        sol.close()
+        for k in env:
+            monkeypatch.delenv(k)
+    for a, b in zip(runs[0], runs[1]):
+        assert torch.equal(a, b)
+    err = capfd.readouterr().err
+    m = re.search(r"B3 skipped (\d+)/(\d+)", err)
+    assert m, err[-2000:]
+    assert int(m.group(1)) >= 1, f"bounded path never taken: {m.group(0)}"
 
 
 def test_solver_host_io_and_determinism():
