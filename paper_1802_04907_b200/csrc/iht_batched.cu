@@ -78,6 +78,18 @@ __device__ __forceinline__ void mbar_wait2(uint32_t mbar, uint32_t parity) {
       : "memory");
 #endif
 }
+// non-blocking probe of an mbarrier phase (1 when the phase with `parity` has completed)
+__device__ __forceinline__ uint32_t mbar_test2(uint32_t mbar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(mbar), "r"(parity)
+      : "memory");
+  return ok;
+}
 __device__ __forceinline__ void bulk_g2s2(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(mbar)
@@ -301,9 +313,20 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     (void)CH;
   } else if (warp == 4) {
     // ---------------------------------------------------------------- MMA issuer
+    // The tensor pipe queues only a few MMAs, so every instruction on the issuing thread's
+    // path between K-blocks is exposed (scripts/microbench/tc2_bench.cu: a try_wait on an
+    // already-completed phase per 16-MMA K-block costs ~5 clk per MMA).  So: the bases are
+    // made warp-uniform once, and halfway through K-block kb lane 0 probes (test_wait, non
+    // blocking) whether K-block kb+1's stage is already full -- then kb+1 starts without a
+    // wait; otherwise it waits as before.
     int ss = 0;
     uint32_t sph = 0;
     int t = 0;
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t sB_u = __shfl_sync(0xffffffffu, smem_u32(sB), 0);
+    const uint32_t full_u = __shfl_sync(0xffffffffu, smem_u32(&st_full[0]), 0);
+    const uint32_t free_u = __shfl_sync(0xffffffffu, smem_u32(&st_free[0]), 0);
+    const uint32_t nb128 = __shfl_sync(0xffffffffu, (uint32_t)NB * 128u, 0);
     for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++t) {
       const int ab = t & 1;
       const int half = u < a.nfull ? -1 : ((u - a.nfull) & 1);
@@ -314,40 +337,44 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
       if (t >= 2) mbar_wait2(smem_u32(&acc_free[ab]), (uint32_t)(((t - 2) >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t] = clock64();
-      const uint32_t dtm = tmem + ab * acc_stride;
+      const uint32_t dtm = tmem_u + ab * acc_stride;
+      uint32_t ready = 0;
       for (int kb = 0; kb < a.nkb; ++kb) {
-        if (!(a.probe & 64) || (t == 0 && kb < ST)) mbar_wait2(smem_u32(&st_full[ss]), sph);   // probe 64: first round only
+        if (!ready && (!(a.probe & 64) || (t == 0 && kb < ST))) mbar_wait2(full_u + 8 * ss, sph);   // probe 64: first round only
         if (a.tlog && lane == 0 && t == 0 && kb < 16) a.tlog[blockIdx.x * 64 + 40 + kb] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // warp-uniform operands (shuffled from lane 0 so the compiler keeps them uniform)
-        const uint32_t atm_u = __shfl_sync(0xffffffffu, tmem + a_col0 + (uint32_t)(ss * ACOLS), 0);
-        const uint32_t bbase_u = __shfl_sync(0xffffffffu, smem_u32(sB + ss * BSZ) + hoff, 0);
+        const int nss = ss + 1 == ST ? 0 : ss + 1;
+        const uint32_t nsph = ss + 1 == ST ? sph ^ 1u : sph;
+        // warp-uniform operands (shuffled from lane 0 so the compiler keeps them on uniform
+        // registers: no per-MMA R2UR broadcast loop)
+        const uint32_t bbase_u = __shfl_sync(0xffffffffu, sB_u + ss * BSZ + hoff, 0);
+        const uint32_t atm = __shfl_sync(0xffffffffu, tmem_u + a_col0 + (uint32_t)(ss * ACOLS), 0);
         const uint32_t dtm_u = __shfl_sync(0xffffffffu, dtm, 0);
         const uint32_t idesc_u = __shfl_sync(0xffffffffu, idesc, 0);
         const uint32_t acc0_u = __shfl_sync(0xffffffffu, kb > 0 ? 1u : 0u, 0);
-        const uint32_t nb128_u = __shfl_sync(0xffffffffu, (uint32_t)NB * 128u, 0);
+        const uint32_t nfull_u = __shfl_sync(0xffffffffu, full_u + 8 * nss, 0);
+        uint32_t peek = 0;
         if (lane == 0) {
           if (a.probe & 2) {                        // probe: no tensor work
-            mbar_arrive2(smem_u32(&st_free[ss]));
+            mbar_arrive2(free_u + 8 * ss);
             if (kb == a.nkb - 1) mbar_arrive2(smem_u32(&acc_full[ab]));
           } else {
-            // base descriptor / TMEM address once per K-block; the per-MMA K offsets are added
-            // to the descriptor's 14-bit start-address field (no carry: stages < 256 KiB), so
-            // the 16 issues stay on uniform registers instead of a broadcast per MMA
+            // base descriptor once per K-block; the per-MMA K offsets are added to the
+            // descriptor's 14-bit start-address field (no carry: stages < 256 KiB)
             const uint64_t bd0 = sw128_desc(bbase_u);
-            const uint32_t nb128 = nb128_u;
 #pragma unroll
             for (int kk = 0; kk < NKS; ++kk) {
+              if (kk == NKS / 2 && kb + 1 < a.nkb && !(a.probe & 64)) peek = mbar_test2(nfull_u, nsph);
               const uint64_t bd = bd0 + (uint64_t)(((uint32_t)(kk >> 2) * nb128 + (uint32_t)(kk & 3) * 32u) >> 4);
               const uint32_t acc = kk > 0 ? 1u : acc0_u;
               asm volatile(
                   "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                   "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtm_u),
-                  "r"(atm_u + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc_u), "r"(acc)
+                  "r"(atm + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc_u), "r"(acc)
                   : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(&st_free[ss]))
+                             free_u + 8 * ss)
                          : "memory");
             if (kb == a.nkb - 1)
               asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -355,8 +382,9 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                            : "memory");
           }
         }
-        __syncwarp();
-        if (++ss == ST) { ss = 0; sph ^= 1u; }
+        ready = __shfl_sync(0xffffffffu, peek, 0);
+        ss = nss;
+        sph = nsph;
       }
       if (a.tlog && lane == 0 && t < 16) a.tlog[blockIdx.x * 64 + 2 * t + 1] = clock64();
     }

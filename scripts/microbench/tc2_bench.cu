@@ -9,6 +9,12 @@
 //   D  cta_group::2, M = 256 (each CTA 128 lanes of A in its TMEM), B = 2 x 64 columns, one
 //      per CTA's shared memory, stepping like A; issued by the pair's leader
 //   E  D + C's TMEM-load warps in both CTAs
+//   F  A + a tcgen05.commit to a (never waited) mbarrier after every 16-MMA K-block
+//   G  F + tcgen05.fence::after_thread_sync before every K-block
+//   H  G with the kernel's issue loop: all 32 lanes run the K-block loop, operands broadcast
+//      with __shfl_sync, lane 0 issues, __syncwarp after every K-block
+//   I  H with the accumulator alternating between two TMEM buffers every 9 K-blocks (a tile)
+//   J  I + an mbarrier try_wait per K-block on a phase that has already completed (all lanes)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc2_bench tc2_bench.cu
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -75,7 +81,51 @@ __global__ void __launch_bounds__(256, 1) tc(int nkb, long long* cyc) {
   if (PAIR) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t bbase = su32(smem);
-  if (warp == 4) {
+  if (warp == 4 && MODE >= 5) {
+    __shared__ uint64_t kbar, rbar;
+    if (lane == 0) {
+      mbar_init(su32(&kbar), 1);
+      mbar_init(su32(&rbar), 1);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&rbar)) : "memory");   // phase 0 done
+    }
+    __syncwarp();
+    const long long t0 = clock64();
+    const uint32_t idesc = idesc_i8(128, 128);
+    for (int kb = 0; kb < nkb; ++kb) {
+      if (MODE >= 9) mbar_wait(su32(&rbar), 0);
+      if (MODE >= 6) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t st = bbase + (kb & 1) * (128 * 512), at = tmem + 256 + (uint32_t)((kb & 1) * 128);
+      uint32_t dt = tmem + (MODE >= 8 ? (uint32_t)(((kb / 9) & 1) * 128) : 0u);
+      if (MODE >= 7) {
+        st = __shfl_sync(0xffffffffu, st, 0);
+        at = __shfl_sync(0xffffffffu, at, 0);
+        dt = __shfl_sync(0xffffffffu, dt, 0);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < KPB; ++kk) {
+          const uint64_t bd = sw128_desc(st + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
+          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dt),
+                       "r"(at + (uint32_t)(kk * 8)), "l"(bd), "r"(idesc), "r"(acc)
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&kbar))
+                     : "memory");
+      }
+      if (MODE >= 7) __syncwarp();
+    }
+    if (lane == 0)
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&done))
+                   : "memory");
+    __syncwarp();
+    mbar_wait(su32(&done), 0);
+    if (lane == 0) {
+      cyc[blockIdx.x] = clock64() - t0;
+      stop = 1;
+    }
+  } else if (warp == 4) {
     const long long t0 = clock64();
     if (lane == 0 && rank == 0) {
       const uint32_t idesc = PAIR ? idesc_i8(256, 128) : idesc_i8(128, 128);
@@ -188,5 +238,10 @@ int main() {
   run<2>("C: A + epilogue-like TMEM loads (4 warps)", sms);
   run<3>("D: cta_group::2 M256 N128, A TMEM, B split over the pair", sms);
   run<4>("E: D + epilogue-like TMEM loads", sms);
+  run<5>("F: A + commit per K-block", sms);
+  run<6>("G: F + fence::after_thread_sync per K-block", sms);
+  run<7>("H: G + warp-wide loop, shfl operands, lane-0 issue, syncwarp", sms);
+  run<8>("I: H + accumulator alternating per 9 K-blocks", sms);
+  run<9>("J: I + try_wait on a completed phase per K-block", sms);
   return 0;
 }
