@@ -42,7 +42,8 @@ constexpr int kBThreads = 352;         // 11 warps (roles above)
 // TMEM columns left by the two accumulators; B stages take 128 KiB of shared memory.
 // Measured (in-kernel timeline probe, config 5): every K-block handoff costs the MMA pipe
 // ~300-400 clk whatever the depth, so fewer, larger K-blocks win: 2 stages x 16 MMAs ran
-// at 87 clk per MMA (MMA-only), 4 stages x 8 MMAs at 100, against 64 back to back.
+// at 87 clk per MMA (MMA-only), 4 stages x 8 MMAs at 100, against 64 back to back; r02
+// again with the current issuer: 8-MMA K-blocks at 2 bits 49.2 us per call against 41.7.
 template <int BITS> struct BCfg {
   static constexpr int TS = BITS == 8 ? 4 : BITS;       // tile-steps per K-block
   static constexpr int KBR = TS * 512 / BITS;           // rows (= u8 bytes per pixel row) per K-block
@@ -50,9 +51,9 @@ template <int BITS> struct BCfg {
   static constexpr int ACOLS = KBR / 4;                 // TMEM columns of one A stage
   static constexpr int STAGES = 256 / ACOLS;            // 2 (2/4-bit) or 4 (8-bit)
   static constexpr int PK = 8 * TS * 1024;              // packed bytes per K-block (8 column tiles)
-  static constexpr int PKSLOTS = PK <= 16384 ? 4 : 2;   // packed-code slots
+  static constexpr int PKSLOTS = PK <= 8192 ? 8 : (PK <= 16384 ? 4 : 2);   // packed-code slots
 };
-constexpr int kStagesMax = 4, kPkSlotsMax = 4;
+constexpr int kStagesMax = 4, kPkSlotsMax = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
