@@ -514,18 +514,17 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
               cur_seg = seg;
             }
             const int run = min(KSB - kk, KPC - ks0 % KPC);
-            // two register sets (ping-pong, no copies): set A = (c0, c1, bw), set B = (n0, n1, bw2)
+            // two register sets, set A = (c0, c1, bw), set B = (n0, n1, bw2), alternating
+            // without copies (a copy of a just-loaded register would wait for the load)
             uint4 c0 = lds128(sbase + kk * 1024 + lane_off), c1 = lds128(sbase + kk * 1024 + lane_off + 512);
-            uint4 n0 = c0, n1 = c1;
+            uint4 n0, n1;
             if (bload) load_b(ks0, bw);
-            for (int r = 0; r < run; r += 2) {
-              if (r + 1 < run) {
-                n0 = lds128(sbase + (kk + r + 1) * 1024 + lane_off);
-                n1 = lds128(sbase + (kk + r + 1) * 1024 + lane_off + 512);
-                if (bload) load_b(ks0 + r + 1, bw2);
-              }
+            int r = 0;
+            for (; r + 1 < run; r += 2) {
+              n0 = lds128(sbase + (kk + r + 1) * 1024 + lane_off);
+              n1 = lds128(sbase + (kk + r + 1) * 1024 + lane_off + 512);
+              if (bload) load_b(ks0 + r + 1, bw2);
               kstep_mma(c0, c1, bw);
-              if (r + 1 >= run) break;
               if (r + 2 < run) {
                 c0 = lds128(sbase + (kk + r + 2) * 1024 + lane_off);
                 c1 = lds128(sbase + (kk + r + 2) * 1024 + lane_off + 512);
@@ -533,6 +532,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
               }
               kstep_mma(n0, n1, bw2);
             }
+            if (r < run) kstep_mma(c0, c1, bw);                   // odd run: the last k-step
             kk += run;
           }
           __syncwarp();                                           // every lane has read the slot
