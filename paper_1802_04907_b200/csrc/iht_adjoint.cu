@@ -482,7 +482,7 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   while ((p.KRp / 1024) % d) --d;
   p.KC = 1024 * d;
   p.nK = (int)((Rpad + KR - 1) / KR);
-  p.limb_stride = p.KRp + 32;                          // limb planes 2 bank quads apart
+  p.limb_stride = p.KRp + 64;   // planes 64 B apart (mod 128): the 8 lanes of an LDS.128 phase (planes 0, 1) hit disjoint banks
   const int nchunks = p.KRp / p.KC;
   p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
            sizeof(float) * nchunks * kMmaWarps + 16;

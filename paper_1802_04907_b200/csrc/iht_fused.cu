@@ -53,7 +53,7 @@ struct FusedArgs {
   int s, n_iter;
   int ntiles, tile_bytes, nchunks, wpc, words_total, cap_c, s_cap;
   int nsub, block_bytes, mslot;        // ring: a tile = nsub blocks; each warp owns mslot block slots
-  int limb_stride;                     // bytes between the 3 limb planes (Rpad + 32: bank spread)
+  int limb_stride;                     // bytes between the 3 limb planes (Rpad + 64: bank spread)
   const float* yhat;                   // [Rpad] stacked, pads 0
   float* r;                            // [Rpad] scratch (and the last r)
   float* g;                            // [N] the last g
@@ -876,7 +876,7 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
     const size_t bars = o;
     o = al16(o + 8 * (size_t)nring);
     const size_t limbs = o;
-    o = al16(o + 3 * (size_t)(Rpad + 32));
+    o = al16(o + 3 * (size_t)(Rpad + 64));
     const size_t fc = o;
     o = al16(o + 16 * (size_t)nchunks);
     const size_t as = o;
@@ -973,7 +973,7 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   A.wpc = wpc;
   A.words_total = words_total;
   A.cap_c = cap_c;
-  A.limb_stride = Rpad + 32;                          // planes 2 bank quads apart
+  A.limb_stride = Rpad + 64;   // planes 64 B apart (mod 128): the 8 lanes of an LDS.128 phase (planes 0, 1) hit disjoint banks
   A.s_cap = s_cap;
   A.yhat = yhat;
   A.r = r;

@@ -1,0 +1,7 @@
+#!/bin/bash
+# limb planes 64 B apart (conflict-free LDS.128 phases) in the fused and int8-MMA adjoints
+OUT=gpurun_out/r02g40; mkdir -p $OUT
+TL_CTAS=0 timeout 300 python scripts/r02/fused_tl.py 2 3 > $OUT/fused_tl.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -rf -k "adjoint or free_running or fused_bounded or teacher" -p no:cacheprovider > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
+for c in 2 3; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err; done
+for b in 2 4; do timeout 600 python bench.py --bits $b --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_c4_b$b.json 2> $OUT/bench_c4_b$b.err; done
