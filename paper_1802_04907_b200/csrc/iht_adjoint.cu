@@ -149,7 +149,7 @@ struct AdjArgs {
 //           (a lane only ever reads back what it copied itself)
 //   [limbs] 3 planes x limb_stride bytes: r in 3 signed 8-bit limbs, permuted per lane chunk
 //   [Fc, Sl, red] per-chunk exponents, exact per-limb integer sums of r_int, scratch
-template <int B>
+template <int B, int RING>
 __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs a) {
   pdl_launch_dependents();
   constexpr int P = 8 / B;               // codes per byte
@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   extern __shared__ __align__(16) uint8_t smem[];
   const int nchunks = a.KRp / a.KC;
   uint8_t* ring = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMmaWarps * kRing * kSlot);   // [warp][slot]
-  uint8_t* limbs = smem + kMmaWarps * kRing * kSlot + kMmaWarps * kRing * 8;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMmaWarps * RING * kSlot);   // [warp][slot]
+  uint8_t* limbs = smem + kMmaWarps * RING * kSlot + kMmaWarps * RING * 8;
   int* Fc = reinterpret_cast<int*>(limbs + 3 * a.limb_stride);
   int* Sl = Fc + ((nchunks + 1) & ~1);                     // [chunk][3] limb sums of r_int
   float* red = reinterpret_cast<float*>(Sl + 3 * nchunks);  // [nchunks][kMmaWarps] scratch
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   const int64_t row0 = (int64_t)kr * a.KR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // ---- work assignment; the first kRing k-steps are requested before the prologue ------
+  // ---- work assignment; the first RING k-steps are requested before the prologue ------
   const int g8 = lane >> 2, t = lane & 3;
   const int64_t ntask = (a.N + 15) / 16;
   const int64_t wid = (int64_t)blockIdx.x * kMmaWarps + warp;
@@ -187,10 +187,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   // the request loop runs npad k-steps per task (nsteps rounded up to whole requests); the
   // padded steps past nsteps are skipped (config 3: 9 real k-steps of 12 per task)
   const int npad = (nsteps + kReq - 1) / kReq * kReq;
-  const uint32_t ring_w = (uint32_t)__cvta_generic_to_shared(ring + warp * kRing * kSlot);
-  const uint32_t bar_w = (uint32_t)__cvta_generic_to_shared(bars + warp * kRing);
+  const uint32_t ring_w = (uint32_t)__cvta_generic_to_shared(ring + warp * RING * kSlot);
+  const uint32_t bar_w = (uint32_t)__cvta_generic_to_shared(bars + warp * RING);
   if (lane == 0)
-    for (int j = 0; j < kRing; ++j) mbar_init(bar_w + 8 * j, 1);
+    for (int j = 0; j < RING; ++j) mbar_init(bar_w + 8 * j, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
   // request cursor (lane 0) over this warp's flat k-step sequence (task wid, wid + wstride,
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)min(kReq, nsteps - rq_ks) * 1024;
         const uint32_t bar = bar_w + 8 * slot;
-        IHT_DCHECK(slot < kRing && rq >= a.codes && rq + bytes <= a.codes + ntask * 16 * a.strip_bytes,
+        IHT_DCHECK(slot < RING && rq >= a.codes && rq + bytes <= a.codes + ntask * 16 * a.strip_bytes,
                    "adjoint: bulk request inside the copy");
         mbar_expect_tx(bar, bytes);
         bulk_g2s(ring_w + slot * kSlot, rq, bytes, bar);
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
     }
   };
 #pragma unroll 1
-  for (int j = 0; j < kRing; ++j) request(j);
+  for (int j = 0; j < RING; ++j) request(j);
 
   unsigned int* cmax = reinterpret_cast<unsigned int*>(red);   // [nchunks] max |r| bit pattern
   for (int c = tid; c < nchunks; c += blockDim.x) cmax[c] = 0u;
@@ -331,8 +331,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   __syncthreads();
 
   // ---- main loop: tasks (16 columns x this K-range) -> fixed-point chunks -> k-steps.
-  //      Step ks (global step counter gs) lives in ring slot gs % kRing; after consuming it
-  //      the slot is refilled with the step kRing later (this task or the next one).
+  //      Step ks (global step counter gs) lives in ring slot gs % RING; after consuming it
+  //      the slot is refilled with the step RING later (this task or the next one).
   const int spc = a.KC / KSTEP;                            // k-steps per chunk
   const uint32_t limb_n = (uint32_t)__cvta_generic_to_shared(limbs + (g8 < 3 ? g8 : 0) * a.limb_stride);
   const bool bload = g8 < 3;
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
             }
           if (h == kReq - 1) {
             __syncwarp();                        // every lane has its fragments: slot is free
-            request(slot);                       // refill it with the request kRing later
+            request(slot);                       // refill it with the request RING later
           }
 #pragma unroll
           for (int i = 0; i < NMMA; ++i) {   // consecutive MMAs update different accumulators
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
             }
           }
         }
-        if (++slot == kRing) {
+        if (++slot == RING) {
           slot = 0;
           parity ^= 1u;
         }
@@ -452,7 +452,7 @@ __global__ void adjoint_reduce_kernel(const float* __restrict__ part, int nK, in
 }
 
 struct AdjPlan {
-  int KR, KRp, KC, nK, limb_stride;
+  int KR, KRp, KC, nK, limb_stride, ring;
   size_t smem;
   int ctas_x;
 };
@@ -477,6 +477,11 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
     if (kr_env >= 1024) KR = min64((int64_t)kr_env / 1024 * 1024, kMaxKR);
   }
   p.KR = (int)KR;
+  {
+    static int ring_env = -1;                     // profiling override (IHT_ADJ_RING = 3 or 5 slots per warp)
+    if (ring_env < 0) ring_env = getenv("IHT_ADJ_RING") ? atoi(getenv("IHT_ADJ_RING")) : 0;
+    p.ring = ring_env == 5 ? 5 : kRing;
+  }
   p.KRp = (int)((KR + 1023) / 1024 * 1024);
   int d = 4;                            // KC = 1024 d <= kChunkRows, dividing KRp
   while ((p.KRp / 1024) % d) --d;
@@ -484,7 +489,7 @@ static AdjPlan plan_adjoint(const iht_qmat* A, int num_sms) {
   p.nK = (int)((Rpad + KR - 1) / KR);
   p.limb_stride = p.KRp + 64;   // planes 64 B apart (mod 128): the 8 lanes of an LDS.128 phase (planes 0, 1) hit disjoint banks
   const int nchunks = p.KRp / p.KC;
-  p.smem = (size_t)kMmaWarps * kRing * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
+  p.smem = (size_t)kMmaWarps * p.ring * (kSlot + 8) + (size_t)3 * p.limb_stride + sizeof(int) * ((nchunks + 1) & ~1) + sizeof(int) * 3 * nchunks +
            sizeof(float) * nchunks * kMmaWarps + 16;
   int per_sm = (int)(size_t)min64(4, (size_t)(227 * 1024) / p.smem);
   if (per_sm < 1) per_sm = 1;
@@ -571,19 +576,25 @@ static int adjoint_impl(const iht_qmat* A, const float* r, float* g, int variant
   a.g = p.nK > 1 ? static_cast<float*>(ws) : g;
   a.limb_stride = p.limb_stride;
   dim3 grid((unsigned)p.ctas_x, (unsigned)p.nK);
-#define IHT_ADJ0(BB)                                                                              \
+#define IHT_ADJ0(BB, RR)                                                                          \
   do {                                                                                            \
     static bool attr_set = false;                                                                 \
     if (!attr_set) {                                                                              \
-      IHT_CUDA_CHECK(cudaFuncSetAttribute(adjoint_mma_kernel<BB>,                                 \
+      IHT_CUDA_CHECK(cudaFuncSetAttribute(adjoint_mma_kernel<BB, RR>,                             \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); \
       attr_set = true;                                                                            \
     }                                                                                             \
-    IHT_CUDA_CHECK(launch_pdl(adjoint_mma_kernel<BB>, grid, dim3(kMmaWarps * 32), p.smem, st, a));  \
+    IHT_CUDA_CHECK(launch_pdl(adjoint_mma_kernel<BB, RR>, grid, dim3(kMmaWarps * 32), p.smem, st, a));  \
   } while (0)
-  if (A->bits == 2) IHT_ADJ0(2);
-  else if (A->bits == 4) IHT_ADJ0(4);
-  else IHT_ADJ0(8);
+  if (p.ring == 5) {
+    if (A->bits == 2) IHT_ADJ0(2, 5);
+    else if (A->bits == 4) IHT_ADJ0(4, 5);
+    else IHT_ADJ0(8, 5);
+  } else {
+    if (A->bits == 2) IHT_ADJ0(2, kRing);
+    else if (A->bits == 4) IHT_ADJ0(4, kRing);
+    else IHT_ADJ0(8, kRing);
+  }
 #undef IHT_ADJ0
   IHT_LAUNCH_CHECK();
   if (nparts) {                       // solver: the fused threshold sums the partials

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     const uint8_t* __restrict__ codes, int64_t strip_bytes, int64_t words_total, int rows, int rpad, int L,
     float sigma, const int32_t* __restrict__ x_idx, const float* __restrict__ x_val,
     const int32_t* __restrict__ x_nnz, int32_t max_nnz, int32_t ldx, int64_t col_offset, int64_t ncols,
-    const float* __restrict__ yhat, float* __restrict__ r, int64_t vlen) {
+    const float* __restrict__ yhat, float* __restrict__ r, int64_t vlen, int strips) {
   constexpr int CPW = 32 / B;
   constexpr uint32_t MASK = (1u << B) - 1u;
   __shared__ float part[kFwdThreads / 32][kFwdWords][CPW];
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   nnz = nnz < 0 ? 0 : (nnz > max_nnz ? max_nnz : nnz);
   const int64_t word = (int64_t)blockIdx.x * kFwdWords + wl;
   const bool live = word < words_total;
-  const int64_t kofs = (word >> 4) * 1024 + (word & 15) * 4;   // tiled offset of this word, sans column
+  // tiled offset of this word, sans column (strips: column-contiguous layout)
+  const int64_t kofs = strips ? word * 4 : (word >> 4) * 1024 + (word & 15) * 4;
   // acc_i = sum_j x_j code_ij and xs = sum_j x_j; the affine map q = 2 code - (L-1) is
   // applied once at the end: sum_j x_j q_ij = 2 acc_i - (L-1) xs
   float acc[CPW];
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     int64_t col = (int64_t)x_idx[st0 + j] - col_offset;
     const bool ok = col >= 0 && col < ncols;
     col = ok ? col : 0;
-    sidx[j] = (col >> 4) * (16 * strip_bytes) + (col & 15) * 64;
+    sidx[j] = strips ? col * strip_bytes : (col >> 4) * (16 * strip_bytes) + (col & 15) * 64;
     sval[j] = ok ? x_val[st0 + j] : 0.0f;
   }
   __syncthreads();
@@ -181,6 +182,8 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
   const unsigned blocks16 = (unsigned)ceil_div<int64_t>(words_total, 16);
   static int ww_env = -1;                        // profiling override (IHT_FWD_WORDS = 8, 16, 32)
   if (ww_env < 0) ww_env = getenv("IHT_FWD_WORDS") ? atoi(getenv("IHT_FWD_WORDS")) : 0;
+  static int strips_env = -1;                    // EXPERIMENT: column-contiguous address pattern
+  if (strips_env < 0) strips_env = getenv("IHT_FWD_STRIPS") ? atoi(getenv("IHT_FWD_STRIPS")) : 0;
   const bool mid = ww_env == 16 || (ww_env == 0 && nrhs == 1 && blocks16 >= 2u * kNumSMs);
   const int64_t vlen = iht_vec_len(F->rows, F->planes);
   if (F->rows > 0x7FFFFFFF) return IHT_EINVAL;
@@ -189,7 +192,7 @@ extern "C" int iht_forward_batched(const iht_qmat* F, const int32_t* x_idx, cons
 #define IHT_FWD(BB, WW, NBLK)                                                                   \
   IHT_CUDA_CHECK(launch_pdl(forward_kernel<BB, WW>, dim3(NBLK, nrhs), dim3(kFwdThreads), 0, st, codes,    \
                             F->strip_bytes, words_total, (int)F->rows, (int)iht_rows_pad(F->rows), L, sigma, \
-                            x_idx, x_val, x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen))
+                            x_idx, x_val, x_nnz, max_nnz, ldx, F->col_offset, F->cols, yhat, r, vlen, strips_env))
   if ((wide && ww_env == 0) || ww_env == 32) {
     if (F->bits == 2) IHT_FWD(2, 32, blocks32);
     else if (F->bits == 4) IHT_FWD(4, 32, blocks32);
