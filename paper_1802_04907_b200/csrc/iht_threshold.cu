@@ -229,6 +229,100 @@ __global__ void __launch_bounds__(kTileThreads) thr_candidates(int s, int64_t N,
   }
 }
 
+// Exact top-s of `total` gathered candidates (cidx, cval in shared memory, increasing index
+// order) that contain every key with digit >= d1 (the bin of the s-th largest key; `above` keys
+// lie in higher bins): keys in bins above d1 are kept, the need = s - above remaining come from
+// bin d1 through a second 11-bit histogram and a rank of the few keys of sub-bin d2; keys below
+// d1 (a bounded superset) are dropped.  Ordered compaction into out_*.  All NT threads call it.
+template <int NT>
+__device__ void gathered_select(int total, const int32_t* cidx, const float* cval, unsigned char* keep, int* hist,
+                                int* grp_k, int* gpos, unsigned int d1, int above, int s, bool all,
+                                int32_t* __restrict__ out_idx, float* __restrict__ out_val,
+                                int32_t* __restrict__ out_nnz, int* scratch, int* wgt, int* weq, int* wtake,
+                                int* wbase, int* sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  for (int b = tid; b < 2048; b += NT) hist[b] = 0;
+  __syncthreads();
+  auto key_of = [&](int i) { return __float_as_uint(cval[i]) & 0x7FFFFFFFu; };
+  if (all || total <= s) {
+    for (int i = tid; i < total; i += NT) keep[i] = 1;
+  } else {
+    const int need = s - above;                 // >= 1
+    // second level: 11-bit histogram of the bin-d1 keys (bits 19..9)
+    for (int i = tid; i < total; i += NT) {
+      const unsigned int k = key_of(i);
+      keep[i] = (k >> 20) > d1;
+      if ((k >> 20) == d1) atomicAdd(&hist[(k >> 9) & 2047], 1);
+    }
+    __syncthreads();
+    find_bin<NT>(hist, 2048, need, &sh[0], &sh[1], scratch);
+    const unsigned int d2 = (unsigned int)sh[0];
+    const int need2 = need - sh[1];             // >= 1 keys to take from sub-bin d2
+    const unsigned int pre = (d1 << 11) | d2;   // 22-bit prefix of the sub-bin
+    // compact sub-bin d2 (index order); keep the keys above it
+    int ng = 0;
+    for (int i0 = 0; i0 < total; i0 += NT) {
+      const int i = i0 + tid;
+      const unsigned int k = i < total ? key_of(i) : 0u;
+      const bool f = i < total && (k >> 9) == pre;
+      if (i < total && (k >> 20) == d1 && ((k >> 9) & 2047) > d2) keep[i] = 1;
+      const unsigned int bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wgt[warp] = __popc(bal);
+      __syncthreads();
+      int off = ng, tot = 0;
+      for (int q = 0; q < NT / 32; ++q) {
+        if (q < warp) off += wgt[q];
+        tot += wgt[q];
+      }
+      if (f && off + __popc(bal & lt) < 1024) {
+        grp_k[off + __popc(bal & lt)] = (int)k;
+        gpos[off + __popc(bal & lt)] = i;  // reuse: list position of the group member
+      }
+      ng += tot;
+      __syncthreads();
+    }
+    if (ng <= 1024) {
+      for (int e = tid; e < ng; e += NT) {
+        const unsigned int ke = (unsigned int)grp_k[e];
+        int rk = 0;
+        for (int f = 0; f < ng; ++f) {
+          const unsigned int kf = (unsigned int)grp_k[f];
+          rk += kf > ke || (kf == ke && f < e);
+        }
+        if (rk < need2) keep[gpos[e]] = 1;
+      }
+    } else {                                    // a crowded sub-bin: radix passes over the candidates
+      __syncthreads();
+      select_ordered<NT>(total, s, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, out_idx, out_val,
+                         out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
+      return;
+    }
+  }
+  __syncthreads();
+  // ordered compaction of the kept candidates
+  int base = 0;
+  for (int i0 = 0; i0 < total; i0 += NT) {
+    const int i = i0 + tid;
+    const bool f = i < total && keep[i];
+    const unsigned int bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wgt[warp] = __popc(bal);
+    __syncthreads();
+    int off = base, tot = 0;
+    for (int q = 0; q < NT / 32; ++q) {
+      if (q < warp) off += wgt[q];
+      tot += wgt[q];
+    }
+    if (f) {
+      out_idx[off + __popc(bal & lt)] = cidx[i];
+      out_val[off + __popc(bal & lt)] = cval[i];
+    }
+    base += tot;
+    __syncthreads();
+  }
+  if (tid == 0) *out_nnz = base;
+}
+
 // T3 (one CTA per snapshot): gather the candidates (index order), then the exact top-s.  Keys
 // in bins above d1 (`above` < s of them) are all kept; the need = s - above remaining come from
 // bin d1: a second 11-bit histogram over the bin-d1 keys finds the sub-bin d2 of the need-th
@@ -332,86 +426,247 @@ __global__ void __launch_bounds__(kThrThreads, 1) thr_select(
       }
     }
   }
-  for (int b = tid; b < 2048; b += kThrThreads) hist[b] = 0;
-  __syncthreads();
-  auto key_of = [&](int i) { return __float_as_uint(cval[i]) & 0x7FFFFFFFu; };
-  if (all || total <= s) {
-    for (int i = tid; i < total; i += kThrThreads) keep[i] = 1;
-  } else {
-    const int need = s - above;                 // >= 1
-    // second level: 11-bit histogram of the bin-d1 keys (bits 19..9)
-    for (int i = tid; i < total; i += kThrThreads) {
-      const unsigned int k = key_of(i);
-      keep[i] = (k >> 20) > d1;
-      if ((k >> 20) == d1) atomicAdd(&hist[(k >> 9) & 2047], 1);
+  gathered_select<kThrThreads>(total, cidx, cval, keep, hist, grp_k, tile_base, d1, above, s, all, out_idx, out_val,
+                               out_nnz, scratch, wgt, weq, wtake, wbase, sh);
+  finish();
+}
+
+// ---------------------------------------------------------------------------- one-launch grid path
+// ONE cooperative launch over the tiles (replaces T1 - T3; all CTAs co-resident):
+//   phase 1  CTA t forms a = x + mu g on its tile in shared memory (split-K partials summed in
+//            adjoint_reduce_kernel's order), adds its 2048-bin histogram to the global one;
+//   barrier  (arrival counter per snapshot, release / acquire);
+//   phase 2  every CTA finds the same bin d1 of the s-th largest key in the global histogram
+//            and writes its keys with digit >= d1 (from shared memory) to its candidate slot
+//            in index order, then arrives on the counter again;
+//   finish   the last CTA to arrive gathers the candidates and finishes the exact select
+//            (gathered_select, as T3), then zeroes the histogram, flags and counter.
+// Same arithmetic and output as T1 - T3 (H_s with the tie rule of reading c15), two launches
+// and their PDL hand-offs fewer.
+constexpr int kOpThreads = 512;
+constexpr int kOpWarps = kOpThreads / 32;
+constexpr int kOpMaxTiles = 1024;              // per-tile counts scanned in shared memory
+
+__global__ void __launch_bounds__(kOpThreads, 1) thr_onepass(
+    const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
+    int64_t N, int64_t col_offset, ThrWs w0, int nparts, float gsigma, float* __restrict__ gout,
+    int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz) {
+  extern __shared__ __align__(16) unsigned char dsm[];   // last CTA: gathered candidates
+  __shared__ float as[kTile];
+  __shared__ int hist[kHistBins];
+  __shared__ unsigned char keep[kCandCap];
+  __shared__ int tile_base[kOpMaxTiles + 1];
+  __shared__ int grp_k[1024];
+  __shared__ int scratch[kOpWarps], wgt[kOpWarps], weq[kOpWarps], wtake[kOpWarps], wbase[kOpWarps], sh[8];
+  __shared__ int s_last, s_stop;
+  pdl_launch_dependents();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned int lt = (1u << lane) - 1u;
+  for (int b = tid; b < kHistBins; b += kOpThreads) hist[b] = 0;
+  pdl_wait();                                   // g (adjoint) and x (previous H_s)
+  const int bq = blockIdx.y;
+  if (mu_dev) mu = mu_dev[bq];
+  const ThrWs w = thr_at(w0, bq);
+  x_idx += (int64_t)bq * ldx;
+  x_val += (int64_t)bq * ldx;
+  const int xn = x_nnz[bq];
+  out_idx += (int64_t)bq * ldo;
+  out_val += (int64_t)bq * ldo;
+  out_nnz += bq;
+  g += (int64_t)bq * N;
+  if (gout) gout += (int64_t)bq * N;
+  const int G = (int)gridDim.x;
+  const int64_t start = (int64_t)blockIdx.x * kTile;
+  const int cnt = (int)min64(kTile, N - start);
+  // ---- phase 1: a, NaN flag, histogram
+  constexpr int PER = kTile / kOpThreads;       // 4 entries per thread, all loads in flight
+  float gv[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kOpThreads;
+    float v = 0.0f;
+    if (i < cnt) {
+      v = __ldg(g + start + i);
+      for (int k = 1; k < nparts; ++k) v = __fadd_rn(v, __ldg(g + (int64_t)k * N + start + i));
+      if (nparts > 0) v = __fmul_rn(gsigma, v);   // adjoint_reduce_kernel's order and rounding
     }
-    __syncthreads();
-    find_bin<kThrThreads>(hist, 2048, need, &sh[0], &sh[1], scratch);
-    const unsigned int d2 = (unsigned int)sh[0];
-    const int need2 = need - sh[1];             // >= 1 keys to take from sub-bin d2
-    const unsigned int pre = (d1 << 11) | d2;   // 22-bit prefix of the sub-bin
-    // compact sub-bin d2 (index order); keep the keys above it
-    int ng = 0;
-    for (int i0 = 0; i0 < total; i0 += kThrThreads) {
-      const int i = i0 + tid;
-      const unsigned int k = i < total ? key_of(i) : 0u;
-      const bool f = i < total && (k >> 9) == pre;
-      if (i < total && (k >> 20) == d1 && ((k >> 9) & 2047) > d2) keep[i] = 1;
-      const unsigned int bal = __ballot_sync(0xffffffffu, f);
-      if (lane == 0) wgt[warp] = __popc(bal);
-      __syncthreads();
-      int off = ng, tot = 0;
-      for (int q = 0; q < kThrWarps; ++q) {
-        if (q < warp) off += wgt[q];
-        tot += wgt[q];
-      }
-      if (f && off + __popc(bal & lt) < 1024) {
-        grp_k[off + __popc(bal & lt)] = (int)k;
-        tile_base[off + __popc(bal & lt)] = i;  // reuse: list position of the group member
-      }
-      ng += tot;
-      __syncthreads();
-    }
-    if (ng <= 1024) {
-      for (int e = tid; e < ng; e += kThrThreads) {
-        const unsigned int ke = (unsigned int)grp_k[e];
-        int rk = 0;
-        for (int f = 0; f < ng; ++f) {
-          const unsigned int kf = (unsigned int)grp_k[f];
-          rk += kf > ke || (kf == ke && f < e);
-        }
-        if (rk < need2) keep[tile_base[e]] = 1;
-      }
-    } else {                                    // a crowded sub-bin: radix passes over the candidates
-      __syncthreads();
-      select_ordered(total, s, [&](int i) { return cval[i]; }, [&](int i) { return cidx[i]; }, out_idx, out_val,
-                     out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
-      finish();
-      return;
+    gv[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kOpThreads;
+    if (i < cnt) {
+      if (gout && nparts > 0) gout[start + i] = gv[u];
+      as[i] = __fmul_rn(mu, gv[u]);
     }
   }
+  const int nnz = xn < 0 ? 0 : min(xn, max_nnz);
   __syncthreads();
-  // ordered compaction of the kept candidates
-  int base = 0;
-  for (int i0 = 0; i0 < total; i0 += kThrThreads) {
-    const int i = i0 + tid;
-    const bool f = i < total && keep[i];
-    const unsigned int bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) wgt[warp] = __popc(bal);
+  for (int j = tid; j < nnz; j += kOpThreads) {
+    const int64_t n = (int64_t)x_idx[j] - col_offset;   // local column (column shards)
+    if (n >= start && n < start + cnt) as[n - start] = __fadd_rn(x_val[j], as[n - start]);
+  }
+  __syncthreads();
+  int nan = 0;
+  for (int i = tid; i < cnt; i += kOpThreads) {
+    const float v = as[i];
+    w.a[start + i] = v;                         // kept for the massive-tie fallback
+    const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
+    nan |= key > 0x7F800000u;
+    atomicAdd(&hist[key >> 20], 1);
+  }
+  nan = __syncthreads_or(nan);
+  if (tid == 0 && nan) atomicOr(&w.flags[0], 1);
+  for (int b = tid; b < kHistBins; b += kOpThreads)
+    if (hist[b]) atomicAdd(&w.hist[b], hist[b]);
+  // ---- grid barrier of this snapshot's CTAs (co-resident: cooperative launch)
+  __syncthreads();
+  unsigned int* ctr = reinterpret_cast<unsigned int*>(&w.flags[3]);
+  if (tid == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned int v;
+#ifdef IHT_CHECKS
+    long long spins = 0;
+#endif
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+#ifdef IHT_CHECKS
+      if (++spins > IHT_SPIN_LIMIT) {
+        printf("IHT_DCHECK: thr_onepass barrier did not complete (block %d)\n", (int)blockIdx.x);
+        __trap();
+      }
+#endif
+    } while (v < (unsigned int)G);
+    s_stop = xn < 0 || __ldcg(&w.flags[0]) != 0 || s == 0;
+  }
+  __syncthreads();
+  // ---- phase 2: bin d1 of the s-th largest key (every CTA, same histogram), candidates
+  const bool all = (int64_t)s >= N;
+  const bool stop = s_stop != 0;
+  unsigned int d1 = 0u;
+  int above = 0;
+  if (!stop) {
+    for (int b = tid; b < kHistBins; b += kOpThreads) hist[b] = __ldcg(&w.hist[b]);
     __syncthreads();
-    int off = base, tot = 0;
-    for (int q = 0; q < kThrWarps; ++q) {
-      if (q < warp) off += wgt[q];
+    if (!all) {
+      find_bin<kOpThreads>(hist, kHistBins, s, &sh[0], &sh[1], scratch);
+      d1 = (unsigned int)sh[0];
+      above = sh[1];
+    }
+    constexpr int per_warp = kTile / kOpWarps;  // 128 contiguous entries per warp
+    const int lo = warp * per_warp, hi = min(cnt, lo + per_warp);
+    auto pick = [&](float v) {
+      const unsigned int key = __float_as_uint(v) & 0x7FFFFFFFu;
+      return key > 0u && (all || (key >> 20) >= d1);
+    };
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < per_warp / 32; ++u) {
+      const int i = lo + u * 32 + lane;
+      c += __popc(__ballot_sync(0xffffffffu, i < hi && pick(as[i])));
+    }
+    if (lane == 0) wgt[warp] = c;
+    __syncthreads();
+    int base = 0, tot = 0;
+    for (int q = 0; q < kOpWarps; ++q) {
+      if (q < warp) base += wgt[q];
       tot += wgt[q];
     }
-    if (f) {
-      out_idx[off + __popc(bal & lt)] = cidx[i];
-      out_val[off + __popc(bal & lt)] = cval[i];
+#pragma unroll
+    for (int u = 0; u < per_warp / 32; ++u) {
+      const int i = lo + u * 32 + lane;
+      const float v = i < hi ? as[i] : 0.0f;
+      const bool sel = i < hi && pick(v);
+      const unsigned int bb = __ballot_sync(0xffffffffu, sel);
+      if (sel) {
+        const int pos = base + __popc(bb & lt);
+        w.cidx[start + pos] = (int32_t)(col_offset + start + i);
+        w.cval[start + pos] = v;
+      }
+      base += __popc(bb);
     }
-    base += tot;
+    if (tid == 0) w.ccount[blockIdx.x] = tot;
+  }
+  // ---- the last CTA to arrive finishes the select
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(ctr, 1u) == 2u * (unsigned int)G - 1u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  auto finish = [&]() {                         // zero the histogram, flags and counter for the next call
+    __syncthreads();
+    for (int b = tid; b < kHistBins; b += kOpThreads) w.hist[b] = 0;
+    if (tid < 4) w.flags[tid] = 0;
+  };
+  if (stop) {                                   // poisoned input / NaN -> domain error; H_0 keeps nothing
+    if (tid == 0) *out_nnz = s == 0 && xn >= 0 && __ldcg(&w.flags[0]) == 0 ? 0 : -1;
+    finish();
+    return;
+  }
+  int carry = 0;                                // exclusive scan of the tile counts
+  for (int t0 = 0; t0 < G; t0 += kOpThreads) {
+    const int t = t0 + tid;
+    const int myc = t < G ? __ldcg(&w.ccount[t]) : 0;
+    int incl = myc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) scratch[warp] = incl;
+    __syncthreads();
+    int before = carry, tot = 0;
+    for (int q = 0; q < kOpWarps; ++q) {
+      if (q < warp) before += scratch[q];
+      tot += scratch[q];
+    }
+    if (t < G) tile_base[t] = before + incl - myc;
+    carry += tot;
     __syncthreads();
   }
-  if (tid == 0) *out_nnz = base;
+  if (tid == 0) tile_base[G] = carry;
+  __syncthreads();
+  const int total = carry;
+  if (total > kCandCap) {                       // massive ties: radix passes over a itself
+    const float* a = w.a;
+    const int c0 = (int)col_offset;
+    select_ordered<kOpThreads>((int)N, s, [&](int i) { return __ldcg(&a[i]); }, [&](int i) { return c0 + i; },
+                               out_idx, out_val, out_nnz, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
+    finish();
+    return;
+  }
+  int32_t* cidx = reinterpret_cast<int32_t*>(dsm);
+  float* cval = reinterpret_cast<float*>(dsm + kCandCap * 4);
+  for (int i0 = 0; i0 < total; i0 += 2 * kOpThreads) {
+    int32_t ci[2];
+    float cv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * kOpThreads + tid;
+      if (i < total) {
+        int lo = 0, hi = G;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (tile_base[mid] <= i) lo = mid; else hi = mid;
+        }
+        const int64_t src = (int64_t)lo * kTile + (i - tile_base[lo]);
+        ci[u] = __ldcg(&w.cidx[src]);
+        cv[u] = __ldcg(&w.cval[src]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * kOpThreads + tid;
+      if (i < total) {
+        cidx[i] = ci[u];
+        cval[i] = cv[u];
+      }
+    }
+  }
+  gathered_select<kOpThreads>(total, cidx, cval, keep, hist, grp_k, tile_base, d1, above, s, all, out_idx, out_val,
+                              out_nnz, scratch, wgt, weq, wtake, wbase, sh);
   finish();
 }
 
@@ -996,6 +1251,7 @@ static int thr_attrs() {
   if (!g_thr_attr) {
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_select, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
+    IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_onepass, cudaFuncAttributeMaxDynamicSharedMemorySize, kCandCap * 8));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     IHT_CUDA_CHECK(cudaFuncSetAttribute(thr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kClusterSlice * 4 + kClWarps * kWarpCand * 16));
@@ -1009,6 +1265,27 @@ static int thr_attrs() {
 // instead of CL <= 8 (config 4, N = 262144: 22.5 us in the cluster).  IHT_THR_MULTI=1 forces
 // the grid path, =2 the cluster path where it fits (profiling).
 constexpr int64_t kGridSelMinN = 131072;
+// Grid path: the one-launch select (thr_onepass, default, when its tiles fit the device at once)
+// or T1 - T3 (IHT_THR_ONEPASS=0, profiling, or too many tiles).
+static bool thr_onepass_on() {
+  static int env = -1;
+  if (env < 0) env = getenv("IHT_THR_ONEPASS") ? atoi(getenv("IHT_THR_ONEPASS")) : 1;
+  return env != 0;
+}
+// CTAs of thr_onepass that fit the device at once (its grid barrier needs them co-resident).
+static int64_t thr_onepass_capacity() {
+  static int64_t cap = -1;
+  if (cap < 0) {
+    int dev = 0, sms = 0, per = 0;
+    if (thr_attrs() != IHT_OK || cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, thr_onepass, kOpThreads, (size_t)kCandCap * 8) !=
+            cudaSuccess)
+      per = 0;
+    cap = (int64_t)sms * per;
+  }
+  return cap;
+}
 static bool thr_grid_path(int64_t N, int nrhs) {
   static int env = -1;
   if (env < 0) env = getenv("IHT_THR_MULTI") ? atoi(getenv("IHT_THR_MULTI")) : 0;
@@ -1106,6 +1383,23 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
   // workspace (standalone calls) is zeroed here
   if (!ws_prezeroed) IHT_CUDA_CHECK(cudaMemsetAsync(ws, 0, nrhs * thr_hdr_bytes(), st));
   const unsigned tiles = (unsigned)((N + kTile - 1) / kTile);
+  if (thr_onepass_on() && tiles <= (unsigned)kOpMaxTiles && (int64_t)tiles * nrhs <= thr_onepass_capacity()) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(tiles, nrhs);
+    lc.blockDim = dim3(kOpThreads);
+    lc.dynamicSmemBytes = (size_t)kCandCap * 8;
+    lc.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;                        // grid barrier: all CTAs co-resident
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see pdl_wait
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 2;
+    IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_onepass, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s, N,
+                                      col_offset, w, nparts, gsigma, gout, out_idx, out_val, ldo, out_nnz));
+    return IHT_OK;
+  }
   IHT_CUDA_CHECK(launch_pdl(thr_update_hist, dim3(tiles, nrhs), dim3(kTileThreads), 0, st, x_idx, x_val, x_nnz,
                             max_nnz, ldx, g, mu, mu_dev, N, col_offset, w, nparts, gsigma, gout));
   IHT_CUDA_CHECK(launch_pdl(thr_candidates, dim3(tiles, nrhs), dim3(kTileThreads), 0, st, s, N, col_offset, w));
@@ -1122,7 +1416,11 @@ extern "C" int iht_threshold_batched(const int32_t* x_idx, const float* x_val, c
                         out_val, ldo, out_nnz, ws, ws_bytes, stream, false);   // caller's (cold) workspace
 }
 
-int iht_threshold_launches(int64_t N) { return thr_grid_path(N, 1) ? 3 : 1; }
+int iht_threshold_launches(int64_t N) {
+  if (!thr_grid_path(N, 1)) return 1;
+  const int64_t tiles = (N + kTile - 1) / kTile;
+  return thr_onepass_on() && tiles <= kOpMaxTiles && tiles <= thr_onepass_capacity() ? 1 : 3;
+}
 
 extern "C" int iht_threshold(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz,
                              const float* g, float mu, int32_t s, int64_t N, int32_t* out_idx,

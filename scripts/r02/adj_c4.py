@@ -8,8 +8,8 @@ sys.path.insert(0, "/root/repo")
 from paper_1802_04907_b200 import iht
 
 dev = torch.device("cuda:0")
-M, N = 65536, 262144
 bits = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+M, N = 65536, int(sys.argv[2]) if len(sys.argv) > 2 else 262144
 A = [iht.new_copy(M, N, 1, bits, 0, 77, k, 1.0, device=dev) for k in range(2)]
 for c in A:
     c.codes.random_(0, 255)
@@ -27,5 +27,5 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / reps * 1e3
 byts = M * N * bits / 8 + 4 * M + 4 * N
-print(f"bits {bits} KR={os.environ.get('IHT_ADJ_KR', 'auto')} RING={os.environ.get('IHT_ADJ_RING', '3')}: "
+print(f"N {N} bits {bits} KR={os.environ.get('IHT_ADJ_KR', 'auto')} RING={os.environ.get('IHT_ADJ_RING', '3')}: "
       f"{us:.1f} us per adjoint, {byts / us / 1e3:.1f} GB/s")

@@ -224,6 +224,56 @@ def test_threshold_ties_and_zeros():
     assert idx.tolist() == ri.tolist()
 
 
+def _iterate_like(N, s, rng, jump=1.0, crowd=0):
+    """H_s input shaped like a solver iteration: x = H_s(a0) (so min |x| is the previous
+    threshold), then a new g; `jump` scales g (the threshold moves far), `crowd` places that
+    many keys just below the previous threshold (more candidates than the gather holds)."""
+    a0 = rng.standard_normal(N).astype(np.float32)
+    xi, xv = OI.hard_threshold(a0.astype(np.float64), s)
+    xv = xv.astype(np.float32)
+    g = (0.3 * jump * rng.standard_normal(N)).astype(np.float32)
+    if crowd:
+        thr = np.float32(np.min(np.abs(xv)))
+        pos = rng.choice(np.setdiff1d(np.arange(N), xi), crowd, replace=False)
+        g[pos] = np.float32(0.95) * thr * np.where(rng.random(crowd) < 0.5, 1, -1).astype(np.float32)
+    return xi, xv, g
+
+
+@pytest.mark.parametrize("N,s,jump,crowd", [(131072, 1024, 1.0, 0), (262144, 1024, 1.0, 0), (262144, 1024, 30.0, 0),
+                                            (262144, 1024, 1.0, 12000), (300000, 7000, 1.0, 0),
+                                            (262145, 4000, 0.1, 0), (262144, 64, 1.0, 0)])
+def test_threshold_onepass_iteration_shaped(N, s, jump, crowd):
+    """The one-launch grid select (thr_onepass: histogram, grid barrier, candidates, last-CTA
+    finish) on iteration-shaped inputs, incl. a threshold jump and a crowded bin that
+    overflows the gather: exact H_s of the same fp32 a."""
+    rng = np.random.default_rng(N + s + int(jump) + crowd)
+    xi, xv, g = _iterate_like(N, s, rng, jump, crowd)
+    idx, val = _thr(xi, xv, g, 1.0, s)
+    a = _a32(xi, xv, g, 1.0)
+    ri, rv = OI.hard_threshold(a.astype(np.float64), s)
+    np.testing.assert_array_equal(idx, ri)
+    np.testing.assert_array_equal(val, rv.astype(np.float32))
+
+
+def test_threshold_onepass_ties_at_threshold():
+    """Ties at the selected key spread over many tiles of the grid select: the lowest
+    indices win across tile boundaries (reading c15)."""
+    N, s = 262144, 1000
+    rng = np.random.default_rng(7)
+    xi = np.sort(rng.choice(N, s, replace=False))
+    xv = np.full(s, 1.0, np.float32)
+    g = np.zeros(N, np.float32)
+    g[xi] = 0.0
+    tie = np.sort(rng.choice(np.setdiff1d(np.arange(N), xi), 3000, replace=False))
+    g[tie] = 0.95                                    # 3000 keys at 0.95 compete for nothing; x stays
+    xv[:200] = 0.5                                   # 200 of x fall below the ties: 200 ties at 0.95 are taken
+    idx, val = _thr(xi, xv, g, 1.0, s)
+    a = _a32(xi, xv, g, 1.0)
+    ri, rv = OI.hard_threshold(a.astype(np.float64), s)
+    np.testing.assert_array_equal(idx, ri)
+    np.testing.assert_array_equal(val, rv.astype(np.float32))
+
+
 @pytest.mark.parametrize("N", [16384, 65536, 262144])
 def test_threshold_ties_across_cluster(N):
     """Gathered select (few candidates): ties at T spread over every CTA of the cluster;
