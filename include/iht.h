@@ -169,7 +169,14 @@ IHT_API int iht_quantize_vec_batched(const float* y_dev, int64_t rows, int64_t r
  * vector ... scale-and-add"): only the x_nnz support columns of F
  * are read.  x_idx_dev / x_val_dev: device arrays of length >= max_nnz;
  * x_nnz_dev: device int32 (values < 0 are treated as 0).  yhat_dev and r_dev are
- * stacked vectors of length iht_vec_len(F rows, planes). */
+ * stacked vectors of length iht_vec_len(F rows, planes).  ws_dev: device workspace of
+ * iht_forward_ws_bytes(F, max_nnz) bytes, caller-owned, ZERO before its first use (its
+ * arrival counters are left at zero by every call, so one zeroing suffices); when that
+ * size is > 0 and ws_dev is NULL or smaller, the call falls back to the single-pass
+ * kernel (same results to rounding order).  Large single observations (>= 2 x 148 row
+ * blocks of 64 bytes per strip) use a row-block x column-group grid whose G > 1 groups'
+ * partial row sums are added in group order by the last CTA of each row block:
+ * deterministic. */
 IHT_API int64_t iht_forward_ws_bytes(const iht_qmat* F, int32_t max_nnz);
 IHT_API int iht_forward(const iht_qmat* F, const int32_t* x_idx_dev, const float* x_val_dev,
                 const int32_t* x_nnz_dev, int32_t max_nnz, const float* yhat_dev, float* r_dev,

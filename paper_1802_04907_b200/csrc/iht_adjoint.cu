@@ -142,7 +142,7 @@ struct AdjArgs {
   const float* r;
   float* g;              // nK == 1: final g; else partial[nK][N] (unscaled by sigma)
   int limb_stride;       // bytes between limb planes in smem
-  int probe;             // profiling (IHT_ADJ_PROBE): 1 no r prologue, 2 no MMA work; results invalid
+  int probe;             // profiling (IHT_ADJ_PROBE=1): no r prologue; results invalid
 };
 
 // Shared-memory layout of the MMA kernel:
@@ -270,73 +270,138 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
   // ---- prologue 2: r -> three balanced signed 8-bit limbs, permuted per lane chunk -----
   // A thread converts whole lane chunks (RPC consecutive rows = the 4P items of one lane's
   // 16-byte code chunk): RPC/4 contiguous float4 loads per chunk, 16 float4 in flight per
-  // thread, issued before any conversion; two STS.128 per plane and bit position.
-  if (!(a.probe & 1)) {
-    constexpr int NV = RPC / 4;                   // float4 per lane chunk: 4 (b = 8), 8 (4), 16 (2)
-    constexpr int CPT = NV >= 16 ? 1 : 16 / NV;   // lane chunks per thread per round
-    const int nch = a.KRp / RPC;                  // a multiple of 256: warp-uniform trip counts
-    for (int ch0 = tid; ch0 < nch; ch0 += CPT * 256) {
-      float4 rv[CPT][NV];
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        const int ch = ch0 + q * 256;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int64_t row = row0 + (int64_t)ch * RPC + 4 * v;
-          rv[q][v] = (ch < nch && row < rend) ? __ldg(reinterpret_cast<const float4*>(a.r + row))
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);   // zero limbs past the K-range
+  // thread, issued before any conversion; two STS.128 per plane and bit position.  At b = 2
+  // (64-row lane chunks, only a multiple of 16 of them per K-range) the item-wise form: a
+  // thread converts items of 4 rows with kIt items' loads in flight.
+  if constexpr (B == 2) {
+    if (!(a.probe & 1)) {
+      // items = KRp / 4, a multiple of 256: every warp runs the same trip count.  The r loads
+      // of kIt items per thread are issued before any of them is converted.
+      constexpr int kIt = 4;
+      const int items = a.KRp / RPC * (4 * P);
+      for (int it0 = tid; it0 < items; it0 += kIt * 256) {
+      float rvs[kIt][4];
+  #pragma unroll
+      for (int q = 0; q < kIt; ++q) {
+        const int it = it0 + q * 256;
+        const int ch = it / (4 * P), rho = it % (4 * P);
+        const int base = ch * RPC + (rho / P) * (32 / B) + (rho % P);
+  #pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = row0 + base + P * i;
+          rvs[q][i] = (it < items && row < rend) ? __ldg(a.r + row) : 0.0f;   // zero limbs past the K-range
         }
       }
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        const int ch = ch0 + q * 256;
-        if (ch >= nch) break;                     // warp-uniform
+  #pragma unroll
+      for (int q = 0; q < kIt; ++q) {
+        const int it = it0 + q * 256;
+        if (it >= items) break;                                 // warp-uniform
+        const int ch = it / (4 * P), rho = it % (4 * P);
         const int c = (ch * RPC) / a.KC;
         const float scale = ldexpf(1.0f, Fc[c]);
-        const float* rr = reinterpret_cast<const float*>(&rv[q][0]);   // rows ch*RPC + 0 .. RPC-1
+        uint32_t l0w = 0, l1w = 0, l2w = 0;
         int s0 = 0, s1 = 0, s2 = 0;
-#pragma unroll
-        for (int e = 0; e < P; ++e) {
-          uint32_t l0w[4], l1w[4], l2w[4];
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {           // item rho = h P + e: rows h CPW + e + P i
-            l0w[h] = l1w[h] = l2w[h] = 0u;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int ri = __float2int_rn(rr[h * (32 / B) + e + P * i] * scale);   // exact power-of-two scaling
-              const int l0 = ((ri + 128) & 255) - 128;
-              const int t1 = (ri - l0) >> 8;
-              const int l1 = ((t1 + 128) & 255) - 128;
-              const int l2 = (t1 - l1) >> 8;
-              s0 += l0; s1 += l1; s2 += l2;
-              l0w[h] |= (uint32_t)(l0 & 255) << (8 * i);
-              l1w[h] |= (uint32_t)(l1 & 255) << (8 * i);
-              l2w[h] |= (uint32_t)(l2 & 255) << (8 * i);
-            }
-          }
-          // bank-spread layout: k-step ch / 4 holds 64 P bytes per plane; the 16-byte chunk of
-          // (bit position j = e, lane t = ch % 4) sits at (4 j + t) 16, word h inside it
-          const int off = (ch >> 2) * (64 * P) + (4 * e + (ch & 3)) * 16;
-          IHT_DCHECK(off + 16 <= a.limb_stride, "adjoint: limb chunk inside its plane");
-          *reinterpret_cast<uint4*>(limbs + off) = make_uint4(l0w[0], l0w[1], l0w[2], l0w[3]);
-          *reinterpret_cast<uint4*>(limbs + a.limb_stride + off) = make_uint4(l1w[0], l1w[1], l1w[2], l1w[3]);
-          *reinterpret_cast<uint4*>(limbs + 2 * a.limb_stride + off) = make_uint4(l2w[0], l2w[1], l2w[2], l2w[3]);
+  #pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float rv = rvs[q][i];
+          const int ri = __float2int_rn(rv * scale);            // exact power-of-two scaling
+          const int l0 = ((ri + 128) & 255) - 128;
+          const int t1 = (ri - l0) >> 8;
+          const int l1 = ((t1 + 128) & 255) - 128;
+          const int l2 = (t1 - l1) >> 8;
+          s0 += l0; s1 += l1; s2 += l2;
+          l0w |= (uint32_t)(l0 & 255) << (8 * i);
+          l1w |= (uint32_t)(l1 & 255) << (8 * i);
+          l2w |= (uint32_t)(l2 & 255) << (8 * i);
         }
-        // exact per-chunk limb sums (|sum| <= 128 x 4096): one native int32 atomic per limb
-        // and warp when the warp's 32 lane chunks lie in one fixed-point chunk, else per thread
-        if (__all_sync(0xffffffffu, c == __shfl_sync(0xffffffffu, c, 0))) {
-          s0 = __reduce_add_sync(0xffffffffu, s0);
-          s1 = __reduce_add_sync(0xffffffffu, s1);
-          s2 = __reduce_add_sync(0xffffffffu, s2);
-          if (lane == 0) {
+        // bank-spread layout: k-step ch / 4 holds 64 P bytes per plane; the 16-byte chunk of
+        // (bit position j = rho % P, lane t = ch % 4) sits at (4 j + t) 16, word v = rho / P in it
+        const int off = (ch >> 2) * (64 * P) + (4 * (rho % P) + (ch & 3)) * 16 + (rho / P) * 4;
+        IHT_DCHECK(off + 4 <= a.limb_stride, "adjoint: limb word inside its plane");
+        *reinterpret_cast<uint32_t*>(limbs + off) = l0w;
+        *reinterpret_cast<uint32_t*>(limbs + a.limb_stride + off) = l1w;
+        *reinterpret_cast<uint32_t*>(limbs + 2 * a.limb_stride + off) = l2w;
+        // the 32 items of a warp lie in one chunk (128 consecutive rows): one native int32
+        // atomic per limb and warp (|sum| <= 128 x 4096 per chunk)
+        s0 = __reduce_add_sync(0xffffffffu, s0);
+        s1 = __reduce_add_sync(0xffffffffu, s1);
+        s2 = __reduce_add_sync(0xffffffffu, s2);
+        if (lane == 0) {
+          atomicAdd(&Sl[3 * c], s0);
+          atomicAdd(&Sl[3 * c + 1], s1);
+          atomicAdd(&Sl[3 * c + 2], s2);
+        }
+      }
+      }
+    }
+  } else {
+    if (!(a.probe & 1)) {
+      constexpr int NV = RPC / 4;                   // float4 per lane chunk: 4 (b = 8), 8 (4), 16 (2)
+      constexpr int CPT = NV >= 16 ? 1 : 16 / NV;   // lane chunks per thread per round
+      const int nch = a.KRp / RPC;                  // a multiple of 32 (b >= 4): warp-uniform trip counts
+      for (int ch0 = tid; ch0 < nch; ch0 += CPT * 256) {
+        float4 rv[CPT][NV];
+  #pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          const int ch = ch0 + q * 256;
+  #pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int64_t row = row0 + (int64_t)ch * RPC + 4 * v;
+            rv[q][v] = (ch < nch && row < rend) ? __ldg(reinterpret_cast<const float4*>(a.r + row))
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);   // zero limbs past the K-range
+          }
+        }
+  #pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          const int ch = ch0 + q * 256;
+          if (ch >= nch) break;                     // warp-uniform
+          const int c = (ch * RPC) / a.KC;
+          const float scale = ldexpf(1.0f, Fc[c]);
+          const float* rr = reinterpret_cast<const float*>(&rv[q][0]);   // rows ch*RPC + 0 .. RPC-1
+          int s0 = 0, s1 = 0, s2 = 0;
+  #pragma unroll
+          for (int e = 0; e < P; ++e) {
+            uint32_t l0w[4], l1w[4], l2w[4];
+  #pragma unroll
+            for (int h = 0; h < 4; ++h) {           // item rho = h P + e: rows h CPW + e + P i
+              l0w[h] = l1w[h] = l2w[h] = 0u;
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int ri = __float2int_rn(rr[h * (32 / B) + e + P * i] * scale);   // exact power-of-two scaling
+                const int l0 = ((ri + 128) & 255) - 128;
+                const int t1 = (ri - l0) >> 8;
+                const int l1 = ((t1 + 128) & 255) - 128;
+                const int l2 = (t1 - l1) >> 8;
+                s0 += l0; s1 += l1; s2 += l2;
+                l0w[h] |= (uint32_t)(l0 & 255) << (8 * i);
+                l1w[h] |= (uint32_t)(l1 & 255) << (8 * i);
+                l2w[h] |= (uint32_t)(l2 & 255) << (8 * i);
+              }
+            }
+            // bank-spread layout: k-step ch / 4 holds 64 P bytes per plane; the 16-byte chunk of
+            // (bit position j = e, lane t = ch % 4) sits at (4 j + t) 16, word h inside it
+            const int off = (ch >> 2) * (64 * P) + (4 * e + (ch & 3)) * 16;
+            IHT_DCHECK(off + 16 <= a.limb_stride, "adjoint: limb chunk inside its plane");
+            *reinterpret_cast<uint4*>(limbs + off) = make_uint4(l0w[0], l0w[1], l0w[2], l0w[3]);
+            *reinterpret_cast<uint4*>(limbs + a.limb_stride + off) = make_uint4(l1w[0], l1w[1], l1w[2], l1w[3]);
+            *reinterpret_cast<uint4*>(limbs + 2 * a.limb_stride + off) = make_uint4(l2w[0], l2w[1], l2w[2], l2w[3]);
+          }
+          // exact per-chunk limb sums (|sum| <= 128 x 4096): one native int32 atomic per limb
+          // and warp when the warp's 32 lane chunks lie in one fixed-point chunk, else per thread
+          if (__all_sync(0xffffffffu, c == __shfl_sync(0xffffffffu, c, 0))) {
+            s0 = __reduce_add_sync(0xffffffffu, s0);
+            s1 = __reduce_add_sync(0xffffffffu, s1);
+            s2 = __reduce_add_sync(0xffffffffu, s2);
+            if (lane == 0) {
+              atomicAdd(&Sl[3 * c], s0);
+              atomicAdd(&Sl[3 * c + 1], s1);
+              atomicAdd(&Sl[3 * c + 2], s2);
+            }
+          } else {
             atomicAdd(&Sl[3 * c], s0);
             atomicAdd(&Sl[3 * c + 1], s1);
             atomicAdd(&Sl[3 * c + 2], s2);
           }
-        } else {
-          atomicAdd(&Sl[3 * c], s0);
-          atomicAdd(&Sl[3 * c + 1], s1);
-          atomicAdd(&Sl[3 * c + 2], s2);
         }
       }
     }
@@ -369,13 +434,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32, 1) adjoint_mma_kernel(AdjArgs 
         // slot is refilled after the request's last k-step has its fragments
         auto kstep = [&](int h) {
           const int ks = ks0 + h;
-          if (a.probe & 2) {                     // profiling probe 2: stream only (timing only)
-            if (h == kReq - 1) {
-              __syncwarp();
-              request(slot);
-            }
-            return;
-          }
           const uint32_t src = ring_w + slot * kSlot + h * 1024 + g8 * 64 + t * 16;
           const uint4 s0 = lds128(src), s1 = lds128(src + 512);
           if (bload) {                           // other lanes keep the zeros set once below

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
 #pragma unroll
         for (int i = 0; i < CPW; ++i) acc[i] = 0.0f;
         float xs = 0.0f;
+        const uint32_t mant_mask = MASK << (23 - B), exp_b = (uint32_t)(127 + B) << 23;   // 2^B
         constexpr int U4 = 4;
         for (int j0 = cl; j0 < nnz; j0 += ncl * U4) {
           uint32_t w[U4];
@@ -310,14 +311,17 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
             xs = __fadd_rn(xs, xv[u]);
 #pragma unroll
             for (int i = 0; i < CPW; ++i) {
-              const float cfv = __int_as_float(0x4B000000u | ((w[u] >> (i * B)) & MASK)) - 8388608.0f;
-              acc[i] = __fmaf_rn(xv[u], cfv, acc[i]);              // exact code; xv = 0 adds +0
+              // the float 2^B + code, exactly (as forward_kernel): one shift + one LOP3
+              const int sh = 23 - B - i * B;
+              const uint32_t xw = sh >= 0 ? (w[u] << sh) : (w[u] >> -sh);
+              const float cfv = __uint_as_float(lop3_and_or(xw, mant_mask, exp_b));
+              acc[i] = __fmaf_rn(xv[u], cfv, acc[i]);              // xv = 0 adds +0
             }
           }
         }
         // affine map q = 2 code - (L-1) once per row, then the fixed-order reductions:
         // column lanes of the warp (xor shuffles), then the 8 warps in order
-        const float xl = __fmul_rn((float)(a.L - 1), xs);
+        const float xl = __fmul_rn((float)((2 << B) + a.L - 1), xs);   // sum x q = 2 acc - (2^{B+1} + L-1) sum x
 #pragma unroll
         for (int i = 0; i < CPW; ++i) acc[i] = __fsub_rn(__fmul_rn(2.0f, acc[i]), xl);
         for (int o = wpc; o < 32; o <<= 1) {                      // CPW independent shuffles per level

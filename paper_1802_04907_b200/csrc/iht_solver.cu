@@ -177,8 +177,8 @@ struct iht_solver {
   // device buffers (one allocation)
   void* block = nullptr;
   float *y = nullptr, *c_y = nullptr, *yhat = nullptr, *r = nullptr, *g = nullptr;
-  void *ws_adj = nullptr, *ws_thr = nullptr;
-  int64_t ws_adj_bytes = 0, ws_thr_bytes = 0;
+  void *ws_adj = nullptr, *ws_thr = nullptr, *ws_fwd = nullptr;
+  int64_t ws_adj_bytes = 0, ws_thr_bytes = 0, ws_fwd_bytes = 0;
   int32_t* xs_idx = nullptr;   // [nslots][B][s]
   float* xs_val = nullptr;     // [nslots][B][s]
   int32_t* xs_nnz = nullptr;   // [nslots][B]
@@ -357,6 +357,9 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
     const float* yh = (S->colshard && S->rank != 0) ? nullptr : S->yhat;
     if (S->fresh) {
       if ((rc = iht_forward_fresh(&S->fm, 2 * n - 1, xi, xv, xn, s, S->yhat, S->r, st)) != IHT_OK) return rc;
+    } else if (B == 1 && yh != nullptr) {
+      // single observation: iht_forward (the row-block x column-group kernel where it applies)
+      if ((rc = iht_forward(&F, xi, xv, xn, s, yh, S->r, S->ws_fwd, S->ws_fwd_bytes, st)) != IHT_OK) return rc;
     } else if ((rc = iht_forward_batched(&F, xi, xv, xn, s, s, B, yh, S->r, st)) != IHT_OK) {
       return rc;
     }
@@ -529,6 +532,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->ws_adj_bytes = fm ? iht_adjoint_fresh_ws_bytes(fm)
                       : batched ? iht_adjoint_batched_ws_bytes(&q0, B) : iht_adjoint_ws_bytes(&q0);
   S->ws_thr_bytes = iht_threshold_batched_ws_bytes(S->N, cfg->s, B);
+  S->ws_fwd_bytes = (!fm && !batched) ? iht_forward_ws_bytes(&q0, cfg->s) : 0;
   S->nslots = cfg->trace ? cfg->n_iter + 1 : 2;
   const int s = cfg->s > 0 ? cfg->s : 1;
   S->cand_words = (S->colshard || S->shardsel) ? 2 * (int64_t)B * s + B : 0;
@@ -536,7 +540,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   const int64_t ycount = q0.rows * q0.planes;
   const int64_t sz_y = al((int64_t)B * ycount * 4), sz_c = al((int64_t)B * 4),
                 sz_v = al((int64_t)B * S->vlen * 4), sz_g = al((int64_t)B * S->N * 4),
-                sz_wa = al(S->ws_adj_bytes), sz_wt = al(S->ws_thr_bytes),
+                sz_wa = al(S->ws_adj_bytes), sz_wt = al(S->ws_thr_bytes), sz_wf = al(S->ws_fwd_bytes),
                 sz_xi = al((int64_t)S->nslots * B * s * 4), sz_xv = al((int64_t)S->nslots * B * s * 4),
                 sz_xn = al((int64_t)S->nslots * B * 4), sz_cs = al(S->cand_words * 4),
                 sz_cr = al(S->cand_words * 4 * world);
@@ -546,7 +550,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   const int64_t sz_ad = ad ? (6 * sz_b4 + al((int64_t)B * 8) + 2 * sz_bs + sz_b4 + 2 * sz_bs + sz_b4 + 2 * sz_b2s +
                               sz_b4 + sz_v + 2 * sz_rec)
                            : 0;
-  const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_xi + sz_xv + sz_xn +
+  const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_wf + sz_xi + sz_xv + sz_xn +
                         ((S->colshard || S->shardsel) ? sz_cs + sz_cr : 0) + sz_ad;
   if (cudaMalloc(&S->block, total) != cudaSuccess) {
     delete S;
@@ -560,6 +564,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->g = reinterpret_cast<float*>(p); p += sz_g;
   S->ws_adj = S->ws_adj_bytes ? p : nullptr; p += sz_wa;
   S->ws_thr = p; p += sz_wt;
+  S->ws_fwd = S->ws_fwd_bytes ? p : nullptr; p += sz_wf;   // zeroed below: the arrival counters start at 0
   S->xs_idx = reinterpret_cast<int32_t*>(p); p += sz_xi;
   S->xs_val = reinterpret_cast<float*>(p); p += sz_xv;
   S->xs_nnz = reinterpret_cast<int32_t*>(p); p += sz_xn;

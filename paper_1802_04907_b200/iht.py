@@ -186,8 +186,11 @@ def forward(F, x_idx, x_val, x_nnz, yhat, max_nnz=None, stream=None):
     _require_cuda(x_idx, x_val, x_nnz, yhat)
     max_nnz = x_idx.numel() if max_nnz is None else max_nnz
     r = torch.empty_like(yhat)
-    check(load().iht_forward(ctypes.byref(F.desc), _ptr(x_idx), _ptr(x_val), _ptr(x_nnz), max_nnz, _ptr(yhat),
-                             _ptr(r), None, 0, _stream(stream)), "iht_forward")
+    lib = load()
+    ws_bytes = lib.iht_forward_ws_bytes(ctypes.byref(F.desc), max_nnz)
+    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=yhat.device)   # arrival counters start at 0
+    check(lib.iht_forward(ctypes.byref(F.desc), _ptr(x_idx), _ptr(x_val), _ptr(x_nnz), max_nnz, _ptr(yhat),
+                          _ptr(r), _ptr(ws), ws_bytes, _stream(stream)), "iht_forward")
     return r
 
 

@@ -5,6 +5,7 @@ per iteration; supports identical whenever the oracle's margin at the s-th
 position exceeds 1e-5 |a|_(s) (otherwise logged as a near-tie).  Shapes span
 several tiles with ragged tails; edge cases cover empty/degenerate inputs.
 """
+import ctypes
 import re
 
 import numpy as np
@@ -127,6 +128,45 @@ def test_forward_parity(M, N, cplx, bits, s):
     r0 = iht.forward(F, _to_dev(x_idx.astype(np.int32)), _to_dev(x_val), _to_dev(np.array([0], np.int32)),
                      _to_dev(yh32))
     np.testing.assert_array_equal(r0.cpu().numpy(), yh32)
+
+
+@pytest.mark.parametrize("M,N,cplx,bits,s,nnz", [(40000, 600, False, 4, 600, 600), (40000, 600, False, 4, 300, 300),
+                                                  (40000, 600, False, 4, 600, 555), (80000, 400, False, 2, 400, 400),
+                                                  (20000, 1100, False, 8, 1100, 1037), (20000, 300, True, 4, 300, 300)])
+def test_forward_split_parity(M, N, cplx, bits, s, nnz):
+    """The row-block x column-group forward (>= 296 row blocks: config-4-like rows) incl. G > 1
+    column groups summed by the last CTA of each row block, a ragged nnz < max_nnz, 2/4/8 bits
+    and complex rows: r within 1e-4 of the oracle's forward; repeated calls reuse the zeroed
+    workspace (the arrival counters are reset by the kernel) and give identical bits."""
+    phi = _phi(M, N, cplx, seed=5)
+    c = OQ.scale_c(phi)
+    (F,) = iht.quantize(_to_dev(phi), bits, 0, SEED, [1], float(c))
+    assert iht.load().iht_forward_ws_bytes(ctypes.byref(F.desc), s) >= (0 if s <= 300 else 1)
+    Fd = OQ.dequantize(OQ.quantize_matrix(phi, bits, 0, SEED, 1, c=c)[0], c, bits, 0)
+    del phi
+    rng = np.random.default_rng(s + nnz)
+    x_idx = np.sort(rng.choice(N, s, replace=False))
+    x_val = rng.standard_normal(s).astype(np.float32)
+    yh = (rng.standard_normal(M) + (1j * rng.standard_normal(M) if cplx else 0)).astype(np.complex128 if cplx else np.float64)
+    yh32 = stack(yh, M).astype(np.float32)
+    args = (_to_dev(x_idx.astype(np.int32)), _to_dev(x_val), _to_dev(np.array([nnz], np.int32)), _to_dev(yh32))
+    lib = iht.load()
+    ws_bytes = lib.iht_forward_ws_bytes(ctypes.byref(F.desc), s)
+    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev())
+    outs = []
+    for _ in range(2):                           # the same workspace twice: counters back at zero
+        r = torch.empty_like(args[3])
+        assert lib.iht_forward(ctypes.byref(F.desc), iht._ptr(args[0]), iht._ptr(args[1]), iht._ptr(args[2]), s,
+                               iht._ptr(args[3]), iht._ptr(r), iht._ptr(ws), ws_bytes, None) == 0
+        torch.cuda.synchronize()
+        outs.append(r.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+    if ws_bytes:                                 # the arrival counters (tail of the workspace) are back at 0
+        nrb = F.desc.strip_bytes // 4 // 16
+        assert int(ws[ws_bytes - 4 * nrb:ws_bytes].count_nonzero().item()) == 0
+    ref = OI.forward(Fd, x_idx[:nnz], x_val[:nnz].astype(np.float64), unstack(yh32, M, 2 if cplx else 1))
+    assert rel_l2(unstack(outs[0], M, 2 if cplx else 1), ref) < TOL
+    assert not np.any(outs[0][stack(np.ones(M) * (1 + 1j if cplx else 1), M) == 0])   # pads stay 0
 
 
 # ------------------------------------------------------------------------- (a5) adjoint
