@@ -150,6 +150,16 @@ struct BatchArgs {
   float* g;                // [B][N]
   long long* tlog;         // probe 32: per-CTA clock64 stamps [cta][64] (profiling only)
   int ep32;                // 1: the integer epilogue fits int32 (Rpad (L-1) < 21700), else fp64
+  // epilogue candidates for the bounded select (iht_threshold.cu, thr_bounded_select; NULL: off):
+  // every (pixel n, snapshot b) with key(mu g) >= bkey_b = bound_key(x_b) is appended to b's list
+  int32_t* cidx;           // [Breal][ccap]
+  float* cval;             // [Breal][ccap]  mu g
+  int* ccnt;               // [Breal] (zero on entry; the select kernel resets it)
+  int ccap;
+  float mu, bound;
+  const float* xval;       // x^[n] of the chunk's snapshots: [Breal][ldx]
+  const int32_t* xnnz;     // [Breal]
+  int ldx, max_nnz;
 };
 
 template <int BITS>
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   float* ep_scale = reinterpret_cast<float*>(tmem_slot + 4);            // [B] sigma 2^-F_b
   long long* ep_off = reinterpret_cast<long long*>(ep_scale + 256);    // [B] (L-1) S_b
   int* ep_off32 = reinterpret_cast<int*>(ep_off + 256);                // [B] same, int32 path
+  unsigned int* ep_bkey = reinterpret_cast<unsigned int*>(ep_off32 + 256);   // [B] candidate bound keys
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -445,6 +456,16 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   } else {
     // ---------------------------------------------------------------- epilogue (warps 7-10)
     const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
+    if (a.cidx) {
+      // bound key of each snapshot (x^[n] was written before the forward this kernel waited on,
+      // transitively); the same function as thr_bounded_select, so both sides agree exactly
+      for (int b = warp - 7; b < a.Breal; b += 4) {
+        const int nnz = min(a.xnnz[b], a.max_nnz);
+        const unsigned int k = warp_bound_key(a.xval + (int64_t)b * a.ldx, nnz, a.bound);
+        if (lane == 0) ep_bkey[b] = k;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
+    }
     int t = 0;
     for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++t) {
       const int ab = t & 1;
@@ -464,21 +485,38 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr + (uint32_t)c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (n < a.N) {
-          // g = sigma 2^-F (2 (D0 + 256 D1) - (L-1) S): exact integers, then one rounding
+        // g = sigma 2^-F (2 (D0 + 256 D1) - (L-1) S): exact integers, then one rounding
+        float gv[8];
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const int b = (cbase + c0 + e) >> 1;
           if (a.ep32) {
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const int b = (cbase + c0 + e) >> 1;
-              const int W = 2 * ((int)v[e] + (int)v[e + 1] * 256) - ep_off32[b];
-              if (b < a.Breal) a.g[(int64_t)b * a.N + n] = __fmul_rn(__int2float_rn(W), ep_scale[b]);
-            }
+            const int W = 2 * ((int)v[e] + (int)v[e + 1] * 256) - ep_off32[b];
+            gv[e >> 1] = __fmul_rn(__int2float_rn(W), ep_scale[b]);
           } else {
+            const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
+            gv[e >> 1] = (float)(2 * V - ep_off[b]) * ep_scale[b];
+          }
+          if (n < a.N && b < a.Breal) a.g[(int64_t)b * a.N + n] = gv[e >> 1];
+        }
+        if (a.cidx) {
+          // candidates: key(mu g) >= bkey_b (x's support is handled by the select kernel); one
+          // atomic per warp and snapshot with any, list order irrelevant (the select ranks)
 #pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const int b = (cbase + c0 + e) >> 1;
-              const long long V = (long long)(int)v[e] + 256ll * (long long)(int)v[e + 1];
-              if (b < a.Breal) a.g[(int64_t)b * a.N + n] = (float)(2 * V - ep_off[b]) * ep_scale[b];
+          for (int e = 0; e < 8; ++e) {
+            const int b = (cbase + c0) / 2 + e;
+            if (b >= a.Breal) break;                      // warp-uniform
+            const float av = __fmul_rn(a.mu, gv[e]);
+            const bool emit = n < a.N && (__float_as_uint(av) & 0x7FFFFFFFu) >= ep_bkey[b];
+            const unsigned int m = __ballot_sync(0xffffffffu, emit);
+            if (m) {
+              int base = 0;
+              if (lane == 0) base = atomicAdd(&a.ccnt[b], __popc(m));
+              base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
+              if (emit && base < a.ccap) {
+                a.cidx[(int64_t)b * a.ccap + base] = (int32_t)n;
+                a.cval[(int64_t)b * a.ccap + base] = av;
+              }
             }
           }
         }
@@ -608,7 +646,7 @@ static size_t batched_smem(int bits, int B) {
   const size_t pk = bits == 2 ? (size_t)BCfg<2>::PK * BCfg<2>::PKSLOTS
                   : bits == 4 ? (size_t)BCfg<4>::PK * BCfg<4>::PKSLOTS : (size_t)BCfg<8>::PK * BCfg<8>::PKSLOTS;
   return 1024 + (size_t)ST * 2 * B * KBB + pk + (size_t)(2 * kPkSlotsMax + 2 * kStagesMax + 4) * 8 + 16 +
-         256 * 4 + 256 * 8 + 256 * 4;
+         256 * 4 + 256 * 8 + 256 * 4 + 256 * 4;
 }
 
 }  // namespace iht
@@ -642,6 +680,11 @@ static int probe_flags() {
 
 extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nrhs, float* G, void* ws,
                                    int64_t ws_bytes, void* stream) {
+  return iht_adjoint_batched_cand(A, R, nrhs, G, ws, ws_bytes, stream, nullptr);
+}
+
+int iht_adjoint_batched_cand(const iht_qmat* A, const float* R, int32_t nrhs, float* G, void* ws, int64_t ws_bytes,
+                             void* stream, const iht_cand_args* cand) {
   if (A == nullptr || R == nullptr || G == nullptr || nrhs <= 0) return IHT_EINVAL;
   if (A->codes == nullptr || (A->bits != 2 && A->bits != 4 && A->bits != 8)) return IHT_EINVAL;
   if (A->strip_bytes != iht_strip_bytes(A->rows, A->planes, A->bits)) return IHT_EINVAL;
@@ -702,6 +745,18 @@ extern "C" int iht_adjoint_batched(const iht_qmat* A, const float* R, int32_t nr
     b.Fb = Fb;
     b.Sb = Sb;
     b.g = G + (int64_t)c0 * A->cols;
+    if (cand) {   // the chunk's snapshots' lists and x
+      b.cidx = cand->cidx + (int64_t)c0 * cand->ccap;
+      b.cval = cand->cval + (int64_t)c0 * cand->ccap;
+      b.ccnt = cand->ccnt + c0;
+      b.ccap = cand->ccap;
+      b.mu = cand->mu;
+      b.bound = cand->bound;
+      b.xval = cand->x_val + (int64_t)c0 * cand->ldx;
+      b.xnnz = cand->x_nnz + c0;
+      b.ldx = cand->ldx;
+      b.max_nnz = cand->max_nnz;
+    }
     const float* Rc = R + (int64_t)c0 * Rpad;
     const size_t smem = batched_smem(A->bits, bp);
 #define IHT_BATCH(BB)                                                                                  \

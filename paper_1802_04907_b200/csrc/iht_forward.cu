@@ -299,8 +299,10 @@ extern "C" int iht_forward(const iht_qmat* F, const int32_t* x_idx, const float*
                            void* ws, int64_t ws_bytes, void* stream) {
   if (yhat == nullptr) return IHT_EINVAL;
   const int G = fs_groups(F, max_nnz);
-  static int fs_env = -1;                        // profiling: IHT_FWD_SPLIT=0 keeps forward_kernel
-  if (fs_env < 0) fs_env = getenv("IHT_FWD_SPLIT") ? atoi(getenv("IHT_FWD_SPLIT")) : 1;
+  // measured (r02 g50, config 4, L2 flushed): forward_split_kernel 35.8 us against forward_kernel's
+  // 27.6 us -- the random 64-byte pieces of the support strips bound both, more bytes in flight per
+  // lane do not help; so forward_kernel is the default and IHT_FWD_SPLIT=1 selects the split kernel
+  const int fs_env = getenv("IHT_FWD_SPLIT") ? atoi(getenv("IHT_FWD_SPLIT")) : 0;   // read per call (tests)
   const int64_t need = iht_forward_ws_bytes(F, max_nnz);
   if (G == 0 || !fs_env || (need > 0 && (ws == nullptr || ws_bytes < need)) || F->codes == nullptr ||
       x_nnz == nullptr || r == nullptr || x_idx == nullptr || x_val == nullptr || F->col_offset < 0 ||

@@ -201,7 +201,30 @@ struct iht_solver {
   int64_t launches = 0;
   int final_slot = 0;
   iht_fused_state* fused = nullptr;    // the whole loop as one persistent kernel (iht_fused.cu)
+  // bounded select (batched, fixed step): epilogue candidate lists + per-snapshot decided flags
+  bool bounded = false;
+  float bound = 0.5f;
+  int32_t* bc_idx = nullptr;   // [B][kBcCap]
+  float* bc_val = nullptr;     // [B][kBcCap]
+  int* bc_cnt = nullptr;       // [B] (zeroed at create, reset by the select kernel)
+  int* bc_done = nullptr;      // [B]
+  int* bc_stats = nullptr;     // [4] decided, fallen back, sum / max list size (IHT_BOUNDED_STATS)
 };
+
+// Candidate slots per snapshot written by the batched epilogue (more: the select falls back).
+static constexpr int kBcCap = 1024;
+
+// IHT_BOUNDED=0 turns the bounded select off (A/B and the bit-identity test); IHT_BOUND sets
+// the bound factor (default 0.5 x the smallest kept |x|).  Read at every solver create.
+static bool bounded_enabled() {
+  const char* e = getenv("IHT_BOUNDED");
+  return e == nullptr || atoi(e) != 0;
+}
+static float bounded_factor() {
+  const char* e = getenv("IHT_BOUND");
+  const float f = e ? (float)atof(e) : 0.5f;
+  return f > 0.0f && f < 1.0f ? f : 0.5f;
+}
 
 // Event record that survives stream capture: inside a capture it becomes an event-record
 // node of the graph (cudaEventRecordExternal), so every replay re-records it.
@@ -382,6 +405,12 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       if ((rc = iht_adjoint(&A, S->r, S->g, S->cfg.adjoint_variant, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK)
         return rc;
       L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
+    } else if (S->bounded) {
+      // the epilogue also lists each snapshot's candidates for the bounded select below
+      iht_cand_args ca{S->bc_idx, S->bc_val, S->bc_cnt, kBcCap, S->cfg.mu, S->bound, xv, xn, s, s};
+      if ((rc = iht_adjoint_batched_cand(&A, S->r, B, S->g, S->ws_adj, S->ws_adj_bytes, st, &ca)) != IHT_OK)
+        return rc;
+      L += 2 * ((B + 63) / 64);
     } else {
       if ((rc = iht_adjoint_batched(&A, S->r, B, S->g, S->ws_adj, S->ws_adj_bytes, st)) != IHT_OK) return rc;
       L += 2 * ((B + 63) / 64);
@@ -416,6 +445,12 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
           IHT_OK)
         return rc;
       L += 1;
+    } else if (S->bounded) {
+      if ((rc = iht_threshold_bounded(xi, xv, xn, s, S->g, S->cfg.mu, S->bound, s, S->N, B, S->bc_idx, S->bc_val,
+                                      S->bc_cnt, kBcCap, S->bc_done, S->bc_stats, oi, ov, s, on, S->ws_thr,
+                                      S->ws_thr_bytes, st)) != IHT_OK)
+        return rc;
+      L += 1 + iht_threshold_launches(S->N);
     } else if (!S->colshard) {
       if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g, S->cfg.mu, nullptr, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)
@@ -550,8 +585,12 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   const int64_t sz_ad = ad ? (6 * sz_b4 + al((int64_t)B * 8) + 2 * sz_bs + sz_b4 + 2 * sz_bs + sz_b4 + 2 * sz_b2s +
                               sz_b4 + sz_v + 2 * sz_rec)
                            : 0;
+  S->bounded = batched && !S->colshard && !fm && cfg->step_mode == 0 && B <= 64 &&
+               iht_threshold_bounded_applies(S->N, cfg->s, B) && bounded_enabled();
+  S->bound = bounded_factor();
+  const int64_t sz_bc = S->bounded ? 2 * al((int64_t)B * kBcCap * 4) + 2 * sz_b4 + al(16) : 0;
   const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_wf + sz_xi + sz_xv + sz_xn +
-                        ((S->colshard || S->shardsel) ? sz_cs + sz_cr : 0) + sz_ad;
+                        ((S->colshard || S->shardsel) ? sz_cs + sz_cr : 0) + sz_ad + sz_bc;
   if (cudaMalloc(&S->block, total) != cudaSuccess) {
     delete S;
     return IHT_ENOMEM;
@@ -592,6 +631,13 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
     S->ad_tmp = reinterpret_cast<float*>(p); p += sz_v;
     S->ad_mu_rec = reinterpret_cast<float*>(p); p += sz_rec;
     S->ad_shr_rec = reinterpret_cast<int32_t*>(p); p += sz_rec;
+  }
+  if (S->bounded) {
+    S->bc_idx = reinterpret_cast<int32_t*>(p); p += al((int64_t)B * kBcCap * 4);
+    S->bc_val = reinterpret_cast<float*>(p); p += al((int64_t)B * kBcCap * 4);
+    S->bc_cnt = reinterpret_cast<int*>(p); p += sz_b4;
+    S->bc_done = reinterpret_cast<int*>(p); p += sz_b4;
+    S->bc_stats = getenv("IHT_BOUNDED_STATS") ? reinterpret_cast<int*>(p) : nullptr; p += al(16);
   }
   // zero everything once (pad rows of the stacked vectors stay 0)
   if (cudaMemset(S->block, 0, total) != cudaSuccess ||
@@ -643,6 +689,12 @@ extern "C" int iht_solver_adjoint_times(iht_solver* S, float* ms) {
 
 extern "C" int iht_solver_destroy(iht_solver* S) {
   if (S == nullptr) return IHT_OK;
+  if (S->bc_stats) {   // profiling (IHT_BOUNDED_STATS): how often the bounded select decided
+    int h[4] = {0, 0, 0, 0};
+    cudaMemcpy(h, S->bc_stats, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "bounded select: decided %d, fell back %d, mean list %.1f, max list %d (bound %.3f)\n", h[0], h[1],
+            h[0] ? (double)h[2] / h[0] : 0.0, h[3], S->bound);
+  }
   for (auto& e : S->ev)
     if (e) cudaEventDestroy(e);
   if (S->exec) cudaGraphExecDestroy(S->exec);

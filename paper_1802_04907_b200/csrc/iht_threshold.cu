@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
     int64_t N, int64_t col_offset, int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
     int32_t ldo, int32_t* __restrict__ out_nnz, int probe, int nparts, float gsigma, float* __restrict__ gout,
-    long long* __restrict__ tl) {
+    long long* __restrict__ tl, const int* __restrict__ skip) {
   // profiling timeline (IHT_THR_TL): globaltimer stamps of CTA ranks 0, 1 of snapshot 0
   auto stamp = [&](int k) {
     if (tl && threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 2) {
@@ -852,6 +852,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   pdl_wait();                                   // g (adjoint) and x (previous H_s)
+  if (skip && skip[blockIdx.y]) return;         // snapshot already selected by thr_bounded_select
   if (mu_dev) mu = mu_dev[blockIdx.y];          // the adaptive step's mu: a predecessor's output too
   stamp(0);
   const int b = blockIdx.y;
@@ -1164,6 +1165,157 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   cluster.sync();                                   // keep shared memory alive for remote readers
 }
 
+// Bounded select (config 5, solver only): the tcgen05 adjoint's epilogue appended every
+// pixel n with key(mu g_n) >= bkey = bound_key(x) to this snapshot's list (cidx, cval, ccnt;
+// iht_batched.cu).  With x's support added (a_j = x_j + mu g_j, the cluster kernel's
+// arithmetic) and the support's own epilogue entries dropped, the list holds every pixel
+// whose key is >= bkey.  If at least s of its keys are >= bkey, the s-th largest key of a is
+// >= bkey too, so every entry of H_s(a) -- including the lowest-index ties at the threshold --
+// is in the list, and the top-s of the list (greater key, then lower index) IS H_s(a), exactly
+// (P:135).  Otherwise (iteration 1, a support change larger than the bound, list
+// overflow, NaN, poisoned x) done[b] = 0 and the cluster kernel that follows selects the
+// snapshot over all of a.  One CTA per snapshot; resets ccnt for the next call.
+constexpr int kBsThreads = 512;
+constexpr int kBsCap = 1024;                   // list entries ranked in shared memory
+constexpr int kBsMaxS = 256;
+
+__global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
+    const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, float bound, int s, int64_t N,
+    const int32_t* __restrict__ cidx, const float* __restrict__ cval, int* __restrict__ ccnt, int ccap,
+    int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz,
+    int* __restrict__ done, int* __restrict__ stats) {
+  __shared__ int32_t lidx[kBsCap];
+  __shared__ unsigned int lkey[kBsCap];
+  __shared__ float lval[kBsCap];
+  __shared__ int32_t sidx[kBsMaxS];
+  __shared__ int sh_n, sh_t, sh_bad, sh_cnt, sh_kept;
+  __shared__ unsigned int sh_bkey;
+  pdl_launch_dependents();
+  pdl_wait();                                   // g and the lists (adjoint), x (previous H_s)
+  const int b = blockIdx.x, tid = threadIdx.x;
+  x_idx += (int64_t)b * ldx;
+  x_val += (int64_t)b * ldx;
+  g += (int64_t)b * N;
+  cidx += (int64_t)b * ccap;
+  cval += (int64_t)b * ccap;
+  out_idx += (int64_t)b * ldo;
+  out_val += (int64_t)b * ldo;
+  const int nraw = x_nnz[b];
+  const int nnz = nraw < 0 ? 0 : min(nraw, max_nnz);
+  if (tid < 32) {
+    const unsigned int k = warp_bound_key(x_val, nraw < 0 ? -1 : nnz, bound);
+    if (tid == 0) {
+      sh_bkey = k;
+      sh_cnt = ccnt[b];
+      sh_n = 0;
+      sh_t = 0;
+      sh_bad = 0;
+      sh_kept = 0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) ccnt[b] = 0;                    // zero for the next call (read above)
+  const int cnt = sh_cnt;
+  const unsigned int bkey = sh_bkey;
+  if (bkey == 0xFFFFFFFFu || s <= 0 || s > kBsMaxS || nnz > kBsMaxS || cnt > ccap || (int64_t)s >= N ||
+      nnz + cnt > kBsCap) {
+    if (tid == 0) {
+      done[b] = 0;
+      if (stats) atomicAdd(&stats[1], 1);
+    }
+    return;
+  }
+  // x's support: a_j = x_j + mu g_j (as the cluster kernel forms it)
+  for (int j = tid; j < nnz; j += kBsThreads) {
+    const int32_t c = x_idx[j];
+    const float av = __fadd_rn(x_val[j], __fmul_rn(mu, __ldg(g + c)));
+    sidx[j] = c;
+    lidx[j] = c;
+    lval[j] = av;
+    lkey[j] = __float_as_uint(av) & 0x7FFFFFFFu;
+  }
+  if (tid == 0) sh_n = nnz;
+  __syncthreads();
+  // the epilogue's entries outside the support (a = mu g there); order is irrelevant
+  for (int i = tid; i < cnt; i += kBsThreads) {
+    const int32_t c = cidx[i];
+    bool in = false;
+    for (int j = 0; j < nnz; ++j) in |= sidx[j] == c;
+    if (!in) {
+      const int p = atomicAdd(&sh_n, 1);
+      const float av = cval[i];
+      lidx[p] = c;
+      lval[p] = av;
+      lkey[p] = __float_as_uint(av) & 0x7FFFFFFFu;
+    }
+  }
+  __syncthreads();
+  const int n = sh_n;
+  int t = 0, bad = 0;
+  for (int i = tid; i < n; i += kBsThreads) {
+    t += lkey[i] >= bkey;
+    bad |= lkey[i] > 0x7F800000u;
+  }
+  if (t) atomicAdd(&sh_t, t);
+  if (bad) sh_bad = 1;
+  __syncthreads();
+  if (sh_bad || sh_t < s) {
+    if (tid == 0) {
+      done[b] = 0;
+      if (stats) atomicAdd(&stats[1], 1);
+    }
+    return;
+  }
+  // rank = keys greater, or equal at a lower index; kept iff rank < s (all kept keys >= bkey > 0)
+  bool keep[(kBsCap + kBsThreads - 1) / kBsThreads];
+#pragma unroll
+  for (int u = 0; u < (kBsCap + kBsThreads - 1) / kBsThreads; ++u) {
+    const int i = tid + u * kBsThreads;
+    keep[u] = false;
+    if (i < n) {
+      const unsigned int ki = lkey[i];
+      const int32_t ii = lidx[i];
+      int rk = 0;
+      for (int j = 0; j < n && rk < s; ++j) {
+        const unsigned int kj = lkey[j];
+        rk += kj > ki || (kj == ki && lidx[j] < ii);
+      }
+      keep[u] = rk < s;
+    }
+  }
+  __syncthreads();
+  // compact the kept entries (s of them) to the front of the list, any order ...
+#pragma unroll
+  for (int u = 0; u < (kBsCap + kBsThreads - 1) / kBsThreads; ++u) {
+    const int i = tid + u * kBsThreads;
+    if (keep[u]) {
+      const int p = atomicAdd(&sh_kept, 1);
+      sidx[p] = lidx[i];
+      reinterpret_cast<float*>(lkey)[p] = lval[i];   // lkey is free now (ranks done)
+    }
+  }
+  __syncthreads();
+  // ... and write them in increasing index order: position = kept entries at lower indices
+  const int kept = sh_kept;
+  for (int i = tid; i < kept; i += kBsThreads) {
+    const int32_t ii = sidx[i];
+    int pos = 0;
+    for (int j = 0; j < kept; ++j) pos += sidx[j] < ii;
+    out_idx[pos] = ii;
+    out_val[pos] = reinterpret_cast<const float*>(lkey)[i];
+  }
+  if (tid == 0) {
+    out_nnz[b] = kept;
+    done[b] = 1;
+    if (stats) {
+      atomicAdd(&stats[0], 1);
+      atomicAdd(&stats[2], n);
+      atomicMax(&stats[3], n);
+    }
+  }
+}
+
 // T4: merge of the shards' local top-s lists (column-sharded batched path): the global
 // top-s is contained in the union of the local top-s (same tie rule), and the shards'
 // lists concatenated in shard order are in increasing global index order.
@@ -1298,7 +1450,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
                           const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
                           int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
                           int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream,
-                          bool ws_prezeroed);
+                          bool ws_prezeroed, const int* skip = nullptr);
 
 int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                              const float* g, float mu, const float* mu_dev, int32_t s, int64_t N, int64_t col_offset,
@@ -1306,6 +1458,27 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
                              int64_t ws_bytes, void* stream) {
   return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, mu_dev, s, N, col_offset, nrhs, out_idx,
                         out_val, ldo, out_nnz, ws, ws_bytes, stream, true);   // the solver's workspace
+}
+
+int iht_threshold_bounded(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
+                          const float* g, float mu, float bound, int32_t s, int64_t N, int32_t nrhs,
+                          const int32_t* cidx, const float* cval, int* ccnt, int32_t ccap, int* done, int* stats,
+                          int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
+                          void* stream) {
+  if (!iht_threshold_bounded_applies(N, s, nrhs) || cidx == nullptr || cval == nullptr || ccnt == nullptr ||
+      done == nullptr || ccap <= 0 || x_nnz == nullptr || g == nullptr || ldx < 0 || ldo < s)
+    return IHT_EINVAL;
+  if (!isfinite(mu) || !isfinite(bound)) return IHT_EDOMAIN;
+  const int32_t max_nnz = ldx < s ? ldx : s;
+  IHT_CUDA_CHECK(launch_pdl(thr_bounded_select, dim3(nrhs), dim3(kBsThreads), 0, (cudaStream_t)stream, x_idx, x_val,
+                            x_nnz, max_nnz, ldx, g, mu, bound, s, N, cidx, cval, ccnt, (int)ccap, out_idx, out_val, ldo,
+                            out_nnz, done, stats));
+  return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, nullptr, s, N, 0, nrhs, out_idx, out_val,
+                        ldo, out_nnz, ws, ws_bytes, stream, true, done);
+}
+
+bool iht_threshold_bounded_applies(int64_t N, int32_t s, int32_t nrhs) {
+  return !thr_grid_path(N, nrhs) && s > 0 && s <= kBsMaxS && (int64_t)s < N && nrhs > 0 && nrhs <= 65535;
 }
 
 int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
@@ -1321,7 +1494,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
                           const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
                           int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
                           int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream,
-                          bool ws_prezeroed) {
+                          bool ws_prezeroed, const int* skip) {
   if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr ||
       s < 0 || N <= 0 || N > 0x7FFFFFFFll || nrhs <= 0 || nrhs > 65535 || ldo < s || ldx < 0 ||
       col_offset < 0 || col_offset + N > 0x7FFFFFFFll)
@@ -1363,7 +1536,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
     lc.numAttrs = 2;
     IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
                                       N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe(), nparts,
-                                      gsigma, gout, thr_timeline()));
+                                      gsigma, gout, thr_timeline(), skip));
     if (thr_timeline()) {   // profiling: per-phase times of ranks 0, 1 of snapshot 0 (stderr)
       static long long h[32];
       cudaStreamSynchronize(st);

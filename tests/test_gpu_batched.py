@@ -350,3 +350,69 @@ def test_batched_solver_nan_snapshot_isolated():
     keep = [b for b in range(B) if b != 5]
     assert torch.equal(gn[keep], rn[keep]) and torch.equal(gi[keep], ri[keep]) and torch.equal(gv[keep], rv[keep])
     sol.close()
+
+
+# ------------------------------------------------------------------ bounded select (config 5)
+def _bounded_runs(pool, p, Y, B, n_iter, monkeypatch, capfd, bound="0.5"):
+    """The batched solver's trace with the bounded select off and on (IHT_BOUNDED, read at
+    every create), and the on-run's decided / fallen-back counts (IHT_BOUNDED_STATS)."""
+    runs = []
+    monkeypatch.setenv("IHT_BOUND", bound)
+    monkeypatch.setenv("IHT_BOUNDED_STATS", "1")
+    for on in ("0", "1"):
+        monkeypatch.setenv("IHT_BOUNDED", on)
+        sol = iht.Solver(pool, p.s, n_iter, p.mu, p.b_y, p.seed, trace=True, nrhs=B)
+        sol.run(_to_dev(Y))
+        torch.cuda.synchronize()
+        runs.append(tuple(t.clone() for t in sol.trace_arrays()))
+        sol.close()
+    import re
+    m = re.search(r"bounded select: decided (\d+), fell back (\d+)", capfd.readouterr().err)
+    assert m, "the bounded select did not run"
+    return runs, int(m.group(1)), int(m.group(2))
+
+
+@pytest.mark.parametrize("B,bound", [(16, "0.5"), (64, "0.9"), (5, "0.3")])
+def test_batched_bounded_select_bit_identical(B, bound, monkeypatch, capfd):
+    """Bounded select (epilogue candidates + thr_bounded_select, cluster kernel only for the
+    snapshots it cannot decide) against the cluster kernel alone: every iterate of every
+    snapshot bit-identical (both are exact H_s of the same fp32 a), and the bounded path
+    decides most snapshot-iterations after the first."""
+    n_iter = 24
+    p, Y = _radio_batch(B, n_iter=n_iter, K=40)
+    pool = iht.quantize(_to_dev(p.phi), p.b_phi, 0, p.seed, list(range(p.K)), float(OQ.scale_c(p.phi)))
+    (off, on), dec, fb = _bounded_runs(pool, p, Y, B, n_iter, monkeypatch, capfd, bound)
+    for a, b in zip(off, on):
+        assert torch.equal(a, b)
+    assert dec + fb == B * n_iter
+    assert fb >= B                          # iteration 1 (x = 0) always falls back
+    assert dec >= B * n_iter // 2, (dec, fb)
+
+
+def test_batched_bounded_select_nan_snapshot(monkeypatch, capfd):
+    """A NaN snapshot falls back (its candidates overflow / carry NaN) and reports nnz = -1;
+    the others are unaffected and identical to the cluster-only run."""
+    B, n_iter = 8, 6
+    p, Y = _radio_batch(B, n_iter=n_iter, K=12)
+    Y = Y.copy()
+    Y[3, 5] = np.nan
+    pool = iht.quantize(_to_dev(p.phi), p.b_phi, 0, p.seed, list(range(p.K)), float(OQ.scale_c(p.phi)))
+    (off, on), dec, fb = _bounded_runs(pool, p, Y, B, n_iter, monkeypatch, capfd)
+    for a, b in zip(off, on):
+        assert torch.equal(a, b)
+    assert int(on[2][n_iter - 1, 3]) == -1
+
+
+def test_config5_bounded_select_bit_identical(monkeypatch, capfd):
+    """The same at BASELINE config 5's full shape (64 snapshots of the 2304 x 65536 radio Phi,
+    2-bit, K = 2 copies), 40 iterations."""
+    from paper_1802_04907_b200.problem import build_pool
+    p5 = G.config_problem(5, K=2)
+    B, n_iter = 64, 40
+    Y = np.ascontiguousarray(p5.meta["batch_y"][:, :B].T)
+    pool, _, _, _, _ = build_pool(p5, 0, 1, _dev(), False, shard="cols")
+    (off, on), dec, fb = _bounded_runs(pool, p5, Y, B, n_iter, monkeypatch, capfd)
+    for a, b in zip(off, on):
+        assert torch.equal(a, b)
+    print(f"config 5 bounded select: decided {dec}, fell back {fb} of {B * n_iter}")
+    assert dec >= B * n_iter // 2, (dec, fb)

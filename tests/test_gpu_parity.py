@@ -133,11 +133,13 @@ def test_forward_parity(M, N, cplx, bits, s):
 @pytest.mark.parametrize("M,N,cplx,bits,s,nnz", [(40000, 600, False, 4, 600, 600), (40000, 600, False, 4, 300, 300),
                                                   (40000, 600, False, 4, 600, 555), (80000, 400, False, 2, 400, 400),
                                                   (20000, 1100, False, 8, 1100, 1037), (20000, 300, True, 4, 300, 300)])
-def test_forward_split_parity(M, N, cplx, bits, s, nnz):
-    """The row-block x column-group forward (>= 296 row blocks: config-4-like rows) incl. G > 1
+def test_forward_split_parity(M, N, cplx, bits, s, nnz, monkeypatch):
+    """The row-block x column-group forward (IHT_FWD_SPLIT=1; measured slower than forward_kernel
+    at config 4, so not the default) on >= 296 row blocks (config-4-like rows) incl. G > 1
     column groups summed by the last CTA of each row block, a ragged nnz < max_nnz, 2/4/8 bits
     and complex rows: r within 1e-4 of the oracle's forward; repeated calls reuse the zeroed
     workspace (the arrival counters are reset by the kernel) and give identical bits."""
+    monkeypatch.setenv("IHT_FWD_SPLIT", "1")
     phi = _phi(M, N, cplx, seed=5)
     c = OQ.scale_c(phi)
     (F,) = iht.quantize(_to_dev(phi), bits, 0, SEED, [1], float(c))
