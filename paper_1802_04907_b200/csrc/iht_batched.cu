@@ -156,10 +156,8 @@ struct BatchArgs {
   float* cval;             // [Breal][ccap]  mu g
   int* ccnt;               // [Breal] (zero on entry; the select kernel resets it)
   int ccap;
-  float mu, bound;
-  const float* xval;       // x^[n] of the chunk's snapshots: [Breal][ldx]
-  const int32_t* xnnz;     // [Breal]
-  int ldx, max_nnz;
+  float mu;
+  const unsigned int* bkey;   // [Breal] bound keys (batched_limbs_kernel, from x^[n])
 };
 
 template <int BITS>
@@ -457,13 +455,8 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
     // ---------------------------------------------------------------- epilogue (warps 7-10)
     const int quarter = warp & 3;               // TMEM lanes 32*quarter .. +31
     if (a.cidx) {
-      // bound key of each snapshot (x^[n] was written before the forward this kernel waited on,
-      // transitively); the same function as thr_bounded_select, so both sides agree exactly
-      for (int b = warp - 7; b < a.Breal; b += 4) {
-        const int nnz = min(a.xnnz[b], a.max_nnz);
-        const unsigned int k = warp_bound_key(a.xval + (int64_t)b * a.ldx, nnz, a.bound);
-        if (lane == 0) ep_bkey[b] = k;
-      }
+      // the snapshots' bound keys (written by batched_limbs_kernel, which this kernel waited on)
+      for (int b = (warp - 7) * 32 + lane; b < a.Breal; b += 128) ep_bkey[b] = a.bkey[b];
       asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
     }
     int t = 0;
@@ -499,23 +492,36 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
           }
           if (n < a.N && b < a.Breal) a.g[(int64_t)b * a.N + n] = gv[e >> 1];
         }
-        if (a.cidx) {
-          // candidates: key(mu g) >= bkey_b (x's support is handled by the select kernel); one
-          // atomic per warp and snapshot with any, list order irrelevant (the select ranks)
+        if (a.cidx && !(a.probe & 128)) {             // probe 128: no candidate lists (timing)
+          // candidates: key(mu g) >= bkey_b (x's support is handled by the select kernel).  The
+          // 8 snapshots' flags are formed without a dependent chain (two 16-byte loads of their
+          // keys) and the warp votes once per chunk; only a chunk with a candidate (rare after the
+          // first iterations) walks its snapshots, one atomic per snapshot with any
+          const int b0 = (cbase + c0) >> 1;         // multiple of 4: 16-byte aligned keys
+          const uint4 k0 = *reinterpret_cast<const uint4*>(ep_bkey + b0);
+          const uint4 k1 = *reinterpret_cast<const uint4*>(ep_bkey + b0 + 4);
+          const unsigned int bk[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+          unsigned int fl = 0u;
+          float av[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int b = (cbase + c0) / 2 + e;
-            if (b >= a.Breal) break;                      // warp-uniform
-            const float av = __fmul_rn(a.mu, gv[e]);
-            const bool emit = n < a.N && (__float_as_uint(av) & 0x7FFFFFFFu) >= ep_bkey[b];
-            const unsigned int m = __ballot_sync(0xffffffffu, emit);
-            if (m) {
-              int base = 0;
-              if (lane == 0) base = atomicAdd(&a.ccnt[b], __popc(m));
-              base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
-              if (emit && base < a.ccap) {
-                a.cidx[(int64_t)b * a.ccap + base] = (int32_t)n;
-                a.cval[(int64_t)b * a.ccap + base] = av;
+            av[e] = __fmul_rn(a.mu, gv[e]);
+            fl |= (unsigned int)((__float_as_uint(av[e]) & 0x7FFFFFFFu) >= bk[e] && b0 + e < a.Breal) << e;
+          }
+          if (n >= a.N) fl = 0u;
+          if (__any_sync(0xffffffffu, fl != 0u)) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const unsigned int m = __ballot_sync(0xffffffffu, (fl >> e) & 1u);
+              if (m) {
+                const int b = b0 + e;
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&a.ccnt[b], __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
+                if (((fl >> e) & 1u) && base < a.ccap) {
+                  a.cidx[(int64_t)b * a.ccap + base] = (int32_t)n;
+                  a.cval[(int64_t)b * a.ccap + base] = av[e];
+                }
               }
             }
           }
@@ -539,15 +545,34 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
 // balanced signed limbs written into the pre-swizzled image, exact limb sums S_b.  A
 // thread owns 16 consecutive rows (one 16-byte K chunk of the image): it reads them as
 // four float4, permutes them into MMA K order in registers and writes two 16-byte stores.
+// With bkey (the bounded select, solver only): also the snapshot's bound key from x^[n]
+// (warp_bound_key), read by the GEMM's epilogue and by thr_bounded_select.
 template <int BITS>
 __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nreal,
                                                             int nkb, uint8_t* __restrict__ bimg, int* __restrict__ Fb,
-                                                            int* __restrict__ Sb) {
+                                                            int* __restrict__ Sb, const float* __restrict__ xval,
+                                                            const int32_t* __restrict__ xnnz, int ldx, int max_nnz,
+                                                            float bound, unsigned int* __restrict__ bkey) {
   constexpr int KBR = BCfg<BITS>::KBR;
   pdl_launch_dependents();
   pdl_wait();                               // R (forward)
   const int b = blockIdx.x;                 // b >= nreal: zero padding snapshot (MMA N granularity)
   const bool live = b < nreal;
+  // bound key: the last warp requests x's values (<= 256 of them: s <= kBsMaxS) before its r
+  // loads and reduces them after the max pass, so the x round trip overlaps the r one
+  const bool kw = bkey && live && threadIdx.x >= 224;
+  int xn = 0;
+  unsigned int xk[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) xk[k] = 0xFFFFFFFFu;
+  if (kw) {                                 // all ldx slots requested at once, masked by nnz later
+    xn = xnnz[b];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = (threadIdx.x & 31) + 32 * k;
+      if (j < ldx) xk[k] = __float_as_uint(xval[(int64_t)b * ldx + j]) & 0x7FFFFFFFu;
+    }
+  }
   const float* r = R + (int64_t)(live ? b : 0) * Rpad;
   __shared__ float red[8];
   __shared__ int ired[2][8];
@@ -572,6 +597,14 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
     }
   }
   m = __reduce_max_sync(0xffffffffu, m);
+  if (kw) {
+    xn = min(xn, max_nnz);                  // < 0 (poisoned): no candidates
+    unsigned int mk = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mk = min(mk, (threadIdx.x & 31) + 32 * k < xn ? xk[k] : 0xFFFFFFFFu);
+    mk = __reduce_min_sync(0xffffffffu, mk);
+    if (threadIdx.x == 224) bkey[b] = bound_key(mk, xn, bound);
+  }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = __uint_as_float(m);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -751,18 +784,17 @@ int iht_adjoint_batched_cand(const iht_qmat* A, const float* R, int32_t nrhs, fl
       b.ccnt = cand->ccnt + c0;
       b.ccap = cand->ccap;
       b.mu = cand->mu;
-      b.bound = cand->bound;
-      b.xval = cand->x_val + (int64_t)c0 * cand->ldx;
-      b.xnnz = cand->x_nnz + c0;
-      b.ldx = cand->ldx;
-      b.max_nnz = cand->max_nnz;
+      b.bkey = cand->bkey + c0;
     }
     const float* Rc = R + (int64_t)c0 * Rpad;
     const size_t smem = batched_smem(A->bits, bp);
 #define IHT_BATCH(BB)                                                                                  \
   do {                                                                                                 \
     IHT_CUDA_CHECK(launch_pdl(batched_limbs_kernel<BB>, dim3(bp), dim3(256), 0, st, Rc, (int)Rpad, bp, nb, \
-                              nkb, bimg, Fb, Sb));                                                     \
+                              nkb, bimg, Fb, Sb, cand ? cand->x_val + (int64_t)c0 * cand->ldx : nullptr,   \
+                              cand ? cand->x_nnz + c0 : nullptr, cand ? cand->ldx : 0,                     \
+                              cand ? cand->max_nnz : 0, cand ? cand->bound : 0.0f,                         \
+                              cand ? cand->bkey + c0 : nullptr));                                          \
     static bool attr = false;                                                                          \
     if (!attr) {                                                                                       \
       IHT_CUDA_CHECK(cudaFuncSetAttribute(adjoint_batched_kernel<BB>,                                  \

@@ -64,7 +64,7 @@ int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t*
 // cluster kernel for the snapshots it could not decide (done[b] = 0).  stats (may be NULL):
 // [0] decided, [1] fallen back, [2] sum of list sizes, [3] max list size.
 int iht_threshold_bounded(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
-                          const float* g, float mu, float bound, int32_t s, int64_t N, int32_t nrhs,
+                          const float* g, float mu, const unsigned int* bkey, int32_t s, int64_t N, int32_t nrhs,
                           const int32_t* cidx, const float* cval, int* ccnt, int32_t ccap, int* done, int* stats,
                           int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
                           void* stream);
@@ -79,6 +79,7 @@ struct iht_cand_args {
   const float* x_val;
   const int32_t* x_nnz;
   int32_t ldx, max_nnz;
+  unsigned int* bkey;   // [nrhs] bound keys written by the limb kernel, read by the epilogue and the select
 };
 int iht_adjoint_batched_cand(const iht_qmat* A, const float* R, int32_t nrhs, float* G, void* ws, int64_t ws_bytes,
                              void* stream, const iht_cand_args* cand);
@@ -178,16 +179,12 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t m, uint32_t
   return d;
 }
 
-// Bound key of the bounded candidate select (config 5; iht_batched.cu epilogue and
-// thr_bounded_select): the key (|.| bit pattern) of bound x min_j |x_j| over x's support, or
-// 0xFFFFFFFF (no candidates, the select falls back to the full path) when x is empty or
-// poisoned or the bound underflows.  Warp-collective; the min is exact, so every caller gets
-// the same key.
-__device__ __forceinline__ unsigned int warp_bound_key(const float* xv, int nnz, float bound) {
-  const int lane = threadIdx.x & 31;
-  unsigned int m = 0xFFFFFFFFu;
-  for (int j = lane; j < nnz; j += 32) m = min(m, __float_as_uint(xv[j]) & 0x7FFFFFFFu);
-  m = __reduce_min_sync(0xffffffffu, m);
+// Bound key of the bounded candidate select (config 5; batched_limbs_kernel writes it, the
+// tcgen05 epilogue lists against it, thr_bounded_select decides with it): the key (|.| bit
+// pattern) of bound x m, m = min_j |x_j| over x's support as a key, or 0xFFFFFFFF (no
+// candidates: the select falls back to the full path) when x is empty or poisoned or the
+// bound underflows.
+__device__ __forceinline__ unsigned int bound_key(unsigned int m, int nnz, float bound) {
   if (nnz <= 0 || m >= 0x7F800000u) return 0xFFFFFFFFu;
   const unsigned int k = __float_as_uint(__fmul_rn(bound, __uint_as_float(m))) & 0x7FFFFFFFu;
   return k == 0u ? 0xFFFFFFFFu : k;

@@ -203,11 +203,12 @@ struct iht_solver {
   iht_fused_state* fused = nullptr;    // the whole loop as one persistent kernel (iht_fused.cu)
   // bounded select (batched, fixed step): epilogue candidate lists + per-snapshot decided flags
   bool bounded = false;
-  float bound = 0.5f;
+  float bound = 0.7f;
   int32_t* bc_idx = nullptr;   // [B][kBcCap]
   float* bc_val = nullptr;     // [B][kBcCap]
   int* bc_cnt = nullptr;       // [B] (zeroed at create, reset by the select kernel)
   int* bc_done = nullptr;      // [B]
+  unsigned int* bc_bkey = nullptr;   // [B] bound keys
   int* bc_stats = nullptr;     // [4] decided, fallen back, sum / max list size (IHT_BOUNDED_STATS)
 };
 
@@ -215,15 +216,17 @@ struct iht_solver {
 static constexpr int kBcCap = 1024;
 
 // IHT_BOUNDED=0 turns the bounded select off (A/B and the bit-identity test); IHT_BOUND sets
-// the bound factor (default 0.5 x the smallest kept |x|).  Read at every solver create.
+// the bound factor (default 0.7 x the smallest kept |x|; measured at config 5, r02 g52/g54:
+// 0.5 -> lists of ~208 and slower ranking, 0.9 -> 5 % of the snapshot-iterations fall back,
+// 0.7 / 0.8 -> 16.5k / 16.4k iter/s against 15.1k without).  Read at every solver create.
 static bool bounded_enabled() {
   const char* e = getenv("IHT_BOUNDED");
   return e == nullptr || atoi(e) != 0;
 }
 static float bounded_factor() {
   const char* e = getenv("IHT_BOUND");
-  const float f = e ? (float)atof(e) : 0.5f;
-  return f > 0.0f && f < 1.0f ? f : 0.5f;
+  const float f = e ? (float)atof(e) : 0.7f;
+  return f > 0.0f && f < 1.0f ? f : 0.7f;
 }
 
 // Event record that survives stream capture: inside a capture it becomes an event-record
@@ -407,7 +410,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       L += (S->cfg.adjoint_variant == 0 && S->ws_adj_bytes > 0) ? 2 : 1;
     } else if (S->bounded) {
       // the epilogue also lists each snapshot's candidates for the bounded select below
-      iht_cand_args ca{S->bc_idx, S->bc_val, S->bc_cnt, kBcCap, S->cfg.mu, S->bound, xv, xn, s, s};
+      iht_cand_args ca{S->bc_idx, S->bc_val, S->bc_cnt, kBcCap, S->cfg.mu, S->bound, xv, xn, s, s, S->bc_bkey};
       if ((rc = iht_adjoint_batched_cand(&A, S->r, B, S->g, S->ws_adj, S->ws_adj_bytes, st, &ca)) != IHT_OK)
         return rc;
       L += 2 * ((B + 63) / 64);
@@ -446,7 +449,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
         return rc;
       L += 1;
     } else if (S->bounded) {
-      if ((rc = iht_threshold_bounded(xi, xv, xn, s, S->g, S->cfg.mu, S->bound, s, S->N, B, S->bc_idx, S->bc_val,
+      if ((rc = iht_threshold_bounded(xi, xv, xn, s, S->g, S->cfg.mu, S->bc_bkey, s, S->N, B, S->bc_idx, S->bc_val,
                                       S->bc_cnt, kBcCap, S->bc_done, S->bc_stats, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
@@ -588,7 +591,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
   S->bounded = batched && !S->colshard && !fm && cfg->step_mode == 0 && B <= 64 &&
                iht_threshold_bounded_applies(S->N, cfg->s, B) && bounded_enabled();
   S->bound = bounded_factor();
-  const int64_t sz_bc = S->bounded ? 2 * al((int64_t)B * kBcCap * 4) + 2 * sz_b4 + al(16) : 0;
+  const int64_t sz_bc = S->bounded ? 2 * al((int64_t)B * kBcCap * 4) + 3 * sz_b4 + al(16) : 0;
   const int64_t total = sz_y + sz_c + 2 * sz_v + sz_g + sz_wa + sz_wt + sz_wf + sz_xi + sz_xv + sz_xn +
                         ((S->colshard || S->shardsel) ? sz_cs + sz_cr : 0) + sz_ad + sz_bc;
   if (cudaMalloc(&S->block, total) != cudaSuccess) {
@@ -637,6 +640,7 @@ static int solver_create_impl(const iht_qmat* pool, int K, const iht_config* cfg
     S->bc_val = reinterpret_cast<float*>(p); p += al((int64_t)B * kBcCap * 4);
     S->bc_cnt = reinterpret_cast<int*>(p); p += sz_b4;
     S->bc_done = reinterpret_cast<int*>(p); p += sz_b4;
+    S->bc_bkey = reinterpret_cast<unsigned int*>(p); p += sz_b4;
     S->bc_stats = getenv("IHT_BOUNDED_STATS") ? reinterpret_cast<int*>(p) : nullptr; p += al(16);
   }
   // zero everything once (pad rows of the stacked vectors stay 0)

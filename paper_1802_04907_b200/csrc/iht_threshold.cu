@@ -1166,7 +1166,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
 }
 
 // Bounded select (config 5, solver only): the tcgen05 adjoint's epilogue appended every
-// pixel n with key(mu g_n) >= bkey = bound_key(x) to this snapshot's list (cidx, cval, ccnt;
+// pixel n with key(mu g_n) >= bkey = bound_key(x) (batched_limbs_kernel) to this snapshot's list (cidx, cval, ccnt;
 // iht_batched.cu).  With x's support added (a_j = x_j + mu g_j, the cluster kernel's
 // arithmetic) and the support's own epilogue entries dropped, the list holds every pixel
 // whose key is >= bkey.  If at least s of its keys are >= bkey, the s-th largest key of a is
@@ -1181,16 +1181,17 @@ constexpr int kBsMaxS = 256;
 
 __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
-    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, float bound, int s, int64_t N,
-    const int32_t* __restrict__ cidx, const float* __restrict__ cval, int* __restrict__ ccnt, int ccap,
-    int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz,
+    int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const unsigned int* __restrict__ bkeys,
+    int s, int64_t N, const int32_t* __restrict__ cidx, const float* __restrict__ cval, int* __restrict__ ccnt,
+    int ccap, int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz,
     int* __restrict__ done, int* __restrict__ stats) {
-  __shared__ int32_t lidx[kBsCap];
-  __shared__ unsigned int lkey[kBsCap];
+  constexpr int PER = kBsCap / kBsThreads;      // list slots per thread
+  __shared__ __align__(16) int32_t lidx[kBsCap + 4];
+  __shared__ __align__(16) unsigned int lkey[kBsCap + 4];
   __shared__ float lval[kBsCap];
-  __shared__ int32_t sidx[kBsMaxS];
-  __shared__ int sh_n, sh_t, sh_bad, sh_cnt, sh_kept;
-  __shared__ unsigned int sh_bkey;
+  __shared__ __align__(16) int32_t sidx[kBsMaxS + 4];
+  __shared__ float kval[kBsMaxS];
+  __shared__ int sh_n, sh_t, sh_bad, sh_kept;
   pdl_launch_dependents();
   pdl_wait();                                   // g and the lists (adjoint), x (previous H_s)
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -1201,61 +1202,86 @@ __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
   cval += (int64_t)b * ccap;
   out_idx += (int64_t)b * ldo;
   out_val += (int64_t)b * ldo;
+  // one round trip: the counts, the bound key, x's slots and the first list slots, all at once
+  // (slots past the counts are masked below)
   const int nraw = x_nnz[b];
-  const int nnz = nraw < 0 ? 0 : min(nraw, max_nnz);
-  if (tid < 32) {
-    const unsigned int k = warp_bound_key(x_val, nraw < 0 ? -1 : nnz, bound);
-    if (tid == 0) {
-      sh_bkey = k;
-      sh_cnt = ccnt[b];
-      sh_n = 0;
-      sh_t = 0;
-      sh_bad = 0;
-      sh_kept = 0;
-    }
+  const int cnt = ccnt[b];
+  const unsigned int bkey = bkeys[b];             // the key the epilogue listed against
+  const int32_t xi = tid < max_nnz ? x_idx[tid] : 0;
+  const float xv = tid < max_nnz ? x_val[tid] : 0.0f;
+  int32_t ci[PER];
+  float cv[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kBsThreads;
+    ci[u] = i < ccap ? cidx[i] : 0;
+    cv[u] = i < ccap ? cval[i] : 0.0f;
   }
-  __syncthreads();
-  if (tid == 0) ccnt[b] = 0;                    // zero for the next call (read above)
-  const int cnt = sh_cnt;
-  const unsigned int bkey = sh_bkey;
-  if (bkey == 0xFFFFFFFFu || s <= 0 || s > kBsMaxS || nnz > kBsMaxS || cnt > ccap || (int64_t)s >= N ||
-      nnz + cnt > kBsCap) {
+  const int nnz = nraw < 0 ? 0 : min(nraw, max_nnz);
+  if (tid == 0) {
+    sh_n = nnz;
+    sh_t = 0;
+    sh_bad = 0;
+    sh_kept = 0;
+  }
+  __syncthreads();                              // every thread has read ccnt
+  if (tid == 0) ccnt[b] = 0;                    // zero for the next call
+  if (nraw < 0 || bkey == 0xFFFFFFFFu || s <= 0 || s > kBsMaxS || nnz > kBsMaxS || cnt > ccap || (int64_t)s >= N ||
+      nnz + cnt > kBsCap || max_nnz > kBsThreads) {
     if (tid == 0) {
       done[b] = 0;
       if (stats) atomicAdd(&stats[1], 1);
     }
     return;
   }
-  // x's support: a_j = x_j + mu g_j (as the cluster kernel forms it)
-  for (int j = tid; j < nnz; j += kBsThreads) {
-    const int32_t c = x_idx[j];
-    const float av = __fadd_rn(x_val[j], __fmul_rn(mu, __ldg(g + c)));
-    sidx[j] = c;
-    lidx[j] = c;
-    lval[j] = av;
-    lkey[j] = __float_as_uint(av) & 0x7FFFFFFFu;
+  // x's support: a_j = x_j + mu g_j (the cluster kernel's arithmetic); the g gather is issued
+  // before the membership tests below
+  float gj = 0.0f;
+  if (tid < nnz) {
+    gj = __ldg(g + xi);
+    sidx[tid] = xi;
   }
-  if (tid == 0) sh_n = nnz;
+  if (tid < 4) sidx[nnz + tid] = -1;            // pad to whole int4 (never a column)
   __syncthreads();
-  // the epilogue's entries outside the support (a = mu g there); order is irrelevant
-  for (int i = tid; i < cnt; i += kBsThreads) {
-    const int32_t c = cidx[i];
-    bool in = false;
-    for (int j = 0; j < nnz; ++j) in |= sidx[j] == c;
-    if (!in) {
-      const int p = atomicAdd(&sh_n, 1);
-      const float av = cval[i];
-      lidx[p] = c;
-      lval[p] = av;
-      lkey[p] = __float_as_uint(av) & 0x7FFFFFFFu;
+  // the epilogue's entries outside the support (a = mu g there); list order is irrelevant
+  const int nq = (nnz + 3) >> 2;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kBsThreads;
+    if (i < cnt) {
+      bool in = false;
+      for (int q = 0; q < nq; ++q) {
+        const int4 v = reinterpret_cast<const int4*>(sidx)[q];
+        in |= (v.x == ci[u]) | (v.y == ci[u]) | (v.z == ci[u]) | (v.w == ci[u]);
+      }
+      if (!in) {
+        const int p = atomicAdd(&sh_n, 1);
+        lidx[p] = ci[u];
+        lval[p] = cv[u];
+        lkey[p] = __float_as_uint(cv[u]) & 0x7FFFFFFFu;
+      }
     }
+  }
+  if (tid < nnz) {
+    const float av = __fadd_rn(xv, __fmul_rn(mu, gj));
+    lidx[tid] = xi;
+    lval[tid] = av;
+    lkey[tid] = __float_as_uint(av) & 0x7FFFFFFFu;
   }
   __syncthreads();
   const int n = sh_n;
+  if (tid < 4) {                                // pad to whole uint4: key 0, never before anything
+    lkey[n + tid] = 0u;
+    lidx[n + tid] = 0x7FFFFFFF;
+  }
   int t = 0, bad = 0;
-  for (int i = tid; i < n; i += kBsThreads) {
-    t += lkey[i] >= bkey;
-    bad |= lkey[i] > 0x7F800000u;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * kBsThreads;
+    if (i < n) {
+      t += lkey[i] >= bkey;
+      bad |= lkey[i] > 0x7F800000u;
+    }
   }
   if (t) atomicAdd(&sh_t, t);
   if (bad) sh_bad = 1;
@@ -1267,43 +1293,43 @@ __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
     }
     return;
   }
-  // rank = keys greater, or equal at a lower index; kept iff rank < s (all kept keys >= bkey > 0)
-  bool keep[(kBsCap + kBsThreads - 1) / kBsThreads];
+  // rank = keys greater, or equal at a lower index (4 entries per shared load); kept iff
+  // rank < s -- then rank < s <= the count of keys >= bkey > 0, so every kept key is >= bkey
+  const int n4 = (n + 3) >> 2;
 #pragma unroll
-  for (int u = 0; u < (kBsCap + kBsThreads - 1) / kBsThreads; ++u) {
+  for (int u = 0; u < PER; ++u) {
     const int i = tid + u * kBsThreads;
-    keep[u] = false;
     if (i < n) {
       const unsigned int ki = lkey[i];
       const int32_t ii = lidx[i];
       int rk = 0;
-      for (int j = 0; j < n && rk < s; ++j) {
-        const unsigned int kj = lkey[j];
-        rk += kj > ki || (kj == ki && lidx[j] < ii);
+      for (int q = 0; q < n4; ++q) {
+        const uint4 k4 = reinterpret_cast<const uint4*>(lkey)[q];
+        const int4 i4 = reinterpret_cast<const int4*>(lidx)[q];
+        rk += (k4.x > ki || (k4.x == ki && i4.x < ii)) + (k4.y > ki || (k4.y == ki && i4.y < ii)) +
+              (k4.z > ki || (k4.z == ki && i4.z < ii)) + (k4.w > ki || (k4.w == ki && i4.w < ii));
       }
-      keep[u] = rk < s;
+      if (rk < s) {
+        const int p = atomicAdd(&sh_kept, 1);
+        sidx[p] = ii;                           // sidx is free (membership tests done)
+        kval[p] = lval[i];
+      }
     }
   }
   __syncthreads();
-  // compact the kept entries (s of them) to the front of the list, any order ...
-#pragma unroll
-  for (int u = 0; u < (kBsCap + kBsThreads - 1) / kBsThreads; ++u) {
-    const int i = tid + u * kBsThreads;
-    if (keep[u]) {
-      const int p = atomicAdd(&sh_kept, 1);
-      sidx[p] = lidx[i];
-      reinterpret_cast<float*>(lkey)[p] = lval[i];   // lkey is free now (ranks done)
-    }
-  }
-  __syncthreads();
-  // ... and write them in increasing index order: position = kept entries at lower indices
+  // write the kept entries in increasing index order: position = kept entries at lower indices
   const int kept = sh_kept;
-  for (int i = tid; i < kept; i += kBsThreads) {
-    const int32_t ii = sidx[i];
+  if (tid < 4) sidx[kept + tid] = 0x7FFFFFFF;
+  __syncthreads();
+  if (tid < kept) {
+    const int32_t ii = sidx[tid];
     int pos = 0;
-    for (int j = 0; j < kept; ++j) pos += sidx[j] < ii;
+    for (int q = 0; q < ((kept + 3) >> 2); ++q) {
+      const int4 v = reinterpret_cast<const int4*>(sidx)[q];
+      pos += (v.x < ii) + (v.y < ii) + (v.z < ii) + (v.w < ii);
+    }
     out_idx[pos] = ii;
-    out_val[pos] = reinterpret_cast<const float*>(lkey)[i];
+    out_val[pos] = kval[tid];
   }
   if (tid == 0) {
     out_nnz[b] = kept;
@@ -1461,17 +1487,17 @@ int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int
 }
 
 int iht_threshold_bounded(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
-                          const float* g, float mu, float bound, int32_t s, int64_t N, int32_t nrhs,
+                          const float* g, float mu, const unsigned int* bkey, int32_t s, int64_t N, int32_t nrhs,
                           const int32_t* cidx, const float* cval, int* ccnt, int32_t ccap, int* done, int* stats,
                           int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
                           void* stream) {
   if (!iht_threshold_bounded_applies(N, s, nrhs) || cidx == nullptr || cval == nullptr || ccnt == nullptr ||
-      done == nullptr || ccap <= 0 || x_nnz == nullptr || g == nullptr || ldx < 0 || ldo < s)
+      done == nullptr || bkey == nullptr || ccap <= 0 || x_nnz == nullptr || g == nullptr || ldx < 0 || ldo < s)
     return IHT_EINVAL;
-  if (!isfinite(mu) || !isfinite(bound)) return IHT_EDOMAIN;
+  if (!isfinite(mu)) return IHT_EDOMAIN;
   const int32_t max_nnz = ldx < s ? ldx : s;
   IHT_CUDA_CHECK(launch_pdl(thr_bounded_select, dim3(nrhs), dim3(kBsThreads), 0, (cudaStream_t)stream, x_idx, x_val,
-                            x_nnz, max_nnz, ldx, g, mu, bound, s, N, cidx, cval, ccnt, (int)ccap, out_idx, out_val, ldo,
+                            x_nnz, max_nnz, ldx, g, mu, bkey, s, N, cidx, cval, ccnt, (int)ccap, out_idx, out_val, ldo,
                             out_nnz, done, stats));
   return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, nullptr, s, N, 0, nrhs, out_idx, out_val,
                         ldo, out_nnz, ws, ws_bytes, stream, true, done);
