@@ -59,9 +59,10 @@ int iht_threshold_parts(const int32_t* x_idx, const float* x_val, const int32_t*
                         const float* g, int nparts, float gsigma, float* gout, float mu, int32_t s, int64_t N,
                         int32_t* out_idx, float* out_val, int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes,
                         void* stream);
-// Bounded select (batched solver, fixed step, cluster path): thr_bounded_select on the
-// candidate lists the tcgen05 adjoint's epilogue wrote (iht_adjoint_batched_cand), then the
-// cluster kernel for the snapshots it could not decide (done[b] = 0).  stats (may be NULL):
+// Bounded select (batched solver, fixed step, cluster-sized N): thr_bounded_select on the
+// candidate lists the tcgen05 adjoint's epilogue wrote (iht_adjoint_batched_cand); a snapshot
+// the list cannot decide (done[b] = 0) is selected over all of a by the same CTA, in the
+// workspace's a buffers (ws: iht_threshold_batched_ws_bytes(N, s, nrhs)).  stats (may be NULL):
 // [0] decided, [1] fallen back, [2] sum of list sizes, [3] max list size.
 int iht_threshold_bounded(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                           const float* g, float mu, const unsigned int* bkey, int32_t s, int64_t N, int32_t nrhs,

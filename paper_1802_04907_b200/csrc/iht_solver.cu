@@ -453,7 +453,7 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
                                       S->bc_cnt, kBcCap, S->bc_done, S->bc_stats, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)
         return rc;
-      L += 1 + iht_threshold_launches(S->N);
+      L += 1;
     } else if (!S->colshard) {
       if ((rc = iht_threshold_batched_mu(xi, xv, xn, s, S->g, S->cfg.mu, nullptr, s, S->N, 0, B, oi, ov, s, on, S->ws_thr,
                                       S->ws_thr_bytes, st)) != IHT_OK)

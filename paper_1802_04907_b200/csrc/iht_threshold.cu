@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const float* __restrict__ mu_dev, int s,
     int64_t N, int64_t col_offset, int slice, int32_t* __restrict__ out_idx, float* __restrict__ out_val,
     int32_t ldo, int32_t* __restrict__ out_nnz, int probe, int nparts, float gsigma, float* __restrict__ gout,
-    long long* __restrict__ tl, const int* __restrict__ skip) {
+    long long* __restrict__ tl) {
   // profiling timeline (IHT_THR_TL): globaltimer stamps of CTA ranks 0, 1 of snapshot 0
   auto stamp = [&](int k) {
     if (tl && threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 2) {
@@ -852,7 +852,6 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_launch_dependents();
   pdl_wait();                                   // g (adjoint) and x (previous H_s)
-  if (skip && skip[blockIdx.y]) return;         // snapshot already selected by thr_bounded_select
   if (mu_dev) mu = mu_dev[blockIdx.y];          // the adaptive step's mu: a predecessor's output too
   stamp(0);
   const int b = blockIdx.y;
@@ -1166,29 +1165,157 @@ __global__ void __launch_bounds__(kClThreads, 1) thr_cluster_kernel(
 }
 
 // Bounded select (config 5, solver only): the tcgen05 adjoint's epilogue appended every
-// pixel n with key(mu g_n) >= bkey = bound_key(x) (batched_limbs_kernel) to this snapshot's list (cidx, cval, ccnt;
-// iht_batched.cu).  With x's support added (a_j = x_j + mu g_j, the cluster kernel's
-// arithmetic) and the support's own epilogue entries dropped, the list holds every pixel
-// whose key is >= bkey.  If at least s of its keys are >= bkey, the s-th largest key of a is
-// >= bkey too, so every entry of H_s(a) -- including the lowest-index ties at the threshold --
-// is in the list, and the top-s of the list (greater key, then lower index) IS H_s(a), exactly
-// (P:135).  Otherwise (iteration 1, a support change larger than the bound, list
-// overflow, NaN, poisoned x) done[b] = 0 and the cluster kernel that follows selects the
-// snapshot over all of a.  One CTA per snapshot; resets ccnt for the next call.
+// pixel n with key(mu g_n) >= bkey = bound_key(x) (batched_limbs_kernel) to this snapshot's list
+// (cidx, cval, ccnt; iht_batched.cu).  With x's support added (a_j = x_j + mu g_j, the cluster
+// kernel's arithmetic) and the support's own epilogue entries dropped, the list holds every
+// pixel whose key is >= bkey.  If at least s of its keys are >= bkey, the s-th largest key of a
+// is >= bkey too, so every entry of H_s(a) -- including the lowest-index ties at the threshold
+// -- is in the list, and the top-s of the list (greater key, then lower index) IS H_s(a),
+// exactly.  Otherwise (iteration 1, a support change larger than the bound,
+// list overflow, NaN, poisoned x) the same CTA selects the snapshot over all of a
+// (bs_full_select): no second launch -- a skipped cluster-kernel launch had cost ~9 us per
+// iteration in the graph (r02 g55).  One CTA per snapshot; resets ccnt for the next call;
+// done[b] = 1 when the list decided (statistics / tests).
+// 512 threads (r02 g57: 256 threads, 2 list entries more per thread, were 3 us per iteration
+// slower); ~15 KB of static shared memory, the full select's lists in the workspace.
 constexpr int kBsThreads = 512;
 constexpr int kBsCap = 1024;                   // list entries ranked in shared memory
 constexpr int kBsMaxS = 256;
+constexpr int kBsWarps = kBsThreads / 32;
+
+// Full select of one snapshot over all N columns, when the bounded list could not decide it
+// (iteration 1, a large support change, NaN, overflow): the cluster kernel's arithmetic and
+// result in one CTA.  a = mu g into the workspace ga, its 11-bit histogram (top key bits),
+// x's support patched to a_j = x_j + mu g_j; bin d1 of the s-th largest key; the keys with
+// digit >= d1 listed in index order by each warp over its contiguous range (in the workspace:
+// warp w's list at gl + w * span, it cannot hold more than its range), packed in index order
+// (gp), and select_ordered on them, the values gathered from ga.  Poisoned x or a NaN in a:
+// nnz = -1 (sticky).
+__device__ void bs_full_select(const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, int nraw, int nnz,
+                               const float* __restrict__ g, float mu, int s, int N, float* __restrict__ ga,
+                               int32_t* __restrict__ gl, int32_t* __restrict__ gp, int32_t* __restrict__ out_idx,
+                               float* __restrict__ out_val, int32_t* __restrict__ out_nnz_b, int* hist, int* scratch,
+                               int* wgt, int* weq, int* wtake, int* wbase, int* sh) {
+  constexpr int NT = kBsThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (nraw < 0) {
+    if (tid == 0) *out_nnz_b = -1;
+    return;
+  }
+  for (int q = tid; q < 2048; q += NT) hist[q] = 0;
+  __syncthreads();
+  int nan = 0;
+  const bool vec = (N & 3) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (reinterpret_cast<uintptr_t>(ga) & 15) == 0;
+  const int n4 = vec ? N >> 2 : 0;
+  constexpr int kLd = 8;
+  for (int i0 = 0; i0 < n4; i0 += NT * kLd) {
+    float4 v[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int i = i0 + u * NT + tid;
+      v[u] = i < n4 ? __ldg(reinterpret_cast<const float4*>(g) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int i = i0 + u * NT + tid;
+      if (i >= n4) break;
+      const float4 a4 = make_float4(__fmul_rn(mu, v[u].x), __fmul_rn(mu, v[u].y), __fmul_rn(mu, v[u].z),
+                                    __fmul_rn(mu, v[u].w));
+      reinterpret_cast<float4*>(ga)[i] = a4;
+      const unsigned int k0 = __float_as_uint(a4.x) & 0x7FFFFFFFu, k1 = __float_as_uint(a4.y) & 0x7FFFFFFFu,
+                         k2 = __float_as_uint(a4.z) & 0x7FFFFFFFu, k3 = __float_as_uint(a4.w) & 0x7FFFFFFFu;
+      nan |= (k0 > 0x7F800000u) | (k1 > 0x7F800000u) | (k2 > 0x7F800000u) | (k3 > 0x7F800000u);
+      atomicAdd(&hist[k0 >> 20], 1);
+      atomicAdd(&hist[k1 >> 20], 1);
+      atomicAdd(&hist[k2 >> 20], 1);
+      atomicAdd(&hist[k3 >> 20], 1);
+    }
+  }
+  for (int i = (n4 << 2) + tid; i < N; i += NT) {
+    const float a1 = __fmul_rn(mu, __ldg(g + i));
+    ga[i] = a1;
+    const unsigned int k = __float_as_uint(a1) & 0x7FFFFFFFu;
+    nan |= k > 0x7F800000u;
+    atomicAdd(&hist[k >> 20], 1);
+  }
+  __syncthreads();                              // ga complete (global writes of this CTA)
+  for (int j = tid; j < nnz; j += NT) {         // x's entries (distinct indices): move their keys
+    const int c = x_idx[j];
+    const float old = ga[c];
+    const float nw = __fadd_rn(x_val[j], old);
+    ga[c] = nw;
+    const unsigned int ko = __float_as_uint(old) & 0x7FFFFFFFu, kn = __float_as_uint(nw) & 0x7FFFFFFFu;
+    nan |= kn > 0x7F800000u;
+    atomicSub(&hist[ko >> 20], 1);
+    atomicAdd(&hist[kn >> 20], 1);
+  }
+  nan = __syncthreads_or(nan);
+  if (nan) {
+    if (tid == 0) *out_nnz_b = -1;
+    return;
+  }
+  find_bin<NT>(hist, 2048, s, &sh[0], &sh[1], scratch);
+  const unsigned int d1 = (unsigned int)sh[0];
+  const int span = ((N + kBsWarps - 1) / kBsWarps + 127) / 128 * 128;
+  const int wlo = warp * span, whi = min(N, wlo + span);
+  int32_t* wl = gl + wlo;                       // this warp's list: at most whi - wlo entries
+  int wc = 0;
+  for (int i00 = wlo; i00 < whi; i00 += 128) {  // lane = 4 consecutive entries
+    const int ib = i00 + 4 * lane;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = ib + e < whi ? __ldcg(ga + ib + e) : 0.0f;
+    unsigned int f = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const unsigned int key = __float_as_uint(v[e]) & 0x7FFFFFFFu;
+      f |= (unsigned int)(ib + e < whi && key > 0u && (key >> 20) >= d1) << e;
+    }
+    if (__any_sync(0xffffffffu, f)) {
+      const int cnt = __popc(f);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int pos = wc + incl - cnt;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if ((f >> e) & 1u) wl[pos++] = ib + e;
+      }
+      wc += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (lane == 0) wgt[warp] = wc;
+  __syncthreads();                              // the lists (global, this CTA) and their counts
+  int off = 0, total = 0;
+  for (int w = 0; w < kBsWarps; ++w) {
+    if (w == warp) off = total;
+    total += wgt[w];
+  }
+  for (int j = lane; j < wc; j += 32) gp[off + j] = __ldcg(wl + j);
+  __syncthreads();
+  select_ordered<NT>(total, s, [&](int i) { return __ldcg(ga + __ldcg(gp + i)); }, [&](int i) { return __ldcg(gp + i); },
+                     out_idx, out_val, out_nnz_b, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
+}
 
 __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
     const int32_t* __restrict__ x_idx, const float* __restrict__ x_val, const int32_t* __restrict__ x_nnz,
     int32_t max_nnz, int32_t ldx, const float* __restrict__ g, float mu, const unsigned int* __restrict__ bkeys,
     int s, int64_t N, const int32_t* __restrict__ cidx, const float* __restrict__ cval, int* __restrict__ ccnt,
     int ccap, int32_t* __restrict__ out_idx, float* __restrict__ out_val, int32_t ldo, int32_t* __restrict__ out_nnz,
-    int* __restrict__ done, int* __restrict__ stats) {
+    int* __restrict__ done, int* __restrict__ stats, float* __restrict__ ga0, int32_t* __restrict__ gl0,
+    int32_t* __restrict__ gp0, int64_t ws_stride) {
   constexpr int PER = kBsCap / kBsThreads;      // list slots per thread
-  __shared__ __align__(16) int32_t lidx[kBsCap + 4];
-  __shared__ __align__(16) unsigned int lkey[kBsCap + 4];
-  __shared__ float lval[kBsCap];
+  // the list (lidx | lkey | lval) and, on the full-select path, its histogram in the same bytes
+  __shared__ __align__(16) unsigned char lbuf[(2 * (kBsCap + 4) + kBsCap) * 4];
+  int32_t* lidx = reinterpret_cast<int32_t*>(lbuf);
+  unsigned int* lkey = reinterpret_cast<unsigned int*>(lidx + kBsCap + 4);
+  float* lval = reinterpret_cast<float*>(lkey + kBsCap + 4);
+  int* f_hist = reinterpret_cast<int*>(lbuf);   // 2048 ints <= the list's bytes
+  static_assert(2048 * 4 <= (2 * (kBsCap + 4) + kBsCap) * 4, "histogram fits the list buffer");
+  __shared__ int f_scratch[kBsWarps], f_wgt[kBsWarps], f_weq[kBsWarps], f_wtake[kBsWarps], f_wbase[kBsWarps], f_sh[4];
   __shared__ __align__(16) int32_t sidx[kBsMaxS + 4];
   __shared__ float kval[kBsMaxS];
   __shared__ int sh_n, sh_t, sh_bad, sh_kept;
@@ -1226,12 +1353,19 @@ __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
   }
   __syncthreads();                              // every thread has read ccnt
   if (tid == 0) ccnt[b] = 0;                    // zero for the next call
-  if (nraw < 0 || bkey == 0xFFFFFFFFu || s <= 0 || s > kBsMaxS || nnz > kBsMaxS || cnt > ccap || (int64_t)s >= N ||
-      nnz + cnt > kBsCap || max_nnz > kBsThreads) {
+  auto full = [&]() {                           // not decidable from the list: select over all of a
     if (tid == 0) {
       done[b] = 0;
       if (stats) atomicAdd(&stats[1], 1);
     }
+    __syncthreads();                            // the list buffer becomes the histogram
+    bs_full_select(x_idx, x_val, nraw, nnz, g, mu, s, (int)N, ga0 + (int64_t)b * ws_stride,
+                   gl0 + (int64_t)b * ws_stride, gp0 + (int64_t)b * ws_stride, out_idx, out_val, out_nnz + b, f_hist,
+                   f_scratch, f_wgt, f_weq, f_wtake, f_wbase, f_sh);
+  };
+  if (nraw < 0 || bkey == 0xFFFFFFFFu || s <= 0 || s > kBsMaxS || nnz > kBsMaxS || cnt > ccap || (int64_t)s >= N ||
+      nnz + cnt > kBsCap || max_nnz > kBsThreads) {
+    full();
     return;
   }
   // x's support: a_j = x_j + mu g_j (the cluster kernel's arithmetic); the g gather is issued
@@ -1287,10 +1421,7 @@ __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
   if (bad) sh_bad = 1;
   __syncthreads();
   if (sh_bad || sh_t < s) {
-    if (tid == 0) {
-      done[b] = 0;
-      if (stats) atomicAdd(&stats[1], 1);
-    }
+    full();
     return;
   }
   // rank = keys greater, or equal at a lower index (4 entries per shared load); kept iff
@@ -1476,7 +1607,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
                           const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
                           int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
                           int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream,
-                          bool ws_prezeroed, const int* skip = nullptr);
+                          bool ws_prezeroed);
 
 int iht_threshold_batched_mu(const int32_t* x_idx, const float* x_val, const int32_t* x_nnz, int32_t ldx,
                              const float* g, float mu, const float* mu_dev, int32_t s, int64_t N, int64_t col_offset,
@@ -1495,12 +1626,15 @@ int iht_threshold_bounded(const int32_t* x_idx, const float* x_val, const int32_
       done == nullptr || bkey == nullptr || ccap <= 0 || x_nnz == nullptr || g == nullptr || ldx < 0 || ldo < s)
     return IHT_EINVAL;
   if (!isfinite(mu)) return IHT_EDOMAIN;
+  if (ws == nullptr || ws_bytes < thr_ws_layout(N, nrhs, nullptr, nullptr)) return IHT_EINVAL;
   const int32_t max_nnz = ldx < s ? ldx : s;
+  ThrWs w{};
+  thr_ws_layout(N, nrhs, static_cast<char*>(ws), &w);   // the full select's a, list and packed buffers
   IHT_CUDA_CHECK(launch_pdl(thr_bounded_select, dim3(nrhs), dim3(kBsThreads), 0, (cudaStream_t)stream, x_idx, x_val,
                             x_nnz, max_nnz, ldx, g, mu, bkey, s, N, cidx, cval, ccnt, (int)ccap, out_idx, out_val, ldo,
-                            out_nnz, done, stats));
-  return threshold_impl(x_idx, x_val, x_nnz, ldx, g, 0, 1.0f, nullptr, mu, nullptr, s, N, 0, nrhs, out_idx, out_val,
-                        ldo, out_nnz, ws, ws_bytes, stream, true, done);
+                            out_nnz, done, stats, w.a, w.cidx, reinterpret_cast<int32_t*>(w.cval),
+                            (int64_t)(w.body_stride / 4)));
+  return IHT_OK;
 }
 
 bool iht_threshold_bounded_applies(int64_t N, int32_t s, int32_t nrhs) {
@@ -1520,7 +1654,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
                           const float* g, int nparts, float gsigma, float* gout, float mu, const float* mu_dev,
                           int32_t s, int64_t N, int64_t col_offset, int32_t nrhs, int32_t* out_idx, float* out_val,
                           int32_t ldo, int32_t* out_nnz, void* ws, int64_t ws_bytes, void* stream,
-                          bool ws_prezeroed, const int* skip) {
+                          bool ws_prezeroed) {
   if (x_nnz == nullptr || g == nullptr || out_idx == nullptr || out_val == nullptr || out_nnz == nullptr ||
       s < 0 || N <= 0 || N > 0x7FFFFFFFll || nrhs <= 0 || nrhs > 65535 || ldo < s || ldx < 0 ||
       col_offset < 0 || col_offset + N > 0x7FFFFFFFll)
@@ -1562,7 +1696,7 @@ static int threshold_impl(const int32_t* x_idx, const float* x_val, const int32_
     lc.numAttrs = 2;
     IHT_CUDA_CHECK(cudaLaunchKernelEx(&lc, thr_cluster_kernel, x_idx, x_val, x_nnz, max_nnz, ldx, g, mu, mu_dev, s,
                                       N, col_offset, slice, out_idx, out_val, ldo, out_nnz, thr_probe(), nparts,
-                                      gsigma, gout, thr_timeline(), skip));
+                                      gsigma, gout, thr_timeline()));
     if (thr_timeline()) {   // profiling: per-phase times of ranks 0, 1 of snapshot 0 (stderr)
       static long long h[32];
       cudaStreamSynchronize(st);

@@ -374,10 +374,10 @@ def _bounded_runs(pool, p, Y, B, n_iter, monkeypatch, capfd, bound="0.5"):
 
 @pytest.mark.parametrize("B,bound", [(16, "0.5"), (64, "0.9"), (5, "0.3")])
 def test_batched_bounded_select_bit_identical(B, bound, monkeypatch, capfd):
-    """Bounded select (epilogue candidates + thr_bounded_select, cluster kernel only for the
-    snapshots it cannot decide) against the cluster kernel alone: every iterate of every
-    snapshot bit-identical (both are exact H_s of the same fp32 a), and the bounded path
-    decides most snapshot-iterations after the first."""
+    """Bounded select (epilogue candidates + thr_bounded_select; a snapshot the list cannot
+    decide is selected over all of a by the same CTA) against the cluster kernel alone: every
+    iterate of every snapshot bit-identical (both are exact H_s of the same fp32 a), and the
+    bounded path decides most snapshot-iterations after the first."""
     n_iter = 24
     p, Y = _radio_batch(B, n_iter=n_iter, K=40)
     pool = iht.quantize(_to_dev(p.phi), p.b_phi, 0, p.seed, list(range(p.K)), float(OQ.scale_c(p.phi)))
