@@ -795,6 +795,12 @@ int iht_adjoint_batched_cand(const iht_qmat* A, const float* R, int32_t nrhs, fl
                               cand ? cand->x_nnz + c0 : nullptr, cand ? cand->ldx : 0,                     \
                               cand ? cand->max_nnz : 0, cand ? cand->bound : 0.0f,                         \
                               cand ? cand->bkey + c0 : nullptr));                                          \
+    if (getenv("IHT_DUP_LIMBS")) /* profiling: the limb kernel twice (idempotent), its in-graph cost */ \
+      IHT_CUDA_CHECK(launch_pdl(batched_limbs_kernel<BB>, dim3(bp), dim3(256), 0, st, Rc, (int)Rpad, bp, nb,  \
+                                nkb, bimg, Fb, Sb, cand ? cand->x_val + (int64_t)c0 * cand->ldx : nullptr,   \
+                                cand ? cand->x_nnz + c0 : nullptr, cand ? cand->ldx : 0,                     \
+                                cand ? cand->max_nnz : 0, cand ? cand->bound : 0.0f,                         \
+                                cand ? cand->bkey + c0 : nullptr));                                          \
     static bool attr = false;                                                                          \
     if (!attr) {                                                                                       \
       IHT_CUDA_CHECK(cudaFuncSetAttribute(adjoint_batched_kernel<BB>,                                  \

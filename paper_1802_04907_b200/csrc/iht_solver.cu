@@ -388,6 +388,8 @@ static int enqueue_run(iht_solver* S, cudaStream_t st, int64_t* launches) {
       if ((rc = iht_forward(&F, xi, xv, xn, s, yh, S->r, S->ws_fwd, S->ws_fwd_bytes, st)) != IHT_OK) return rc;
     } else if ((rc = iht_forward_batched(&F, xi, xv, xn, s, s, B, yh, S->r, st)) != IHT_OK) {
       return rc;
+    } else if (S->batched && getenv("IHT_DUP_FWD")) {   // profiling: the forward twice (idempotent),
+      if ((rc = iht_forward_batched(&F, xi, xv, xn, s, s, B, yh, S->r, st)) != IHT_OK) return rc;   // its in-graph cost
     }
     L += 1;
     if (S->colshard) {
