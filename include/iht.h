@@ -419,6 +419,21 @@ IHT_API int iht_solver_adjoint_times(iht_solver* solver, float* ms_host);
 /* Adaptive step (cfg.step_mode = 1): the accepted mu and the number of shrinks of every
  * iteration of the LAST run, [n_iter][B] each (host arrays).  Synchronises the stream. */
 IHT_API int iht_solver_steps(iht_solver* solver, float* mu_host, int32_t* shrinks_host, void* stream);
+/* RecoveryReport of the last run (cfg.trace = 1; "one row per iteration with
+ * columns iter, mu, residual_norm, support_size, support_change, shrink_count"), host arrays
+ * [n_iter][B]:
+ *   residual_norm[n-1]  = || y-hat - Phi-hat_{2n} x^[n] ||_2, the forward residual of
+ *                         iteration n (Algorithm 1), recomputed from the recorded
+ *                         iterate x^[n] by the solver's own forward kernel on the same copy
+ *                         (stacked re/im rows: the complex norm); squared norms summed in
+ *                         fp32 in a fixed order (all-reduced over row shards), sqrt in fp64;
+ *   support_size[n-1]   = || x^[n+1] ||_0 (-1 when the iterate is poisoned);
+ *   support_change[n-1] = | supp x^[n+1] symmetric-difference supp x^[n] | (x^[1] = 0).
+ * mu and shrink_count come from cfg.mu / iht_solver_steps.  Uses scratch device memory of
+ * B * vec_len + n_iter * B floats (allocated and freed here); synchronises the stream.
+ * IHT_EINVAL without cfg.trace or with a NULL pointer. */
+IHT_API int iht_solver_report(iht_solver* solver, double* residual_norm_host, int32_t* support_size_host,
+                              int32_t* support_change_host, void* stream);
 /* 1 if the solver runs the fused persistent kernel (cfg.fused and the problem fits), else 0;
  * negative on a NULL solver.  With cfg.profile, iht_solver_adjoint_times then reports the
  * fused kernel's duration divided evenly over the n_iter iterations. */

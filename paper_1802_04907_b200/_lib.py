@@ -111,6 +111,7 @@ SIGNATURES = {
     "iht_solver_launches_per_run": (c_i64, [c_vp]),
     "iht_solver_fused": (c_int, [c_vp]),
     "iht_solver_steps": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "iht_solver_report": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "iht_solve": (c_int, [ctypes.POINTER(IhtQmat), c_int, ctypes.POINTER(IhtConfig), c_vp, c_int, c_vp, c_vp, c_vp, c_vp]),
 }
 

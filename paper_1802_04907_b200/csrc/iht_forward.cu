@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
     const int64_t m = (int64_t)blockIdx.x * kFwdWords * CPW + t;
     ypre[k] = (yhat && t < kFwdWords * CPW && m < (int64_t)words_total * CPW) ? yhat[m] : 0.0f;
   }
+  // the first staging round's support slots, requested together with nnz (they do not depend
+  // on it: the x arrays hold max_nnz slots) -- one dependent round trip fewer
+  // (the first kFwdThreads slots: one per thread)
+  const int32_t pidx = (int)threadIdx.x < max_nnz ? x_idx[threadIdx.x] : 0;
+  const float pval = (int)threadIdx.x < max_nnz ? x_val[threadIdx.x] : 0.0f;
   int nnz = x_nnz[b];
   nnz = nnz < 0 ? 0 : (nnz > max_nnz ? max_nnz : nnz);
   const int64_t word = (int64_t)blockIdx.x * kFwdWords + wl;
@@ -83,11 +88,12 @@ __global__ void __launch_bounds__(kFwdThreads) forward_kernel(
   // stage the support: byte offset of each column's tile + slot (columns outside this
   // shard get value 0 and column 0, adding +0 exactly)
   for (int j = threadIdx.x; j < nst; j += kFwdThreads) {
-    int64_t col = (int64_t)x_idx[st0 + j] - col_offset;
+    const bool pre = st0 == 0 && j == (int)threadIdx.x;   // this thread's slot, loaded above
+    int64_t col = (int64_t)(pre ? pidx : x_idx[st0 + j]) - col_offset;
     const bool ok = col >= 0 && col < ncols;
     col = ok ? col : 0;
     sidx[j] = strips ? col * strip_bytes : (col >> 4) * (16 * strip_bytes) + (col & 15) * 64;
-    sval[j] = ok ? x_val[st0 + j] : 0.0f;
+    sval[j] = ok ? (pre ? pval : x_val[st0 + j]) : 0.0f;
   }
   __syncthreads();
   for (int jb = warp * CS; jb < nst; jb += 8 * CS * kFwdUnroll) {   // warp-uniform trip count

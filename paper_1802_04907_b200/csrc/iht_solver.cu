@@ -784,6 +784,81 @@ extern "C" int iht_solver_trace(iht_solver* S, int32_t* idx_host, float* val_hos
   return IHT_OK;
 }
 
+// RecoveryReport (iht.h): the residual of every iteration recomputed from the recorded iterate
+// with the solver's forward on the same copy, its squared norm (ad_norm, fixed order), the
+// support sizes and changes from the recorded supports (increasing indices: one merge each).
+extern "C" int iht_solver_report(iht_solver* S, double* rn_host, int32_t* size_host, int32_t* change_host,
+                                 void* stream) {
+  if (S == nullptr || !S->cfg.trace || rn_host == nullptr || size_host == nullptr || change_host == nullptr)
+    return IHT_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n_iter = S->cfg.n_iter, B = S->B, s = S->cfg.s;
+  if (n_iter == 0) return IHT_OK;
+  const int64_t xslot = (int64_t)B * s;
+  const int K = (int)S->pool.size();
+  float* rtmp = nullptr;
+  float* nrm = nullptr;
+  if (cudaMalloc(&rtmp, (size_t)B * S->vlen * sizeof(float)) != cudaSuccess) return IHT_ENOMEM;
+  if (cudaMalloc(&nrm, (size_t)n_iter * B * sizeof(float)) != cudaSuccess) {
+    cudaFree(rtmp);
+    return IHT_ENOMEM;
+  }
+  int rc = IHT_OK;
+  for (int n = 1; n <= n_iter && rc == IHT_OK; ++n) {
+    const int32_t* xi = S->xs_idx + (int64_t)(n - 1) * xslot;   // x^[n] (slot n-1)
+    const float* xv = S->xs_val + (int64_t)(n - 1) * xslot;
+    const int32_t* xn = S->xs_nnz + (int64_t)(n - 1) * B;
+    const float* yh = (S->colshard && S->rank != 0) ? nullptr : S->yhat;
+    if (S->fresh) rc = iht_forward_fresh(&S->fm, 2 * n - 1, xi, xv, xn, s, S->yhat, rtmp, st);
+    else rc = iht_forward_batched(&S->pool[(2 * n - 1) % K], xi, xv, xn, s, s, B, yh, rtmp, st);
+    if (rc == IHT_OK && S->colshard) rc = iht_comm_allreduce(S->cfg.comm, rtmp, (int64_t)B * S->vlen, 0, st);
+    if (rc == IHT_OK) rc = ad_norm(rtmp, S->vlen, nrm + (int64_t)(n - 1) * B, B, st);
+  }
+  if (rc == IHT_OK && S->rowshard) rc = iht_comm_allreduce(S->cfg.comm, nrm, (int64_t)n_iter * B, 0, st);
+  std::vector<float> h((size_t)n_iter * B);
+  std::vector<int32_t> idx((size_t)(n_iter + 1) * (xslot > 0 ? xslot : 1)), nz((size_t)(n_iter + 1) * B);
+  if (rc == IHT_OK) {
+    cudaError_t e = cudaMemcpyAsync(h.data(), nrm, h.size() * sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && xslot > 0)
+      e = cudaMemcpyAsync(idx.data(), S->xs_idx, (size_t)(n_iter + 1) * xslot * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(nz.data(), S->xs_nnz, nz.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      iht_set_last_cuda_error(e, "iht_solver_report copies", __FILE__, __LINE__);
+      rc = IHT_ECUDA;
+    }
+  }
+  cudaFree(rtmp);
+  cudaFree(nrm);
+  if (rc != IHT_OK) return rc;
+  for (int n = 1; n <= n_iter; ++n) {
+    for (int b = 0; b < B; ++b) {
+      const size_t o = (size_t)(n - 1) * B + b;
+      rn_host[o] = sqrt((double)h[o]);
+      const int k0 = nz[(size_t)(n - 1) * B + b], k1 = nz[(size_t)n * B + b];
+      size_host[o] = k1;
+      const int a = k0 < 0 ? 0 : k0, c = k1 < 0 ? 0 : k1;
+      const int32_t* p = idx.data() + (size_t)(n - 1) * xslot + (size_t)b * s;   // supp x^[n]
+      const int32_t* q = idx.data() + (size_t)n * xslot + (size_t)b * s;         // supp x^[n+1]
+      int i = 0, j = 0, common = 0;
+      while (i < a && j < c) {
+        if (p[i] == q[j]) {
+          ++common;
+          ++i;
+          ++j;
+        } else if (p[i] < q[j]) {
+          ++i;
+        } else {
+          ++j;
+        }
+      }
+      change_host[o] = a + c - 2 * common;
+    }
+  }
+  return IHT_OK;
+}
+
 extern "C" int iht_solver_buffers(iht_solver* S, const float** yhat, const float** r, const float** g) {
   if (S == nullptr) return IHT_EINVAL;
   if (yhat) *yhat = S->yhat;

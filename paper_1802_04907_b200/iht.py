@@ -10,6 +10,8 @@ mirror include/iht.h:
 import ctypes
 from dataclasses import dataclass
 
+import numpy as np
+
 import torch
 
 from . import _lib
@@ -395,6 +397,7 @@ class Solver:
         lib = load()
         self.pool = pool                     # keep the code / Phi tensors alive
         self.s, self.n_iter = s, n_iter
+        self.mu, self.adaptive = float(mu), bool(adaptive)
         self.trace = trace
         self.nrhs = max(1, nrhs)
         cfg = IhtConfig(s=s, n_iter=n_iter, mu=float(mu), b_y=b_y, level_mode=level_mode,
@@ -466,6 +469,42 @@ class Solver:
         sh = torch.empty(shape, dtype=torch.int32)
         check(load().iht_solver_steps(self.handle, _ptr(mu), _ptr(sh), _stream(stream)), "iht_solver_steps")
         return mu, sh
+
+    def report(self, stream=None):
+        """RecoveryReport of the last run (trace=True): a dict of numpy arrays
+        [n_iter] (batched: [n_iter, B]) -- iter, mu, residual_norm (||y-hat - Phi-hat_{2n} x^[n]||,
+        recomputed on the GPU from the recorded iterates), support_size, support_change,
+        shrink_count.  Marshalling only: every number comes from iht_solver_report /
+        iht_solver_steps."""
+        shape = (self.n_iter, self.nrhs) if self.nrhs > 1 else (self.n_iter,)
+        rn = torch.empty(shape, dtype=torch.float64)
+        sz = torch.empty(shape, dtype=torch.int32)
+        ch = torch.empty(shape, dtype=torch.int32)
+        check(load().iht_solver_report(self.handle, _ptr(rn), _ptr(sz), _ptr(ch), _stream(stream)),
+              "iht_solver_report")
+        if self.adaptive:
+            mu, sh = self.steps(stream)
+            mu, sh = mu.numpy().astype(np.float64), sh.numpy()
+        else:
+            mu = np.full(shape, float(self.mu))
+            sh = np.zeros(shape, np.int32)
+        it = np.arange(1, self.n_iter + 1)
+        if self.nrhs > 1:
+            it = np.repeat(it[:, None], self.nrhs, axis=1)
+        return {"iter": it, "mu": mu, "residual_norm": rn.numpy(), "support_size": sz.numpy(),
+                "support_change": ch.numpy(), "shrink_count": sh}
+
+    def report_csv(self, path, snapshot=0, stream=None):
+        """Write the RecoveryReport as CSV (SPEC.md:234 columns), one row per iteration
+        (batched: of one snapshot)."""
+        rep = self.report(stream)
+        cols = ["iter", "mu", "residual_norm", "support_size", "support_change", "shrink_count"]
+        with open(path, "w") as f:
+            f.write(",".join(cols) + "\n")
+            for n in range(self.n_iter):
+                row = [rep[c][n] if self.nrhs == 1 else rep[c][n, snapshot] for c in cols]
+                f.write(f"{int(row[0])},{float(row[1])!r},{float(row[2])!r},{int(row[3])},{int(row[4])},{int(row[5])}\n")
+        return rep
 
     def launches_per_run(self):
         return int(load().iht_solver_launches_per_run(self.handle))

@@ -64,6 +64,7 @@ def test_host_side_validation_without_gpu(lib):
     assert lib.iht_adjoint(ctypes.byref(q), c(16), c(16), 0, c(0), 0, c(0)) == _lib.IHT_EINVAL
     assert lib.iht_threshold(c(0), c(0), c(0), c(0), 1.0, -1, 10, c(0), c(0), c(0), c(0), 0, c(0)) == _lib.IHT_EINVAL
     assert lib.iht_solver_create(None, 0, None, None) == _lib.IHT_EINVAL
+    assert lib.iht_solver_report(None, c(16), c(16), c(16), c(0)) == _lib.IHT_EINVAL   # RecoveryReport: NULL solver
     # batched entry points (config 5) validate on the host too
     assert lib.iht_absmax_batched(c(16), 4, 0, c(16), c(0)) == _lib.IHT_EINVAL
     assert lib.iht_forward_batched(None, c(0), c(0), c(0), 0, 0, 1, c(0), c(0), c(0)) == _lib.IHT_EINVAL
