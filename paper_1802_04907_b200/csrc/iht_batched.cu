@@ -29,30 +29,14 @@
 #include <stdlib.h>
 
 #include "iht_internal.cuh"
+#include "iht_limbs.cuh"
 #include "iht_mma.cuh"
 
 namespace iht {
 
 constexpr int kBT = 128;               // pixels per GEMM tile (M)
-constexpr int kNonFinite = 1000;       // F_b marker: r_b holds a NaN / inf -> g_b = NaN
 constexpr int kBThreads = 352;         // 11 warps (roles above)
 
-// Per bit width: tile-steps (512/b rows, 1 KiB of a 16-column tile) per K-block, so that a
-// K-block is 16 MMAs (K = 32 each) at 2 and 4 bits and 8 at 8 bits; A stages fill the 256
-// TMEM columns left by the two accumulators; B stages take 128 KiB of shared memory.
-// Measured (in-kernel timeline probe, config 5): every K-block handoff costs the MMA pipe
-// ~300-400 clk whatever the depth, so fewer, larger K-blocks win: 2 stages x 16 MMAs ran
-// at 87 clk per MMA (MMA-only), 4 stages x 8 MMAs at 100, against 64 back to back; r02
-// again with the current issuer: 8-MMA K-blocks at 2 bits 49.2 us per call against 41.7.
-template <int BITS> struct BCfg {
-  static constexpr int TS = BITS == 8 ? 4 : BITS;       // tile-steps per K-block
-  static constexpr int KBR = TS * 512 / BITS;           // rows (= u8 bytes per pixel row) per K-block
-  static constexpr int NKS = KBR / 32;                  // MMAs per K-block
-  static constexpr int ACOLS = KBR / 4;                 // TMEM columns of one A stage
-  static constexpr int STAGES = 256 / ACOLS;            // 2 (2/4-bit) or 4 (8-bit)
-  static constexpr int PK = 8 * TS * 1024;              // packed bytes per K-block (8 column tiles)
-  static constexpr int PKSLOTS = PK <= 8192 ? 8 : (PK <= 16384 ? 4 : 2);   // packed-code slots
-};
 constexpr int kStagesMax = 4, kPkSlotsMax = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -108,23 +92,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // instruction descriptor: kind::i8, A u8, B s8, D s32, both K-major, M, N
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-// byte offset of (row, 16-byte K chunk q) in a K-major SW128 tile whose rows hold KBB
-// bytes: atoms of 128 rows x 128 B (16 KiB) along K, 8-row groups at 1024 B.
-__host__ __device__ inline uint32_t sw128_off(int row, int q, int rows_total) {
-  const int a = q >> 3, c = q & 7;
-  return (uint32_t)(a * rows_total * 128 + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4));
-}
-
-// K permutation inside a 16-byte u8 chunk (shared by A and B): position p (0..15) <-> row
-// offset (32/b) h + j + P i, with p = 4 (h P + j) + i (h: packed word, j: bit-position,
-// i: byte).
-__host__ __device__ inline int perm_row(int p, int bits) {
-  const int P = 8 / bits, cpw = 32 / bits;
-  const int i = p & 3, g = p >> 2;   // g = h P + j
-  const int h = g / P, j = g % P;
-  return cpw * h + j + P * i;
 }
 
 struct BatchArgs {
@@ -541,42 +508,27 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
   }
 }
 
-// Per-snapshot block fixed point of R (one CTA per snapshot): F_b from max |r|, two
-// balanced signed limbs written into the pre-swizzled image, exact limb sums S_b.  A
-// thread owns 16 consecutive rows (one 16-byte K chunk of the image): it reads them as
-// four float4, permutes them into MMA K order in registers and writes two 16-byte stores.
-// With bkey (the bounded select, solver only): also the snapshot's bound key from x^[n]
-// (warp_bound_key), read by the GEMM's epilogue and by thr_bounded_select.
+// Per-snapshot block fixed point of R (one CTA per snapshot): max |r| over bit patterns, then
+// limbs_from_max (iht_limbs.cuh).  With bkey (the bounded select, solver only): also the
+// snapshot's bound key from x^[n] (bound_key), read by the GEMM's epilogue and by
+// thr_bounded_select.  (Folding this into the forward's last CTA per snapshot was measured at
+// the same rate, r02 g61: the conversion's latency only moved, PDL already hid the launch.)
 template <int BITS>
 __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restrict__ R, int Rpad, int B, int nreal,
                                                             int nkb, uint8_t* __restrict__ bimg, int* __restrict__ Fb,
                                                             int* __restrict__ Sb, const float* __restrict__ xval,
                                                             const int32_t* __restrict__ xnnz, int ldx, int max_nnz,
                                                             float bound, unsigned int* __restrict__ bkey) {
-  constexpr int KBR = BCfg<BITS>::KBR;
   pdl_launch_dependents();
   pdl_wait();                               // R (forward)
   const int b = blockIdx.x;                 // b >= nreal: zero padding snapshot (MMA N granularity)
   const bool live = b < nreal;
+  const float* r = R + (int64_t)(live ? b : 0) * Rpad;
   // bound key: the last warp requests x's values (<= 256 of them: s <= kBsMaxS) before its r
   // loads and reduces them after the max pass, so the x round trip overlaps the r one
   const bool kw = bkey && live && threadIdx.x >= 224;
-  int xn = 0;
-  unsigned int xk[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) xk[k] = 0xFFFFFFFFu;
-  if (kw) {                                 // all ldx slots requested at once, masked by nnz later
-    xn = xnnz[b];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int j = (threadIdx.x & 31) + 32 * k;
-      if (j < ldx) xk[k] = __float_as_uint(xval[(int64_t)b * ldx + j]) & 0x7FFFFFFFu;
-    }
-  }
-  const float* r = R + (int64_t)(live ? b : 0) * Rpad;
-  __shared__ float red[8];
-  __shared__ int ired[2][8];
-  __shared__ int Fs;
+  BoundKeyLoads bk;
+  if (kw) bk.load(xval + (int64_t)b * ldx, xnnz[b], ldx);
   // max |r| over bit patterns: a NaN / inf in r_b marks the snapshot (F = kNonFinite) and
   // its g becomes NaN, so that its H_s reports the domain error
   unsigned int m = 0;
@@ -596,77 +548,19 @@ __global__ void __launch_bounds__(256) batched_limbs_kernel(const float* __restr
       }
     }
   }
-  m = __reduce_max_sync(0xffffffffu, m);
   if (kw) {
-    xn = min(xn, max_nnz);                  // < 0 (poisoned): no candidates
-    unsigned int mk = 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) mk = min(mk, (threadIdx.x & 31) + 32 * k < xn ? xk[k] : 0xFFFFFFFFu);
-    mk = __reduce_min_sync(0xffffffffu, mk);
-    if (threadIdx.x == 224) bkey[b] = bound_key(mk, xn, bound);
+    const unsigned int k = bk.key(max_nnz, bound);
+    if (threadIdx.x == 224) bkey[b] = k;
   }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = __uint_as_float(m);
+  __shared__ unsigned int red[8];
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int mb = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mb = max(mb, __float_as_uint(red[w]));
-    const bool bad = mb >= 0x7F800000u;
-    const float mm = bad ? 0.0f : __uint_as_float(mb);
-    int e = 0;
-    if (mm > 0.0f) frexpf(mm, &e);
-    Fs = bad ? kNonFinite : (mm > 0.0f ? min(14 - e, 126) : 0);   // |r| 2^F < 2^14 -> two limbs
-    Fb[b] = Fs;
-  }
-  __syncthreads();
-  const float scale = Fs == kNonFinite ? 0.0f : ldexpf(1.0f, Fs);
-  const int NB = 2 * B;
-  int s0 = 0, s1 = 0;
-  for (int ch = threadIdx.x; ch < nkb * KBR / 16; ch += blockDim.x) {   // rows past Rpad: zero limbs
-    const int row0 = ch * 16;
-    const bool in = live && row0 < Rpad;      // Rpad is a multiple of 256: chunks are all-in or all-out
-    float v[16];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 f = in ? *reinterpret_cast<const float4*>(r + row0 + 4 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
-      v[4 * k] = f.x;
-      v[4 * k + 1] = f.y;
-      v[4 * k + 2] = f.z;
-      v[4 * k + 3] = f.w;
-    }
-    uint32_t w0[4] = {0u, 0u, 0u, 0u}, w1[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int p = 0; p < 16; ++p) {          // byte p of the chunk <- row row0 + perm_row(p)
-      const int ri = __float2int_rn(v[perm_row(p, BITS)] * scale);
-      const int l0 = ((ri + 128) & 255) - 128;
-      const int l1 = (ri - l0) >> 8;
-      s0 += l0;
-      s1 += l1;
-      w0[p >> 2] |= (uint32_t)(l0 & 255) << (8 * (p & 3));
-      w1[p >> 2] |= (uint32_t)(l1 & 255) << (8 * (p & 3));
-    }
-    const int kb = row0 / KBR, q = (row0 % KBR) >> 4;
-    uint8_t* blk = bimg + (int64_t)kb * NB * KBR;
-    *reinterpret_cast<uint4*>(blk + sw128_off(2 * b, q, NB)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-    *reinterpret_cast<uint4*>(blk + sw128_off(2 * b + 1, q, NB)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    ired[0][threadIdx.x >> 5] = s0;
-    ired[1][threadIdx.x >> 5] = s1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int a0 = 0, a1 = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      a0 += ired[0][w];
-      a1 += ired[1][w];
-    }
-    Sb[2 * b] = a0;
-    Sb[2 * b + 1] = a1;
-  }
+  unsigned int mb = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mb = max(mb, red[w]);
+  limbs_from_max<BITS>(r, Rpad, B, b, live, nkb, bimg, Fb, Sb, mb, [](const float* p) {
+    return *reinterpret_cast<const float4*>(p);
+  });
 }
 
 static int kb_rows(int bits) {
