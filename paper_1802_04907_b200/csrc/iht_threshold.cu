@@ -1282,7 +1282,10 @@ __device__ void bs_full_select(const int32_t* __restrict__ x_idx, const float* _
       int pos = wc + incl - cnt;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if ((f >> e) & 1u) wl[pos++] = ib + e;
+        if ((f >> e) & 1u) {
+          IHT_DCHECK(wlo + pos < whi, "bounded select: full-select list inside its warp's range");
+          wl[pos++] = ib + e;
+        }
       }
       wc += __shfl_sync(0xffffffffu, incl, 31);
     }
@@ -1294,7 +1297,10 @@ __device__ void bs_full_select(const int32_t* __restrict__ x_idx, const float* _
     if (w == warp) off = total;
     total += wgt[w];
   }
-  for (int j = lane; j < wc; j += 32) gp[off + j] = __ldcg(wl + j);
+  for (int j = lane; j < wc; j += 32) {
+    IHT_DCHECK(off + j < N, "bounded select: packed full-select list inside N");
+    gp[off + j] = __ldcg(wl + j);
+  }
   __syncthreads();
   select_ordered<NT>(total, s, [&](int i) { return __ldcg(ga + __ldcg(gp + i)); }, [&](int i) { return __ldcg(gp + i); },
                      out_idx, out_val, out_nnz_b, 0, hist, scratch, wgt, weq, wtake, wbase, sh);
@@ -1390,6 +1396,7 @@ __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
       }
       if (!in) {
         const int p = atomicAdd(&sh_n, 1);
+        IHT_DCHECK(p < kBsCap, "bounded select: list slot");
         lidx[p] = ci[u];
         lval[p] = cv[u];
         lkey[p] = __float_as_uint(cv[u]) & 0x7FFFFFFFu;
@@ -1442,6 +1449,7 @@ __global__ void __launch_bounds__(kBsThreads, 1) thr_bounded_select(
       }
       if (rk < s) {
         const int p = atomicAdd(&sh_kept, 1);
+        IHT_DCHECK(p < kBsMaxS, "bounded select: kept slot");
         sidx[p] = ii;                           // sidx is free (membership tests done)
         kval[p] = lval[i];
       }
