@@ -264,17 +264,7 @@ __global__ void __launch_bounds__(kBThreads, 1) adjoint_batched_kernel(BatchArgs
                            : "memory");
           }
         };
-        if (a.probe & 512) {
-          // EXPERIMENT (probe 512): every tile-step of the K-block converted into registers
-          // BEFORE waiting for the stage to be free, so only the TMEM stores sit on the
-          // MMA -> converter -> MMA handoff chain
-          uint32_t out[TS][OW];
-#pragma unroll
-          for (int ts = 0; ts < TS; ++ts) convert(ts, out[ts]);
-          if (s_wrapped) mbar_wait2(smem_u32(&st_free[ss]), sph ^ 1u);
-#pragma unroll
-          for (int ts = 0; ts < TS; ++ts) store(ts, out[ts]);
-        } else {
+        {
           // the first tile-step is converted BEFORE waiting for the stage to be free, so only
           // the stores sit on the MMA -> converter -> MMA handoff chain
           uint32_t out[OW];
