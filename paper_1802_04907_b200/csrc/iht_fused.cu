@@ -74,7 +74,7 @@ struct FusedArgs {
   int tl_cta;
   int probe;                           // profiling (IHT_FUSED_PROBE): 1 no MMA work, 2 no refills inside A, 4 no flush
   int nobound;                         // IHT_FUSED_NOBOUND=1: never take the bounded-candidate path (same results)
-  float bound_frac;                    // bound = bound_frac x the previous threshold (IHT_FUSED_BOUND, default 0.9)
+  float bound_frac;                    // bound = bound_frac x the previous threshold (IHT_FUSED_BOUND, default 0.7)
 };
 
 __device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t parity) {
@@ -247,6 +247,14 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       __syncthreads();
     }
     if (tid == 0) a.cand_cnt[cta] = base;
+  };
+  // the CTA histogram (hist_s, zeroed in the limb phase) into the global one, one atomic per
+  // nonzero bin
+  auto add_hist = [&](int par_) {
+    for (int q = tid; q < 2048; q += kFuThreads) {
+      const int v = hist_s[q];
+      if (v) atomicAdd(&a.hist[par_ * 2048 + q], v);
+    }
   };
   for (int n = 1; n <= a.n_iter; ++n) {
     const int par = n & 1;
@@ -576,18 +584,16 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       __syncthreads();
       // the CTA's histogram in shared memory first (the union region: V sums are consumed),
       // then one global atomic per nonzero bin -- the keys crowd a few dozen 1/8-octave bins,
-      // and per-element global atomics on them serialised at L2 (and delayed the barrier)
+      // and per-element global atomics on them serialised at L2 (and delayed the barrier).
+      // With a bound the histogram is not needed unless the bound misses (S1 builds it then)
       int nan = 0;
       for (int q = tid; q < ncol; q += kFuThreads) {
         const unsigned int key = __float_as_uint(as[q]) & 0x7FFFFFFFu;
         nan |= key > 0x7F800000u;
-        atomicAdd(&hist_s[key >> 20], 1);
+        if (!bkey) atomicAdd(&hist_s[key >> 20], 1);
       }
       nan = __syncthreads_or(nan);
-      for (int q = tid; q < 2048; q += kFuThreads) {
-        const int v = hist_s[q];
-        if (v) atomicAdd(&a.hist[par * 2048 + q], v);
-      }
+      if (!bkey) add_hist(par);
       if (tid == 0 && nan) atomicOr(&a.flags[par], 1);
     }
     if (bkey) write_cands([&](unsigned int key) { return key >= bkey; });
@@ -601,35 +607,48 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
       if (tid == 0) a.flags[par ^ 1] = 0;
     }
     if (tid == 0) s_flag = __ldcg(&a.flags[par]);
-    {
-      int hv[2048 / kFuThreads];                                  // every load in flight at once
-#pragma unroll
-      for (int u = 0; u < 2048 / kFuThreads; ++u) hv[u] = __ldcg(&a.hist[par * 2048 + tid + u * kFuThreads]);
-#pragma unroll
-      for (int u = 0; u < 2048 / kFuThreads; ++u) hist_s[tid + u * kFuThreads] = hv[u];
-    }
-    __syncthreads();
     const bool all = a.s >= a.N;
     unsigned int d1 = 0;
     int above = 0;
-    if (!all && !s_flag && a.s > 0) {
-      find_bin<kFuThreads>(hist_s, 2048, a.s, &sh[0], &sh[1], scratch);
-      d1 = (unsigned int)sh[0];
-      above = sh[1];
-    }
     int* cnt_s = sel_hist;                                        // [G + 1] candidate offsets (S2)
     bool fast = false;
-    if (bkey && !all && !s_flag && a.s > 0 && bkey <= (d1 << 20)) {
+    if (bkey) {
+      // the candidates are exactly the keys >= bkey (x's support included: as[] holds a); if
+      // at least s of them exist, the s-th largest key is >= bkey and every entry of H_s(a),
+      // ties included, is a candidate: S2 selects from them alone (d1 from their histogram)
       for (int c = tid; c < G; c += kFuThreads) cnt_s[c] = __ldcg(&a.cand_cnt[c]);
       __syncthreads();
       int tot = 0;
       for (int c = lane; c < G; c += 32) tot += cnt_s[c];
       tot = __reduce_add_sync(0xffffffffu, tot);
-      fast = tot <= kFuCandCap;                                   // same on every CTA
+      fast = !s_flag && tot >= a.s && tot <= kFuCandCap;         // same on every CTA
       __syncthreads();
+      if (!fast && !s_flag) {                                     // the bound missed: the histogram
+        if (T > 0) {                                              // the A phase skipped
+          for (int q = tid; q < ncol; q += kFuThreads) atomicAdd(&hist_s[(__float_as_uint(as[q]) & 0x7FFFFFFFu) >> 20], 1);
+          __syncthreads();
+          add_hist(par);
+        }
+        grid_sync();                                              // ---- barrier 2b: histogram complete
+      }
     }
-    if (!fast) write_cands([&](unsigned int key) { return all || (key >> 20) >= d1; });
-    (void)above;
+    if (!fast) {
+      {
+        int hv[2048 / kFuThreads];                                // every load in flight at once
+#pragma unroll
+        for (int u = 0; u < 2048 / kFuThreads; ++u) hv[u] = __ldcg(&a.hist[par * 2048 + tid + u * kFuThreads]);
+        __syncthreads();                                          // hist_s may still be read above
+#pragma unroll
+        for (int u = 0; u < 2048 / kFuThreads; ++u) hist_s[tid + u * kFuThreads] = hv[u];
+      }
+      __syncthreads();
+      if (!all && !s_flag && a.s > 0) {
+        find_bin<kFuThreads>(hist_s, 2048, a.s, &sh[0], &sh[1], scratch);
+        d1 = (unsigned int)sh[0];
+        above = sh[1];
+      }
+      write_cands([&](unsigned int key) { return all || (key >> 20) >= d1; });
+    }
     stamp(n, 7);
     if (!fast) grid_sync();                                       // ---- barrier 3: candidates complete
     stamp(n, 8);
@@ -700,6 +719,15 @@ __global__ void __launch_bounds__(kFuThreads, 1) fused_iht_kernel(FusedArgs a) {
         }
       }
       __syncthreads();
+      if (fast) {                                                 // bin d1 and the count above it,
+        for (int q = tid; q < 2048; q += kFuThreads) hsel[q] = 0; // from the candidates' keys
+        __syncthreads();
+        for (int q = tid; q < C; q += kFuThreads) atomicAdd(&hsel[(__float_as_uint(cv_s[q]) & 0x7FFFFFFFu) >> 20], 1);
+        __syncthreads();
+        find_bin<kFuThreads>(hsel, 2048, a.s, &sh[0], &sh[1], scratch);   // C >= s
+        d1 = (unsigned int)sh[0];
+        above = sh[1];
+      }
       // ordered block compaction of the staged candidates whose flag is set -> (dst_i, dst_v)
       auto compact = [&](auto flag, int32_t* di, float* dv) {
         int base = 0;
@@ -988,7 +1016,8 @@ int iht_fused_create(const iht_qmat* pool, int K, int s, int n_iter, float mu, i
   A.trace = trace;
   A.probe = getenv("IHT_FUSED_PROBE") ? atoi(getenv("IHT_FUSED_PROBE")) : 0;   // profiling only
   A.nobound = getenv("IHT_FUSED_NOBOUND") ? atoi(getenv("IHT_FUSED_NOBOUND")) : 0;
-  A.bound_frac = getenv("IHT_FUSED_BOUND") ? (float)atof(getenv("IHT_FUSED_BOUND")) : 0.9f;
+  // 0.7 (r02 g65, count criterion): config 2 63.1k iter/s (0.9: 62.1k, 0.5: 56.9k), config 3 37.9k
+  A.bound_frac = getenv("IHT_FUSED_BOUND") ? (float)atof(getenv("IHT_FUSED_BOUND")) : 0.7f;
   if (getenv("IHT_FUSED_TL")) {        // profiling only: per-phase globaltimer stamps of one CTA
     A.tl_cta = atoi(getenv("IHT_FUSED_TL"));
     if (A.tl_cta >= G) A.tl_cta = 0;
