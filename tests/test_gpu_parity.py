@@ -436,10 +436,11 @@ def test_free_running_solver(case, graph, fused):
 
 @pytest.mark.parametrize("case", ["config1", "gauss2bit", "radio", "gauss8bit", "splitk"])
 def test_fused_bounded_candidates_bit_identical(case, capfd, monkeypatch):
-    """The fused solver's bounded-candidate select (candidates = keys >= half the previous
-    threshold, written before barrier 2; S1 and barrier 3 skipped when bin d1 lies above the
-    bound) is exact: every iterate is bit-identical to the unbounded path (IHT_FUSED_NOBOUND=1),
-    and the bounded path is actually taken (phase timeline: barrier 3 skipped)."""
+    """The fused solver's bounded-candidate select (candidates = keys >= 0.7 x the previous
+    threshold, written before barrier 2; when at least s of them exist, the histogram, S1 and
+    barrier 3 are skipped and S2 selects from them alone) is exact: every iterate is
+    bit-identical to the unbounded path (IHT_FUSED_NOBOUND=1), and the bounded path is actually
+    taken (phase timeline: barrier 3 skipped)."""
     p = CASES[case]()
     n_iter = min(p.n_iter, 40)
     c = OQ.scale_c(p.phi)
