@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5, 6],
+                    help="BASELINE configs 1-5; 6 = the paper's P:534 imaging shape (M 900, N 65536)")
     ap.add_argument("--bits", type=int, default=None, help="override b_Phi (2/4/8 sweep)")
     ap.add_argument("--K", type=int, default=None, help="pool of quantised copies")
     ap.add_argument("--variant", type=int, default=0, help="adjoint: 0 int8 MMA, 1 FFMA")

@@ -5,7 +5,9 @@ iterate x^[n+1] is compared with the float64 oracle's, up to the oracle's first 
 * config 2 (4096 x 16384 real Gaussian, 2-bit): all 200 iterations with K = 2 copies, and the
   first 10 iterations with the bench's K = 400 (copies 0..19, i.e. exact Algorithm 1);
 * config 3 (2304 x 65536 complex radio, 2-bit, single observation): 20 iterations, K = 2;
-* config 5 (the radio Phi, batched tcgen05 path): 8 snapshots, 20 iterations, K = 2.
+* config 5 (the radio Phi, batched tcgen05 path): 8 snapshots, 20 iterations, K = 2;
+* config 6 (the paper's own imaging shape: 900 x 65536 complex radio, 30 sources,
+  SNR 0 dB, 2-bit): all 200 iterations with K = 2, and the first 10 with the bench's K = 400.
 
 Bar: identical supports and x within 1e-4 relative l2 (1e-3 on the tensor-core path) in
 every compared iteration, no escape; a final support identical to the oracle's whenever no
@@ -191,3 +193,40 @@ def test_config5_8_snapshots_20_iterations(radio_oracle):
     # never vacuous: at least half the snapshots run clean to the end and at least half of all
     # snapshot-iterations are compared (oracle near-ties at 1e-3: snapshots 1, 4, 7 at n = 9, 5, 1)
     assert clean >= B // 2 and total >= B * n_iter // 2, (clean, total)
+
+
+# ------------------------------------------------------------------------------ config 6
+@pytest.fixture(scope="module")
+def paper_problem():
+    p = G.config_problem(6, K=2)
+    assert (p.M, p.N, p.s) == (900, 65536, 30)
+    return p, OQ.scale_c(p.phi)
+
+
+def test_config6_all_200_iterations_K2(paper_problem):
+    """The paper's imaging shape free-running for the whole n* loop on the fused solver."""
+    p, c_ref = paper_problem
+    pool, c, _, _, _ = build_pool(p, 0, 1, _dev(), False)
+    assert np.float32(c) == c_ref
+    (idx, val, nnz), final = _run_gpu(pool, p, p.n_iter, p.y)
+    del pool
+    torch.cuda.empty_cache()
+    opool = _CodesPool(p.phi, p.b_phi, p.seed, c_ref, oracle_codes(p.phi, p.b_phi, p.seed, [0, 1], c_ref))
+    ref = OI.qniht(p.phi, p.y, p.s, p.n_iter, p.mu, p.b_phi, p.b_y, p.seed, 2, record=True, pool=opool)
+    checked = _check(ref, idx, val, nnz, (final[0], final[1], final[2][0]), p.s, TOL, 100)
+    print(f"config 6, K = 2: {checked}/{p.n_iter} iterations identical")
+
+
+def test_config6_first_10_iterations_K400(paper_problem):
+    p, c_ref = paper_problem
+    p = G.config_problem(6)                     # K = 2 n* = 400, the bench's pool
+    pool, c, _, _, _ = build_pool(p, 0, 1, _dev(), False)
+    n_iter = 10
+    (idx, val, nnz), final = _run_gpu(pool, p, n_iter, p.y)
+    del pool
+    torch.cuda.empty_cache()
+    opool = _CodesPool(p.phi, p.b_phi, p.seed, c_ref,
+                       oracle_codes(p.phi, p.b_phi, p.seed, list(range(2 * n_iter)), c_ref))
+    ref = OI.qniht(p.phi, p.y, p.s, n_iter, p.mu, p.b_phi, p.b_y, p.seed, p.K, record=True, pool=opool)
+    assert [r.adj_copy for r in ref.trace] == list(range(0, 2 * n_iter, 2))     # exact Algorithm 1
+    _check(ref, idx, val, nnz, (final[0], final[1], final[2][0]), p.s, TOL, n_iter)

@@ -56,3 +56,19 @@ def test_config_steps_follow_reading_c9():
     assert p.mu == 0.1 / p.M
     q = G.gaussian_problem(64, 128, 4, cfg_id=98, n_iter=2, mu=0.25, K=2)
     assert q.mu == 0.25
+
+
+def test_config6_is_the_paper_imaging_shape_at_0dB():
+    """Config 6 = the paper's imaging experiment shape: y in C^900, Phi-hat in
+    C^{900 x 65536} (30 antennas, 256 x 256 pixels), 30 sources, SNR 0 dB at the antenna level,
+    10 log10(||Phi x||^2 / ||e||^2) = 0 -- here within the chi-square spread of 900 complex
+    noise draws (+-0.3 dB, > 4 standard deviations)."""
+    c = G.CONFIGS[6]
+    assert (c["A"] ** 2, c["grid"] ** 2, c["n_src"], c["b_phi"], c["b_y"]) == (900, 65536, 30, 2, 8)
+    p = G.config_problem(6, K=2)
+    assert (p.M, p.N, p.s, p.complex) == (900, 65536, 30, True)
+    vis = p.phi[:, p.x_idx].astype(np.complex128) @ p.x_val
+    e = p.y.astype(np.complex128) - vis
+    snr_db = 10 * np.log10(np.sum(np.abs(vis) ** 2) / np.sum(np.abs(e) ** 2))
+    assert abs(snr_db) < 0.3, snr_db
+    assert 15e6 <= 299792458.0 / p.meta["wavelength"] <= 80e6      # the low band, P:534

@@ -242,11 +242,20 @@ CONFIGS = {
     3: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8),
     4: dict(kind="gauss", M=65536, N=262144, s=1024, values="normal", n_iter=100, b_phi=4, b_y=8),
     5: dict(kind="radio", A=48, grid=256, n_src=64, n_iter=200, b_phi=2, b_y=8, batch=64, phi_cfg_id=3),
+    # config 6 (not a BASELINE config): the paper's own imaging experiment shape, P:534 -- 30
+    # low-band antennas (M = 900), a 256 x 256 sky (N = 65536), 30 strong sources, SNR 0 dB at
+    # the antenna level (||Phi x||^2 = ||e||^2: noise_frac = 1), 2-bit Phi, 8-bit y.  The LOFAR
+    # CS302 layout and sky are data we do not have: synthetic antennas in a 40 m-radius disc at
+    # 60 MHz (inside the 15-80 MHz band), log-normal fluxes; n* = 200 (not stated).
+    # mu = 1/(20 M): at 0 dB the oracle's iterates diverge at 0.1/M and 0.3/M (|x| ~ 1e28 /
+    # 1e151 by iteration 199) and stay bounded at 0.05/M (|x| ~ 5.1 from iteration 50 on).
+    6: dict(kind="radio", A=30, grid=256, n_src=30, n_iter=200, b_phi=2, b_y=8, noise_frac=1.0,
+            radius_m=40.0, freq_hz=60e6, mu_scale=0.05),
 }
 
 
 def config_problem(cfg_id, K=None, materialize=None, b_phi=None):
-    """Build BASELINE config cfg_id (1..5).  K defaults to 2 n* where that fits
+    """Build BASELINE config cfg_id (1..5; 6 = the paper's P:534 imaging shape).  K defaults to 2 n* where that fits
     (configs 1-3, 5) and 2 for config 4 (reading c6)."""
     c = dict(CONFIGS[cfg_id])
     kind = c.pop("kind")
@@ -264,4 +273,5 @@ def config_problem(cfg_id, K=None, materialize=None, b_phi=None):
         K = 2 * c["n_iter"]
     return radio_problem(cfg_id=cfg_id, A=c["A"], grid=c["grid"], n_src=c["n_src"],
                          n_iter=c["n_iter"], b_phi=c["b_phi"], b_y=c["b_y"], K=K,
-                         batch=c.get("batch", 1), name=f"config{cfg_id}", phi_cfg_id=c.get("phi_cfg_id"))
+                         batch=c.get("batch", 1), name=f"config{cfg_id}", phi_cfg_id=c.get("phi_cfg_id"),
+                         **{k: c[k] for k in ("noise_frac", "radius_m", "freq_hz", "mu_scale") if k in c})
