@@ -503,12 +503,16 @@ def main():
     # ---- bookkeeping --------------------------------------------------------------------
     peak, peak_kind = measured_peaks()
     ncols = pool.desc.cols if args.fresh else pool[0].cols     # this rank's columns
-    strip = iht.strip_bytes(rows, p.planes, p.b_phi)
-    copy_bytes = iht._lib.load().iht_qmat_bytes(rows, ncols, p.planes, p.b_phi)
+    # algorithmic bytes count the method's codes only: the layout's pad rows (rows rounded up
+    # to 256 per plane, e.g. 900 -> 1024 at config 6) are streamed but are not the method's
+    # bytes (layout_copy_bytes below reports them)
+    strip = (rows * p.planes * p.b_phi + 7) // 8
+    layout_copy_bytes = iht._lib.load().iht_qmat_bytes(rows, ncols, p.planes, p.b_phi)
+    copy_bytes = (rows * p.planes * ncols * p.b_phi + 7) // 8
     if args.fresh:          # the adjoint streams the fp32 Phi (4 bytes per component), the forward s columns
         copy_bytes = 4 * rows * ncols * p.planes
         strip = 4 * rows * p.planes
-    R = iht.vec_len(rows, p.planes)
+    R = rows * p.planes
     adj_bytes = copy_bytes + B * (4 * R + 4 * ncols)          # codes + r read + g write
     fwd_bytes = B * (p.s * strip + 4 * R + 4 * R)              # support strips + yhat + r
     thr_bytes = B * (4 * ncols * 2 + 8 * p.s)                  # g read + a write (+ x)
@@ -564,6 +568,7 @@ def main():
                       "achieved": iter_bytes / (adj_avg / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                       "frac": iter_bytes / (adj_avg / 1e3) / 1e9 / peak, "peak_kind": peak_kind, "traffic": traffic,
                       "algorithmic_bytes_per_launch": iter_bytes * p.n_iter, "avg_launch_ms": adj_avg * p.n_iter,
+                      "layout_copy_bytes": layout_copy_bytes, "code_bytes_per_copy": copy_bytes,
                       "launches_timed": len(adj_ms) // max(p.n_iter, 1),
                       "how": "CUDA event pair around the fused kernel inside a profiled copy of the solver graph "
                              "(run after the timed region); achieved = algorithmic bytes of one iteration (adjoint "
