@@ -16,7 +16,7 @@
 //
 // K order inside a 16-byte u8 chunk is permuted (row(p) below) identically on A and B.
 //
-// Roles per CTA (320 threads): warps 0-3 expand packed codes -> u8 A stages in TMEM
+// Roles per CTA (352 threads = 11 warps): warps 0-3 expand packed codes -> u8 A stages in TMEM
 // (tcgen05.st); warp 4 issues the MMAs (one thread); warp 5 bulk-copies the packed codes
 // (own ring of slots), warp 6 the r-limb image; warps 7-10 run the epilogue.
 // A (TMEM) and B (shared memory) share ONE stage ring: a stage is full when the 4 converter
